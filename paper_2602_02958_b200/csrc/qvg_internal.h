@@ -1,0 +1,69 @@
+// qvg_internal.h — declarations shared by the .cu files of libqvg_b200.so.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "../../include/qvg.h"
+
+namespace qvg {
+
+int set_err(int code, const char *fmt, ...);
+
+struct PlaneState {
+    double prev;
+    double obj;
+    int32_t done;
+    int32_t iters;
+};
+
+struct KMeansBuffers {
+    double *rows, *cent, *d2, *nodes;
+    int32_t *assign, *counts, *offsets, *members;
+    PlaneState *st;
+    int64_t *pk_off;
+    int32_t *pk_len;
+    int pk_leaves;
+    int64_t *ob_off;
+    int32_t *ob_len, *nd_l, *nd_r, *h_start;
+    int ob_leaves, ob_heights;
+};
+
+// qvg_codec.cu
+int launch_quantize(const void *x, int xdtype, int64_t P, int64_t N, int d, int bits, int B, int S,
+                    int K, const uint16_t *cent, const uint8_t *asg, uint8_t *payload,
+                    uint8_t *scales, int32_t *status, cudaStream_t st);
+int launch_dequantize(const uint8_t *payload, const uint8_t *scales, const uint16_t *cent,
+                      const uint8_t *asg, int64_t P, int64_t N, int d, int bits, int B, int S, int K,
+                      void *out, int odtype, int32_t *status, cudaStream_t st);
+
+int launch_pack(const int8_t *q, int64_t n, int bits, uint8_t *out, int32_t *status, cudaStream_t st);
+int launch_unpack(const uint8_t *in, int64_t n, int bits, int8_t *out, cudaStream_t st);
+
+// qvg_kmeans.cu
+int launch_widen(const void *x, int xbf16, double *rows, int64_t n, int32_t *status, cudaStream_t st);
+int run_kmeanspp(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, const double *draws,
+                 int64_t draws_stride, cudaStream_t st);
+int run_kmeans_stage(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int max_iters,
+                     double tol, const double *draws_stage, int64_t draws_stride, bool warm,
+                     cudaStream_t st);
+int kmeans_outputs(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, uint8_t *assign,
+                   double *objective, int32_t *iters, cudaStream_t st);
+int lloyd_once(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, uint8_t *assign,
+               double *objective, cudaStream_t st);
+int run_assign(const double *rows, const double *cent, int32_t *assign, int64_t P, int64_t N, int d,
+               int K, cudaStream_t st);
+int finalize_stage(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int S, int t,
+                   uint16_t *cent_out, double *cent64_out, uint8_t *assign_out, int32_t *iters_out,
+                   cudaStream_t st);
+int run_add_back(const double *residual, const uint16_t *cent, const uint8_t *assign, int64_t P,
+                 int64_t N, int d, int K, double *out, cudaStream_t st);
+
+// qvg_attn.cu
+size_t attention_workspace_size(int64_t nq, int64_t n_cache, int64_t n_cur, int H, int d,
+                                const qvg_config *cfg);
+int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scales,
+                  const uint16_t *cent, const uint8_t *assign, const uint16_t *kv_bf16,
+                  const uint16_t *k_cur, const uint16_t *v_cur, int64_t nq, int64_t n_cache,
+                  int64_t n_cur, int H, int d, const qvg_config *cfg, float scale, uint16_t *out,
+                  void *workspace, size_t wbytes, cudaStream_t st);
+
+}  // namespace qvg

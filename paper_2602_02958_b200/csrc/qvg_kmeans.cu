@@ -1,0 +1,735 @@
+// qvg_kmeans.cu — Semantic-Aware Smoothing on sm_100a: deterministic Lloyd
+// k-means (Q/clustering.py) reproduced bit for bit on the GPU.
+//
+//  K1 k_kmeanspp        k-means++ seeding, one CTA per plane (Q/clustering.py:47-63);
+//                       the sequential-cumsum inverse-CDF pick is decided from a
+//                       parallel prefix with a rigorous error certificate, with an
+//                       exact sequential fallback when the certificate fails.
+//  K2 k_assign          distance GEMM (fp64 FMA chain in k order, as OpenBLAS
+//                       dgemm) fused with c2 = pairwise(C^2) and first-min argmin
+//                       (Q/clustering.py:66-71).
+//  K3 k_members/k_sums  stable counting sort of rows by cluster, then one ordered
+//                       fp64 chain per (cluster, channel) = np.add.at, divide,
+//                       keep-old for empties (Q/clustering.py:89-95);
+//     k_repair          farthest-row empty-cluster repair (Q/clustering.py:97-104).
+//  K4 k_obj_leaves /    numpy pairwise flat sum of the SSE (Q/clustering.py:106,
+//     k_obj_combine     143) over a host-built copy of numpy's recursion tree, and
+//                       the tol test (Q/clustering.py:148-151) on device.
+// Every kernel reads a per-plane `done` flag, so one launch sequence of
+// max_iters Lloyd steps serves planes that converge at different iterations.
+#include <cstdio>
+#include "qvg_common.cuh"
+#include "qvg_internal.h"
+
+namespace qvg {
+
+// ---- pairwise over one row of d <= 128 values, 8 lanes per row ----------
+// v(k) supplies element k.  Result valid in every lane of the 8-lane group.
+template <typename F>
+__device__ __forceinline__ double row_pairwise8(int d, int j, F v) {
+    if (d < 8) {
+        double s = 0.0;
+        for (int k = 0; k < d; k++) s = __dadd_rn(s, v(k));
+        return __shfl_sync(0xffffffffu, s, (threadIdx.x & 31) & ~7);
+    }
+    const int m = d >> 3;
+    double acc = v(j);
+    for (int i = 1; i < m; i++) acc = __dadd_rn(acc, v(i * 8 + j));
+    acc = pairwise8_tree(acc);
+    for (int k = m * 8; k < d; k++) acc = __dadd_rn(acc, v(k));   // tail, all lanes equal
+    return acc;
+}
+
+// numpy pairwise recursion over precomputed leaf sums (leaves in order).
+__device__ double pw_combine(const double *leaf, int64_t n, int &cur) {
+    if (n <= 128) return leaf[cur++];
+    int64_t h = n / 2;
+    h -= h % 8;
+    double a = pw_combine(leaf, h, cur);
+    double b = pw_combine(leaf, n - h, cur);
+    return __dadd_rn(a, b);
+}
+
+// leaf sum of v over [off, off+len), 8 lanes (len <= 128); numpy leaf rule.
+template <typename F>
+__device__ __forceinline__ double leaf_sum8(int64_t off, int len, int j, F v) {
+    if (len < 8) {
+        double s = 0.0;
+        for (int k = 0; k < len; k++) s = __dadd_rn(s, v(off + k));
+        return s;
+    }
+    const int m = len >> 3;
+    double acc = v(off + j);
+    for (int i = 1; i < m; i++) acc = __dadd_rn(acc, v(off + i * 8 + j));
+    acc = pairwise8_tree(acc);
+    for (int k = m * 8; k < len; k++) acc = __dadd_rn(acc, v(off + k));
+    return acc;
+}
+
+// ------------------------------------------------------------------------
+// widen input to the f64 stage-1 rows (plane.data.astype(np.float64)) + NaN scan
+// ------------------------------------------------------------------------
+__global__ void k_widen(const void *x, int xbf16, double *rows, int64_t n, int32_t *status) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        float f = xbf16 ? bf16_to_f32(static_cast<const uint16_t *>(x)[i]) : static_cast<const float *>(x)[i];
+        if (!isfinite(f)) atomicOr(status, QVG_STATUS_NONFINITE);
+        rows[i] = double(f);
+    }
+}
+
+// ------------------------------------------------------------------------
+// K1: k-means++ (one CTA of 1024 threads per plane)
+// ------------------------------------------------------------------------
+struct PPArgs {
+    const double *rows;      // [P][N][d]
+    const double *draws;     // this stage's draws of plane 0; plane p at + p*draws_stride
+    int64_t draws_stride;
+    double *cent;            // [P][K][d]
+    double *d2;              // [P][N]
+    const int64_t *lf_off;   // pick-tree leaves over N
+    const int32_t *lf_len;
+    int n_leaves;
+    int64_t N;
+    int d, K;
+};
+
+__global__ void __launch_bounds__(1024) k_kmeanspp(PPArgs a) {
+    extern __shared__ double sm[];
+    double *xc = sm;                       // [d]
+    double *leaf = sm + 128;               // [n_leaves]
+    __shared__ double s_total;
+    __shared__ int64_t s_pick;
+    __shared__ double s_wsum[32];
+    __shared__ double s_base;
+    const int64_t p = blockIdx.x;
+    const int64_t N = a.N;
+    const int d = a.d, K = a.K;
+    const double *rows = a.rows + p * N * d;
+    double *d2 = a.d2 + p * N;
+    double *cent = a.cent + p * int64_t(K) * d;
+    const double *draws = a.draws + p * a.draws_stride;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int j8 = lane & 7;
+
+    if (tid == 0) {
+        int64_t c = int64_t(draws[0] * double(N));
+        s_pick = c < N - 1 ? c : N - 1;
+    }
+    __syncthreads();
+    for (int pk = 0; pk < K; pk++) {
+        const int64_t c = s_pick;
+        for (int k = tid; k < d; k += blockDim.x) {
+            double v = rows[c * d + k];
+            xc[k] = v;
+            cent[int64_t(pk) * d + k] = v;
+        }
+        __syncthreads();
+        if (pk == K - 1) break;
+        // d2 = min(d2, ((rows - rows[c])**2).sum(axis=1))
+        for (int64_t i0 = int64_t(warp) * 4; i0 < N; i0 += blockDim.x >> 3) {  // warp-uniform
+            const int64_t i = i0 + (lane >> 3);
+            const int64_t ii = i < N ? i : N - 1;
+            const double *ri = rows + ii * d;
+            double dist = row_pairwise8(d, j8, [&](int k) {
+                double t = __dsub_rn(ri[k], xc[k]);
+                return __dmul_rn(t, t);
+            });
+            dist = __dadd_rn(0.0, dist);
+            if (j8 == 0 && i < N) d2[i] = (pk == 0 || dist < d2[i]) ? dist : d2[i];
+        }
+        __syncthreads();
+        // total = weights.sum() : leaves then numpy recursion
+        for (int L0 = warp * 4; L0 < a.n_leaves; L0 += blockDim.x >> 3) {     // warp-uniform
+            const int L = L0 + (lane >> 3);
+            const int LL = L < a.n_leaves ? L : a.n_leaves - 1;
+            double s = leaf_sum8(a.lf_off[LL], a.lf_len[LL], j8, [&](int64_t e) { return d2[e]; });
+            if (j8 == 0 && L < a.n_leaves) leaf[L] = s;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            int cur = 0;
+            s_total = __dadd_rn(0.0, pw_combine(leaf, N, cur));
+        }
+        __syncthreads();
+        const double r = draws[pk + 1];
+        const double total = s_total;
+        if (!(total > 0.0)) {     // uniform fallback (Q/clustering.py:41-42)
+            if (tid == 0) {
+                int64_t i = int64_t(r * double(N));
+                s_pick = i < N - 1 ? i : N - 1;
+            }
+            __syncthreads();
+            continue;
+        }
+        const double target = __dmul_rn(r, total);
+        // searchsorted(cumsum(d2), target, 'right') = #{j : cum_seq[j] <= target}.
+        // cum_seq (sequential f64) and our parallel prefix both lie within
+        // gamma_N * S_j of the exact prefix S_j (all terms >= 0), so a prefix
+        // farther than 2*gamma_N from target decides its element exactly.
+        const double eps = double(2 * N + 64) * 2.220446049250313e-16;
+        int cnt = 0;
+        bool amb = false;
+        if (tid == 0) s_base = 0.0;
+        __syncthreads();
+        for (int64_t b0 = 0; b0 < N; b0 += blockDim.x) {
+            int64_t i = b0 + tid;
+            double v = i < N ? d2[i] : 0.0;
+            double incl = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                double t = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += t;
+            }
+            if (lane == 31) s_wsum[warp] = incl;
+            __syncthreads();
+            if (warp == 0) {
+                double w = s_wsum[lane];
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    double t = __shfl_up_sync(0xffffffffu, w, o);
+                    if (lane >= o) w += t;
+                }
+                s_wsum[lane] = w;   // inclusive warp prefix
+            }
+            __syncthreads();
+            double pre = s_base + (warp ? s_wsum[warp - 1] : 0.0) + incl;
+            bool le = false, am = false;
+            if (i < N) {
+                double m = pre * eps;
+                le = pre + m < target;
+                bool gt = pre - m > target;
+                am = !le && !gt;
+            }
+            cnt += __syncthreads_count(le);
+            amb |= __syncthreads_or(am) != 0;
+            if (tid == 0) s_base = s_base + s_wsum[31];
+            __syncthreads();
+        }
+        if (tid == 0) {
+            int64_t pick;
+            if (!amb) pick = cnt;
+            else {                       // exact sequential cumsum (rare)
+                double cs = 0.0;
+                int64_t i = 0;
+                for (; i < N; i++) {
+                    cs = __dadd_rn(cs, d2[i]);
+                    if (cs > target) break;
+                }
+                pick = i;
+            }
+            s_pick = pick < N - 1 ? pick : N - 1;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------
+// K2: assignment — fp64 FMA-chain distance GEMM fused with argmin
+// ------------------------------------------------------------------------
+constexpr int AR = 64, AC = 64, AK = 32;
+
+struct AssignArgs {
+    const double *rows;
+    const double *cent;
+    int32_t *assign;       // [P][N]
+    const PlaneState *st;
+    int64_t N;
+    int d, K;
+    int skip_done;
+};
+
+__global__ void __launch_bounds__(256) k_assign(AssignArgs a) {
+    const int64_t p = blockIdx.y;
+    if (a.skip_done && a.st[p].done) return;
+    __shared__ double Xs[AR][AK + 1];
+    __shared__ double Cs[AC][AK + 1];
+    __shared__ double c2s[kMaxK];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int d = a.d, K = a.K;
+    const int64_t N = a.N;
+    const double *rows = a.rows + p * N * d;
+    const double *cent = a.cent + p * int64_t(K) * d;
+    const int64_t r0 = int64_t(blockIdx.x) * AR;
+
+    // c2 = (centroids ** 2).sum(axis=1), numpy pairwise per centroid
+    for (int c0 = (tid >> 5) * 4; c0 < K; c0 += 32) {          // warp-uniform trip count
+        const int c = c0 + ((tid & 31) >> 3);
+        const double *cc = cent + int64_t(c < K ? c : K - 1) * d;
+        double s = row_pairwise8(d, tid & 7, [&](int k) { return __dmul_rn(cc[k], cc[k]); });
+        if ((tid & 7) == 0 && c < K) c2s[c] = __dadd_rn(0.0, s);
+    }
+    double bv[4];
+    int bj[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) { bv[i] = 0.0; bj[i] = -1; }
+
+    for (int c0 = 0; c0 < K; c0 += AC) {
+        double acc[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; i++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) acc[i][j] = 0.0;
+        for (int k0 = 0; k0 < d; k0 += AK) {
+            __syncthreads();
+            for (int e = tid; e < AR * AK; e += 256) {
+                int rr = e / AK, kk = e % AK;
+                int64_t row = r0 + rr;
+                Xs[rr][kk] = (row < N && k0 + kk < d) ? rows[row * d + k0 + kk] : 0.0;
+                int cc = c0 + rr;
+                Cs[rr][kk] = (cc < K && k0 + kk < d) ? cent[int64_t(cc) * d + k0 + kk] : 0.0;
+            }
+            __syncthreads();
+            const int kmax = min(AK, d - k0);
+            for (int kk = 0; kk < kmax; kk++) {
+                double xv[4], cv[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) xv[i] = Xs[ty + 16 * i][kk];
+#pragma unroll
+                for (int j = 0; j < 4; j++) cv[j] = Cs[tx + 16 * j][kk];
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+#pragma unroll
+                    for (int j = 0; j < 4; j++) acc[i][j] = __fma_rn(xv[i], cv[j], acc[i][j]);
+            }
+        }
+        // D = c2 - 2*cross; first minimum (np.argmin)
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            int cj = c0 + tx + 16 * j;
+            if (cj >= K) continue;
+            double c2 = c2s[cj];
+#pragma unroll
+            for (int i = 0; i < 4; i++) {
+                double D = __dsub_rn(c2, __dmul_rn(2.0, acc[i][j]));
+                if (bj[i] < 0 || D < bv[i]) { bv[i] = D; bj[i] = cj; }
+            }
+        }
+    }
+    // reduce over the 16 tx lanes: lexicographic (value, index)
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        double v = bv[i];
+        int j = bj[i];
+#pragma unroll
+        for (int m = 1; m < 16; m <<= 1) {
+            double ov = __shfl_xor_sync(0xffffffffu, v, m);
+            int oj = __shfl_xor_sync(0xffffffffu, j, m);
+            bool take = oj >= 0 && (j < 0 || ov < v || (ov == v && oj < j));
+            if (take) { v = ov; j = oj; }
+        }
+        int64_t row = r0 + ty + 16 * i;
+        if (tx == 0 && row < N) a.assign[p * N + row] = j;
+    }
+}
+
+// ------------------------------------------------------------------------
+// K3a: stable counting sort of rows by cluster (one CTA of 1024 per plane)
+// ------------------------------------------------------------------------
+struct MemberArgs {
+    const int32_t *assign;
+    int32_t *counts;       // [P][K]
+    int32_t *offsets;      // [P][K+1]
+    int32_t *members;      // [P][N]
+    const PlaneState *st;
+    int64_t N;
+    int K;
+};
+
+__global__ void __launch_bounds__(1024) k_members(MemberArgs a) {
+    const int64_t p = blockIdx.x;
+    if (a.st[p].done) return;
+    extern __shared__ int32_t smi[];
+    const int K = a.K;
+    int32_t *cnt = smi;                 // [K]
+    int32_t *base = smi + K;            // [K]
+    int32_t *wcnt = smi + 2 * K;        // [32][K]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t N = a.N;
+    const int32_t *asg = a.assign + p * N;
+    int32_t *mem = a.members + p * N;
+    for (int j = tid; j < K; j += blockDim.x) cnt[j] = 0;
+    for (int j = tid; j < 32 * K; j += blockDim.x) wcnt[j] = 0;
+    __syncthreads();
+    for (int64_t i = tid; i < N; i += blockDim.x) atomicAdd(&cnt[asg[i]], 1);
+    __syncthreads();
+    if (tid == 0) {
+        int run = 0;
+        for (int j = 0; j < K; j++) {
+            a.counts[p * K + j] = cnt[j];
+            a.offsets[p * (K + 1) + j] = run;
+            base[j] = run;
+            run += cnt[j];
+        }
+        a.offsets[p * (K + 1) + K] = run;
+    }
+    __syncthreads();
+    const unsigned lt = (1u << lane) - 1u;
+    for (int64_t b0 = 0; b0 < N; b0 += blockDim.x) {
+        const int64_t i = b0 + tid;
+        const int c = i < N ? asg[i] : -1;
+        const unsigned same = __match_any_sync(0xffffffffu, c);
+        const int rank = __popc(same & lt);
+        if (c >= 0 && rank == 0) wcnt[warp * K + c] = __popc(same);
+        __syncthreads();
+        for (int j = tid; j < K; j += blockDim.x) {     // per-cluster prefix over warps
+            int run = base[j];
+            for (int w = 0; w < 32; w++) {
+                int t = wcnt[w * K + j];
+                wcnt[w * K + j] = run;
+                run += t;
+            }
+            base[j] = run;
+        }
+        __syncthreads();
+        if (c >= 0) mem[wcnt[warp * K + c] + rank] = int32_t(i);
+        __syncthreads();
+        for (int j = tid; j < 32 * K; j += blockDim.x) wcnt[j] = 0;
+        __syncthreads();
+    }
+}
+
+// K3b: per (cluster, channel) ordered sums = np.add.at, then / count.
+struct SumArgs {
+    const double *rows;
+    double *cent;
+    const int32_t *counts, *offsets, *members;
+    const PlaneState *st;
+    int64_t N;
+    int d, K;
+};
+
+__global__ void __launch_bounds__(128) k_sums(SumArgs a) {
+    const int64_t p = blockIdx.y;
+    const int j = blockIdx.x;
+    if (a.st[p].done) return;
+    const int K = a.K, d = a.d;
+    const int cnt = a.counts[p * K + j];
+    if (cnt == 0) return;                         // keep the old centroid
+    const int32_t *mem = a.members + p * a.N + a.offsets[p * (K + 1) + j];
+    const double *rows = a.rows + p * a.N * d;
+    for (int k = threadIdx.x; k < d; k += blockDim.x) {
+        double acc = 0.0;
+        int t = 0;
+        for (; t + 8 <= cnt; t += 8) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) v[u] = rows[int64_t(mem[t + u]) * d + k];
+#pragma unroll
+            for (int u = 0; u < 8; u++) acc = __dadd_rn(acc, v[u]);
+        }
+        for (; t < cnt; t++) acc = __dadd_rn(acc, rows[int64_t(mem[t]) * d + k]);
+        a.cent[(p * K + j) * int64_t(d) + k] = __ddiv_rn(acc, double(cnt));
+    }
+}
+
+// K3c: empty-cluster repair (one CTA of 1024 per plane; returns at once when
+// no cluster is empty, the common case).
+struct RepairArgs {
+    const double *rows;
+    double *cent;
+    int32_t *assign;
+    const int32_t *counts;
+    double *dist;          // [P][N] scratch
+    const PlaneState *st;
+    int64_t N;
+    int d, K;
+};
+
+__global__ void __launch_bounds__(1024) k_repair(RepairArgs a) {
+    const int64_t p = blockIdx.x;
+    if (a.st[p].done) return;
+    const int K = a.K, d = a.d;
+    const int64_t N = a.N;
+    const int32_t *cnt = a.counts + p * K;
+    int any = 0;
+    for (int j = threadIdx.x; j < K; j += blockDim.x) any |= cnt[j] == 0;
+    if (!__syncthreads_or(any)) return;
+    const double *rows = a.rows + p * N * d;
+    double *cent = a.cent + p * int64_t(K) * d;
+    int32_t *asg = a.assign + p * N;
+    double *dist = a.dist + p * N;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, j8 = lane & 7;
+    for (int64_t i0 = int64_t(warp) * 4; i0 < N; i0 += blockDim.x >> 3) {    // warp-uniform
+        const int64_t i = i0 + (lane >> 3);
+        const int64_t ii = i < N ? i : N - 1;
+        const double *ri = rows + ii * d;
+        const double *ci = cent + int64_t(asg[ii]) * d;
+        double s = row_pairwise8(d, j8, [&](int k) {
+            double t = __dsub_rn(ri[k], ci[k]);
+            return __dmul_rn(t, t);
+        });
+        if (j8 == 0 && i < N) dist[i] = __dadd_rn(0.0, s);
+    }
+    __syncthreads();
+    __shared__ double wv[32];
+    __shared__ int64_t wi[32];
+    __shared__ int64_t s_r;
+    for (int j = 0; j < K; j++) {
+        if (cnt[j] != 0) continue;
+        double bv = -1.0 / 0.0;
+        int64_t bi = -1;
+        for (int64_t i = tid; i < N; i += blockDim.x) {
+            double v = dist[i];
+            if (bi < 0 || v > bv) { bv = v; bi = i; }
+        }
+        for (int m = 1; m < 32; m <<= 1) {
+            double ov = __shfl_xor_sync(0xffffffffu, bv, m);
+            int64_t oi = __shfl_xor_sync(0xffffffffu, bi, m);
+            if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) { bv = ov; bi = oi; }
+        }
+        if (lane == 0) { wv[warp] = bv; wi[warp] = bi; }
+        __syncthreads();
+        if (tid == 0) {
+            double v = wv[0];
+            int64_t r = wi[0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); w++)
+                if (wi[w] >= 0 && (r < 0 || wv[w] > v || (wv[w] == v && wi[w] < r))) { v = wv[w]; r = wi[w]; }
+            s_r = r;
+            asg[r] = j;
+            dist[r] = -1.0;
+        }
+        __syncthreads();
+        const int64_t r = s_r;
+        for (int k = tid; k < d; k += blockDim.x) cent[int64_t(j) * d + k] = rows[r * d + k];
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------
+// K4: objective = ((rows - cent[assign])**2).sum() (flat numpy pairwise)
+// ------------------------------------------------------------------------
+struct ObjArgs {
+    const double *rows;
+    const double *cent;
+    const int32_t *assign;
+    double *nodes;            // [P][n_nodes]
+    PlaneState *st;
+    const int64_t *lf_off;
+    const int32_t *lf_len;
+    const int32_t *nd_l, *nd_r, *h_start;
+    int n_leaves, n_heights;
+    int64_t N;
+    int d, K;
+    int mode;                 // 0: initial objective -> prev; 1: Lloyd step + tol test; 2: objective only
+    double tol;
+};
+
+__global__ void __launch_bounds__(256) k_obj_leaves(ObjArgs a) {
+    const int64_t p = blockIdx.y;
+    if (a.mode == 1 && a.st[p].done) return;
+    const int d = a.d;
+    const double *rows = a.rows + p * a.N * d;
+    const double *cent = a.cent + p * int64_t(a.K) * d;
+    const int32_t *asg = a.assign + p * a.N;
+    const int n_nodes = 2 * a.n_leaves - 1;
+    const int j8 = threadIdx.x & 7;
+    const int64_t wg = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;   // global warp
+    const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t L0 = wg * 4; L0 < a.n_leaves; L0 += nw * 4) {                // warp-uniform
+        const int64_t L = L0 + ((threadIdx.x & 31) >> 3);
+        const int64_t LL = L < a.n_leaves ? L : a.n_leaves - 1;
+        double s = leaf_sum8(a.lf_off[LL], a.lf_len[LL], j8, [&](int64_t e) {
+            int64_t row = e / d;
+            int col = int(e - row * d);
+            double t = __dsub_rn(rows[e], cent[int64_t(asg[row]) * d + col]);
+            return __dmul_rn(t, t);
+        });
+        if (j8 == 0 && L < a.n_leaves) a.nodes[p * n_nodes + L] = s;
+    }
+}
+
+__global__ void __launch_bounds__(1024) k_obj_combine(ObjArgs a) {
+    const int64_t p = blockIdx.x;
+    if (a.mode == 1 && a.st[p].done) return;
+    const int nl = a.n_leaves;
+    double *nodes = a.nodes + p * (2 * nl - 1);
+    for (int h = 0; h < a.n_heights; h++) {
+        for (int i = a.h_start[h] + threadIdx.x; i < a.h_start[h + 1]; i += blockDim.x)
+            nodes[nl + i] = __dadd_rn(nodes[a.nd_l[i]], nodes[a.nd_r[i]]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double obj = __dadd_rn(0.0, nodes[nl > 1 ? 2 * nl - 2 : 0]);
+        PlaneState &s = a.st[p];
+        s.obj = obj;
+        if (a.mode == 0) {
+            s.prev = obj;
+        } else if (a.mode == 2) {
+            // objective only (kmeans result / lloyd_step return value)
+        } else {
+            s.iters += 1;
+            const double tiny = 2.2250738585072014e-308;
+            double den = s.prev > tiny ? s.prev : tiny;
+            if (__ddiv_rn(__dsub_rn(s.prev, obj), den) < a.tol) s.done = 1;
+            else s.prev = obj;
+        }
+    }
+}
+
+// ------------------------------------------------------------------------
+// stage finalisation: bf16 centroids, u8 assignments, residual update
+// ------------------------------------------------------------------------
+__global__ void k_finalize_cent(const double *cent, uint16_t *cent_out, double *cent64_out,
+                                int64_t P, int S, int t, int K, int d) {
+    const int64_t n = P * K * d;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        int64_t p = i / (int64_t(K) * d), r = i - p * K * d;
+        int64_t o = (p * S + t) * int64_t(K) * d + r;
+        double c = cent[i];
+        cent_out[o] = f32_to_bf16_bits_rne(__double2float_rn(c));
+        if (cent64_out) cent64_out[o] = c;
+    }
+}
+
+__global__ void k_residual(double *rows, const double *cent, const int32_t *assign,
+                           uint8_t *assign_out, int32_t *iters_out, const PlaneState *st,
+                           int64_t P, int64_t N, int S, int t, int K, int d) {
+    const int64_t n = P * N * d;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        int64_t p = i / (N * d), e = i - p * N * d, row = e / d;
+        int col = int(e - row * d);
+        int c = assign[p * N + row];
+        float cb = bf16_to_f32(f32_to_bf16_bits_rne(__double2float_rn(cent[(p * K + c) * int64_t(d) + col])));
+        rows[i] = __dsub_rn(rows[i], double(cb));
+        if (col == 0) assign_out[(p * S + t) * N + row] = uint8_t(c);
+        if (e == 0 && iters_out) iters_out[p * S + t] = st[p].iters;
+    }
+}
+
+__global__ void k_stage_reset(PlaneState *st, int64_t P) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P; i += int64_t(gridDim.x) * blockDim.x)
+        st[i] = PlaneState{0.0, 0.0, 0, 0};
+}
+
+// ------------------------------------------------------------------------
+// host-side orchestration (called from qvg_capi.cu)
+// ------------------------------------------------------------------------
+
+static int g1d(int64_t n, int b) {
+    int64_t g = (n + b - 1) / b;
+    return int(g < 1 ? 1 : (g > 148 * 32 ? 148 * 32 : g));
+}
+
+int launch_widen(const void *x, int xbf16, double *rows, int64_t n, int32_t *status, cudaStream_t st) {
+    k_widen<<<g1d(n, 256), 256, 0, st>>>(x, xbf16, rows, n, status);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+
+static void objective(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int mode,
+                      double tol, cudaStream_t st) {
+    ObjArgs o{b.rows, b.cent, b.assign, b.nodes, b.st, b.ob_off, b.ob_len, b.nd_l, b.nd_r,
+              b.h_start, b.ob_leaves, b.ob_heights, N, d, K, mode, tol};
+    dim3 g((unsigned)((int64_t(b.ob_leaves) * 8 + 255) / 256 < 4096 ? (int64_t(b.ob_leaves) * 8 + 255) / 256 : 4096),
+           (unsigned)P);
+    k_obj_leaves<<<g, 256, 0, st>>>(o);
+    k_obj_combine<<<(unsigned)P, 1024, 0, st>>>(o);
+}
+
+static void assign_step(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int skip,
+                        cudaStream_t st) {
+    AssignArgs aa{b.rows, b.cent, b.assign, b.st, N, d, K, skip};
+    k_assign<<<dim3((unsigned)((N + AR - 1) / AR), (unsigned)P), 256, 0, st>>>(aa);
+}
+
+int run_kmeanspp(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, const double *draws,
+                 int64_t draws_stride, cudaStream_t st) {
+    PPArgs pa{b.rows, draws, draws_stride, b.cent, b.d2, b.pk_off, b.pk_len, b.pk_leaves, N, d, K};
+    size_t smem = sizeof(double) * (128 + b.pk_leaves);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(k_kmeanspp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_kmeanspp<<<(unsigned)P, 1024, smem, st>>>(pa);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+
+static void lloyd_body(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int mode,
+                       double tol, cudaStream_t st) {
+    size_t msmem = sizeof(int32_t) * (34 * K);
+    if (msmem > 48 * 1024)
+        cudaFuncSetAttribute(k_members, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)msmem);
+    assign_step(b, P, N, d, K, 1, st);
+    MemberArgs ma{b.assign, b.counts, b.offsets, b.members, b.st, N, K};
+    k_members<<<(unsigned)P, 1024, msmem, st>>>(ma);
+    SumArgs sa{b.rows, b.cent, b.counts, b.offsets, b.members, b.st, N, d, K};
+    k_sums<<<dim3((unsigned)K, (unsigned)P), 128, 0, st>>>(sa);
+    RepairArgs ra{b.rows, b.cent, b.assign, b.counts, b.d2, b.st, N, d, K};
+    k_repair<<<(unsigned)P, 1024, 0, st>>>(ra);
+    objective(b, P, N, d, K, mode, tol, st);
+}
+
+// One SAS stage's k-means for all planes (Q/clustering.py:110-160); leaves
+// the final assignment in b.assign and the iteration count in b.st.
+int run_kmeans_stage(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int max_iters,
+                     double tol, const double *draws_stage, int64_t draws_stride, bool warm,
+                     cudaStream_t st) {
+    k_stage_reset<<<g1d(P, 256), 256, 0, st>>>(b.st, P);
+    if (!warm && run_kmeanspp(b, P, N, d, K, draws_stage, draws_stride, st)) return QVG_ERR_CUDA;
+    // objective of the starting centroids (Q/clustering.py:142-143)
+    assign_step(b, P, N, d, K, 0, st);
+    objective(b, P, N, d, K, 0, tol, st);
+    for (int it = 0; it < max_iters; it++) lloyd_body(b, P, N, d, K, 1, tol, st);
+    // final assignment (Q/clustering.py:153)
+    assign_step(b, P, N, d, K, 0, st);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+
+__global__ void k_km_outputs(const int32_t *assign, uint8_t *assign_out, const PlaneState *st,
+                             double *obj_out, int32_t *iters_out, int64_t P, int64_t N) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P * N; i += int64_t(gridDim.x) * blockDim.x) {
+        if (assign_out) assign_out[i] = uint8_t(assign[i]);
+        if (i % N == 0) {
+            int64_t p = i / N;
+            if (obj_out) obj_out[p] = st[p].obj;
+            if (iters_out) iters_out[p] = st[p].iters;
+        }
+    }
+}
+
+int kmeans_outputs(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, uint8_t *assign,
+                   double *objective_out, int32_t *iters, cudaStream_t st) {
+    objective(b, P, N, d, K, 2, 0.0, st);   // Q/clustering.py:154
+    k_km_outputs<<<g1d(P * N, 256), 256, 0, st>>>(b.assign, assign, b.st, objective_out, iters, P, N);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+
+int lloyd_once(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, uint8_t *assign,
+               double *objective_out, cudaStream_t st) {
+    k_stage_reset<<<g1d(P, 256), 256, 0, st>>>(b.st, P);
+    lloyd_body(b, P, N, d, K, 2, 0.0, st);
+    k_km_outputs<<<g1d(P * N, 256), 256, 0, st>>>(b.assign, assign, b.st, objective_out, nullptr, P, N);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+
+int run_assign(const double *rows, const double *cent, int32_t *assign, int64_t P, int64_t N, int d,
+               int K, cudaStream_t st) {
+    AssignArgs aa{rows, cent, assign, nullptr, N, d, K, 0};
+    k_assign<<<dim3((unsigned)((N + AR - 1) / AR), (unsigned)P), 256, 0, st>>>(aa);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+
+// add_back (Q/smoothing.py:44-54): residual + f64(C_bf16[pi])
+__global__ void k_add_back(const double *res, const uint16_t *cent, const uint8_t *asg, int64_t P,
+                           int64_t N, int d, int K, double *out) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < P * N * d; i += int64_t(gridDim.x) * blockDim.x) {
+        int64_t p = i / (N * d), e = i - p * N * d, row = e / d;
+        int col = int(e - row * d);
+        int c = asg[p * N + row];
+        out[i] = __dadd_rn(res[i], double(bf16_to_f32(cent[(p * K + c) * int64_t(d) + col])));
+    }
+}
+
+int run_add_back(const double *residual, const uint16_t *cent, const uint8_t *assign, int64_t P,
+                 int64_t N, int d, int K, double *out, cudaStream_t st) {
+    k_add_back<<<g1d(P * N * d, 256), 256, 0, st>>>(residual, cent, assign, P, N, d, K, out);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+
+int finalize_stage(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int S, int t,
+                   uint16_t *cent_out, double *cent64_out, uint8_t *assign_out, int32_t *iters_out,
+                   cudaStream_t st) {
+    k_finalize_cent<<<g1d(P * K * d, 256), 256, 0, st>>>(b.cent, cent_out, cent64_out, P, S, t, K, d);
+    k_residual<<<g1d(P * N * d, 256), 256, 0, st>>>(b.rows, b.cent, b.assign, assign_out, iters_out,
+                                                    b.st, P, N, S, t, K, d);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+
+}  // namespace qvg

@@ -1,0 +1,157 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+own outputs (tests/golden) and the CPU oracle on seeded inputs.
+
+Bar: bit-exact payload / scale bytes, assignments, bf16 centroids, f64
+centroids, k-means iteration counts; dequantized float32 bit-exact; bf16
+output = RNE(oracle float32)."""
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_planes
+from golden_io import load_plane
+
+pytestmark = pytest.mark.gpu
+
+from paper_2602_02958_b200 import device as D  # noqa: E402
+from paper_2602_02958_b200.qvgcodec.types import QuantConfig  # noqa: E402
+
+
+def cfg_of(rec, **kw):
+    return QuantConfig(bits=rec["bits"], group_size=rec["group_size"], stages=rec["stages"],
+                       centroids=rec["centroids"], **kw)
+
+
+def _u32(a):
+    return np.ascontiguousarray(a, dtype=np.float32).view(np.uint32)
+
+
+@pytest.mark.parametrize("name", golden_planes())
+@pytest.mark.parametrize("xdtype", [torch.bfloat16, torch.float32])
+def test_compress_matches_reference_fixture(name, xdtype):
+    rec = load_plane(name)
+    cfg = cfg_of(rec)
+    x = torch.from_numpy(rec["x"]).to(xdtype).cuda()[None]
+    warm = None
+    if "warm" in rec:
+        warm = torch.from_numpy(rec["warm"]).cuda()[None]
+    dc = D.compress(x, cfg, chunk_index=rec["chunk_index"], warm_init=warm, keep_f64=True)
+    torch.cuda.synchronize()
+    S = rec["stages"]
+    if S:
+        assert np.array_equal(dc.iters[0].cpu().numpy(), rec["iters"]), "iterations"
+        assert np.array_equal(dc.assignments[0].cpu().numpy(), rec["assignments"]), "assignments"
+        assert np.array_equal(dc.centroids_f64[0].cpu().numpy().view(np.uint64),
+                              rec["cent_f64"].view(np.uint64)), "f64 centroids"
+        assert np.array_equal(_u32(dc.centroids[0].float().cpu().numpy()),
+                              _u32(rec["centroids_bf16"])), "bf16 centroids"
+    assert np.array_equal(dc.payload[0].cpu().numpy(), rec["payload"]), "payload"
+    assert np.array_equal(dc.scales[0].cpu().numpy(), rec["scales"]), "scales"
+    out = D.dequantize(dc, torch.float32)
+    assert np.array_equal(_u32(out[0].cpu().numpy()), _u32(rec["decoded"])), "decoded f32"
+    outb = D.dequantize(dc, torch.bfloat16)
+    ref_b = torch.from_numpy(rec["decoded"]).to(torch.bfloat16)
+    assert torch.equal(outb[0].cpu().view(torch.int16), ref_b.view(torch.int16)), "decoded bf16"
+
+
+def _rand_planes(rng, P, N, d, scale_outlier):
+    x = rng.normal(0, 2.5, size=(P, N, d)) + rng.normal(0, 0.125, size=(P, N, d))
+    x[:, :, ::16] *= scale_outlier
+    return torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("bits,B,S,K,d", [
+    (2, 64, 2, 64, 128), (4, 16, 1, 32, 128), (8, 32, 3, 8, 64), (2, 16, 4, 16, 128),
+    (2, 128, 1, 256, 128), (4, 8, 2, 5, 24), (2, 4, 1, 7, 20), (4, 128, 0, 1, 128)])
+def test_quantize_dequantize_given_metas_vs_oracle(oracle_lib, bits, B, S, K, d):
+    rng = np.random.default_rng(bits * 1000 + B * 10 + S)
+    P, N = 3, 517
+    x = _rand_planes(rng, P, N, d, 40.0)
+    # metas: centroids drawn near the data, random assignments
+    cent = torch.from_numpy(rng.normal(0, 2.0, size=(P, S, K, d)).astype(np.float32)).to(torch.bfloat16)
+    asg = torch.from_numpy(rng.integers(0, K, size=(P, S, N)).astype(np.uint8))
+    cfg = QuantConfig(bits=bits, group_size=B, stages=S, centroids=K)
+    pay, sc = D.quantize(x.cuda(), cfg, cent.cuda(), asg.cuda())
+    rp, rs = oracle_lib.quantize_given_metas_batch(x.float().numpy(), cent.float().numpy(),
+                                                   asg.numpy(), bits, B, 4)
+    assert np.array_equal(pay.cpu().numpy(), rp)
+    assert np.array_equal(sc.cpu().numpy(), rs)
+    dc = D.DeviceChunks(cfg, N, d, pay, sc, cent.cuda(), asg.cuda())
+    out = D.dequantize(dc, torch.float32).cpu().numpy()
+    ref = oracle_lib.prq_decompress_batch(rp, rs, cent.float().numpy(), asg.numpy(), N, d, bits, B, 4)
+    assert np.array_equal(_u32(out), _u32(ref))
+
+
+def test_quantize_boundary_cases(oracle_lib):
+    """Residuals placed exactly on / one ulp around rounding boundaries, zero
+    groups, saturating groups (s > 448) and sub-2^-9 scales exercise the
+    certified fallback paths of the fast kernel."""
+    rng = np.random.default_rng(7)
+    P, N, d, B = 2, 256, 128, 64
+    x = rng.normal(size=(P, N, d)).astype(np.float32)
+    s = np.float32(0.15625)
+    x[0, 0, :B] = 0.0                                  # zero group -> 0x38
+    x[0, 1, :B] = 0.0
+    x[0, 1, 0] = 1e-7                                  # tiny scale -> 0x01
+    x[0, 2, :B] = 3000.0                               # saturating scale
+    x[0, 3, :B] = s / 2                                # exact half -> ties
+    x[0, 3, 0] = s
+    x[0, 4, :B] = np.nextafter(s / 2, np.float32(1))   # just above the tie
+    x[0, 4, 0] = s
+    x[0, 5, :B] = np.nextafter(s / 2, np.float32(0))
+    x[0, 5, 0] = s
+    for bits in (2, 4, 8):
+        cfg = QuantConfig(bits=bits, group_size=B, stages=0, centroids=1)
+        xt = torch.from_numpy(x).cuda()
+        pay, sc = D.quantize(xt, cfg)
+        rp, rs = oracle_lib.quantize_given_metas_batch(x, np.zeros((P, 0, 1, d), np.float32),
+                                                       np.zeros((P, 0, N), np.uint8), bits, B, 4)
+        assert np.array_equal(sc.cpu().numpy(), rs), bits
+        assert np.array_equal(pay.cpu().numpy(), rp), bits
+
+
+def test_kmeans_primitives_vs_oracle(oracle_lib):
+    rec = load_plane("s4_pro")
+    rows = rec["x"].astype(np.float64)
+    K = 16
+    draws = oracle_lib.pp_draws(0, 0, 1, K)[0]
+    cent_o, _ = oracle_lib.kmeans_pp(rows, K, draws)
+    rt = torch.from_numpy(rows).cuda()[None]
+    cent_g = D.kmeans_pp(rt, K, torch.from_numpy(draws).cuda()[None])
+    assert np.array_equal(cent_g[0].cpu().numpy(), cent_o)
+    a_o = oracle_lib.assign(rows, cent_o)
+    a_g = D.assign(rt, cent_g)[0].cpu().numpy()
+    assert np.array_equal(a_g, a_o)
+    c_o, asg_o, obj_o, it_o = oracle_lib.kmeans(rows, K, 10, 1e-4, draws=draws)
+    c_g, asg_g, obj_g, it_g = D.kmeans(rt, K, 10, 1e-4, draws=torch.from_numpy(draws).cuda()[None])
+    assert np.array_equal(c_g[0].cpu().numpy().view(np.uint64), c_o.view(np.uint64))
+    assert np.array_equal(asg_g[0].cpu().numpy(), asg_o.astype(np.uint8))
+    assert obj_g[0].item() == obj_o and it_g[0].item() == it_o
+
+
+def test_batched_planes_independent(oracle_lib):
+    """P planes in one launch == each plane alone (and == the oracle)."""
+    rng = np.random.default_rng(3)
+    P, N, d = 5, 700, 128
+    x = _rand_planes(rng, P, N, d, 10.0)
+    cfg = QuantConfig(bits=2, group_size=64, stages=2, centroids=16)
+    dc = D.compress(x.cuda(), cfg, chunk_index=[0, 1, 2, 3, 4])
+    draws = np.stack([oracle_lib.pp_draws(0, c, 2, 16) for c in range(P)])
+    pay, sc, cent, asg, iters = oracle_lib.prq_compress_batch(x.float().numpy(), 2, 64, 2, 16, 10,
+                                                              1e-4, draws, 4)
+    assert np.array_equal(dc.assignments.cpu().numpy(), asg)
+    assert np.array_equal(dc.payload.cpu().numpy(), pay)
+    assert np.array_equal(dc.scales.cpu().numpy(), sc)
+    assert np.array_equal(dc.iters.cpu().numpy(), iters)
+    one = D.compress(x[2:3].cuda(), cfg, chunk_index=2)
+    assert torch.equal(one.payload[0], dc.payload[2])
+
+
+def test_nonfinite_input_raises():
+    from paper_2602_02958_b200.qvgcodec.errors import NonFiniteInput
+    x = torch.zeros((1, 16, 128), dtype=torch.float32, device="cuda")
+    x[0, 3, 5] = float("nan")
+    with pytest.raises(NonFiniteInput):
+        D.compress(x, QuantConfig(stages=1, centroids=4))
+    with pytest.raises(NonFiniteInput):
+        D.quantize(x, QuantConfig(stages=0))
