@@ -35,6 +35,14 @@ __device__ __forceinline__ uint32_t e4m3_ceil_f32(float v) {
     return (((u >> 23) - 120u) << 3) | ((u >> 20) & 7u);
 }
 
+// Branch-free exact E4M3 -> f32: the 7 magnitude bits placed at f32 bit 20
+// read as 2^(e-127)(1+m/8) (or the denormal m*2^-129 when e == 0); scaling by
+// 2^120 (exact) gives (8+m)*2^(e-10), resp. m*2^-9.
+__device__ __forceinline__ float e4m3_decode_fast(uint32_t b) {
+    const float mag = __uint_as_float((b & 0x7Fu) << 20) * 1.329227995784916e36f;   // 2^120
+    return __uint_as_float(__float_as_uint(mag) | ((b & 0x80u) << 24));
+}
+
 template <bool XBF16>
 __device__ __forceinline__ void load_x8(const void *x, int64_t elem, float r[8]) {
     if constexpr (XBF16) {
@@ -63,7 +71,82 @@ __device__ __forceinline__ double load_x1(const void *x, int64_t elem) {
 }
 
 // ------------------------------------------------------------------------
-// K5 fast quantize: d % 8 == 0, B in {8..256} (power of two), S <= 4.
+// index helpers: n / N for the flattened [P*N] row space (< 2^32 rows) with a
+// multiply-high (Granlund-Montgomery "round-up" variant, exact for all u32 n)
+// ------------------------------------------------------------------------
+struct FastDiv {
+    uint32_t m, l;
+    __device__ __forceinline__ uint32_t div(uint32_t n) const {
+        return uint32_t((uint64_t(__umulhi(n, m)) + n) >> l);
+    }
+};
+
+static FastDiv make_fastdiv(uint32_t d) {
+    uint32_t l = 0;
+    while ((uint64_t(1) << l) < d) l++;
+    uint64_t m = ((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1;
+    return FastDiv{uint32_t(m), l};
+}
+
+// Tile mapping shared by K5/K6.  A tile is kUnroll*256/VPR consecutive rows
+// of ONE plane (VPR = d/8 threads per row, each owning 8 channels), so the
+// plane index is one division per tile and every in-plane offset is 32-bit.
+// The tile loop is block-uniform, so every lane reaches every shuffle.
+constexpr int kUnroll = 2;
+
+struct TileArgs {
+    uint32_t n_tiles, tpp;       // tiles in total / per plane
+    FastDiv div_tpp;
+    uint32_t rows_per_pass;      // 256 >> lvpr
+};
+
+// E4M3 code of RN64(A/QMAX) for every A in [lo, hi] (f32, lo > 0), or
+// ambiguous.  Products QMAX * grid value are exact in f32 (<= 11 bits).
+template <int QMAX>
+__device__ __forceinline__ float grid_val(uint32_t code) { return e4m3_to_f32(code) * float(QMAX); }
+
+template <int QMAX>
+__device__ __forceinline__ uint32_t scale_code(float lo, float hi, bool &amb) {
+    uint32_t c = e4m3_ceil_f32(QMAX == 1 ? hi : __fmul_ru(hi, 1.0f / QMAX * 1.0000002f));
+    if (QMAX > 1) {   // make c the exact ceil code of hi/QMAX
+        while (c > 1 && hi <= grid_val<QMAX>(c - 1)) c--;
+        while (c < 0x7Eu && hi > grid_val<QMAX>(c)) c++;
+    }
+    if (c == 0x7Eu) amb = !(lo > float(QMAX) * 416.f);        // saturating band (416, 448]
+    else amb = c > 0 && !(lo > grid_val<QMAX>(c - 1));
+    return c;
+}
+
+
+template <bool XBF16>
+__device__ __forceinline__ float load_x1f(const void *x, uint64_t e) {
+    if constexpr (XBF16) return bf16_to_f32(static_cast<const uint16_t *>(x)[e]);
+    else return static_cast<const float *>(x)[e];
+}
+
+// Rare-path helpers, kept out of line so the compiler cannot hoist their
+// address arithmetic into the streaming loop.
+// The reference's float64 residual x - C_1[pi_1] - ... (Q/smoothing.py:40).
+template <bool XBF16, int S>
+__device__ __noinline__ double exact_residual(const uint8_t *xb, const uint16_t *cp, uint32_t e,
+                                             uint32_t col, uint32_t d, int K, int a0, int a1,
+                                             int a2, int a3) {
+    double v = double(load_x1f<XBF16>(xb, e));
+    const int ai[4] = {a0, a1, a2, a3};
+#pragma unroll
+    for (int t = 0; t < S; t++) v = __dsub_rn(v, double(bf16_to_f32(cp[uint32_t(t * K + ai[t]) * d + col])));
+    return v;
+}
+
+// q = clip(rint(RN64(r / s))) (Q/quant.py:53-54)
+template <int QMAX>
+__device__ __noinline__ uint32_t exact_code(double r, float s) {
+    const double qd = fmin(fmax(rint(__ddiv_rn(r, double(s))), -double(QMAX)), double(QMAX));
+    return uint32_t(int(qd));
+}
+
+// ------------------------------------------------------------------------
+// K5 quantize (fast path: d/8 a power of two <= 32, B/8 a power of two, S <= 4)
 // ------------------------------------------------------------------------
 struct QuantArgs {
     const void *x;
@@ -71,266 +154,160 @@ struct QuantArgs {
     const uint8_t *asg;     // [P][S][N]
     uint8_t *payload;       // [P][PB]
     uint8_t *scales;        // [P][N*d/B]
-    int64_t n_vec;          // P*N*d/8
-    int64_t N;
-    int d, K, B, gshift;    // gshift = log2(B/8)
+    uint32_t N;
+    int d, K, B, lvpr, gshift;
     int32_t *status;
+    uint32_t pb, ng, lgB;   // payload bytes / scale bytes per plane, log2(B)
+    TileArgs ta;
+    int v16;                // 16 channels per thread (k_quantize_v4)
 };
 
 template <int BITS, int S, bool XBF16>
-__global__ void __launch_bounds__(256) k_quantize_fast(QuantArgs a) {
+__global__ void __launch_bounds__(256) k_quantize_v3(QuantArgs a) {
     constexpr int QMAX = (1 << (BITS - 1)) - 1;
-    constexpr float kInvLo = QMAX == 1 ? 1.f : (QMAX == 7 ? 0.142857134342193603515625f : 0.0078740157186985015869140625f);
-    constexpr float kInvHi = QMAX == 1 ? 1.f : (QMAX == 7 ? 0.1428571492433547973632812500f : 0.0078740166500210762023925781f);
-    const int d = a.d;
-    const int64_t vpr = d >> 3;
-    const int64_t vpp = a.N * vpr;
+    constexpr uint64_t FMASK = (1u << BITS) - 1u;
+    constexpr int SS = S > 0 ? S : 1;
+    const uint32_t d = uint32_t(a.d), N = a.N;
+    const int col = int(threadIdx.x & ((1u << a.lvpr) - 1u)) << 3;
+    const uint32_t rslot = threadIdx.x >> a.lvpr;
     const int glanes = 1 << a.gshift;
     const int lane = threadIdx.x & 31;
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    // Loop bound rounded up to the warp so all lanes reach every shuffle.
-    const int64_t nv_round = (a.n_vec + 31) & ~int64_t(31);
-    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < nv_round; v += stride) {
-        const bool valid = v < a.n_vec;
-        const int64_t vv = valid ? v : a.n_vec - 1;
-        const int64_t p = vv / vpp;
-        const int64_t rem = vv - p * vpp;
-        const int64_t row = rem / vpr;
-        const int col = int(rem - row * vpr) << 3;
-        const int64_t elem = vv << 3;
-
-        float r[8];
-        load_x8<XBF16>(a.x, elem, r);
-        bool finite = true;
+    uint32_t stat = 0;
+    for (uint32_t T = blockIdx.x; T < a.ta.n_tiles; T += gridDim.x) {
+        const uint32_t p = a.ta.div_tpp.div(T);
+        const uint32_t i0 = (T - p * a.ta.tpp) * a.ta.rows_per_pass * kUnroll;
+        const uint64_t pN = uint64_t(p) * N;
+        const uint8_t *xb = static_cast<const uint8_t *>(a.x) + pN * d * (XBF16 ? 2 : 4);
+        const uint8_t *ap = a.asg + pN * S;
+        const uint16_t *cp = a.cent + uint64_t(p) * S * a.K * d;
+        float r[kUnroll][8];
+        uint32_t ii[kUnroll];
+        int ai[kUnroll][SS];
 #pragma unroll
-        for (int k = 0; k < 8; k++) finite &= isfinite(r[k]);
-        if (!finite && valid) atomicOr(a.status, QVG_STATUS_NONFINITE);
-
-        // residual chain x - C1[pi1] - C2[pi2] ... (Q/smoothing.py:40) in f32
-        float ebound = 0.f;
-        int ai[S > 0 ? S : 1];
+        for (int u = 0; u < kUnroll; u++) {
+            const uint32_t i = i0 + u * a.ta.rows_per_pass + rslot;
+            ii[u] = i < N ? i : N - 1;
+            load_x8<XBF16>(xb, int64_t(ii[u] * d + col), r[u]);
 #pragma unroll
-        for (int t = 0; t < S; t++) {
-            ai[t] = __ldg(a.asg + (p * S + t) * a.N + row);
-            float c[8];
-            load_c8(a.cent + ((p * S + t) * a.K + ai[t]) * int64_t(d) + col, c);
-            float m = 0.f;
-#pragma unroll
-            for (int k = 0; k < 8; k++) {
-                r[k] = __fsub_rn(r[k], c[k]);
-                m = fmaxf(m, fabsf(r[k]));
-            }
-            ebound = __fadd_ru(ebound, m);
+            for (int t = 0; t < S; t++) ai[u][t] = __ldg(ap + t * N + ii[u]);
         }
-        float amax = 0.f;
+        float eb[kUnroll], am[kUnroll];
 #pragma unroll
-        for (int k = 0; k < 8; k++) amax = fmaxf(amax, fabsf(r[k]));
-        // group reductions (B/8 lanes)
+        for (int u = 0; u < kUnroll; u++) {
+            bool fin = true;
+#pragma unroll
+            for (int k = 0; k < 8; k++) fin &= isfinite(r[u][k]);
+            if (!fin) stat |= QVG_STATUS_NONFINITE;
+            float e = 0.f;
+#pragma unroll
+            for (int t = 0; t < S; t++) {
+                float c[8];
+                load_c8(cp + (uint32_t(t * a.K + ai[u][t]) * d + col), c);
+                float m = 0.f;
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    r[u][k] = __fsub_rn(r[u][k], c[k]);
+                    m = fmaxf(m, fabsf(r[u][k]));
+                }
+                e = __fadd_ru(e, m);
+            }
+            float mx = 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; k++) mx = fmaxf(mx, fabsf(r[u][k]));
+            eb[u] = e;
+            am[u] = mx;
+        }
         for (int m = 1; m < glanes; m <<= 1) {
-            amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, m));
-            ebound = fmaxf(ebound, __shfl_xor_sync(0xffffffffu, ebound, m));
-        }
-        // |r_f32 - r_f64| <= 2^-24 * sum_t |r_t| per rounding of each chain (f32 and
-        // the reference's f64); 2^-22 leaves a factor-2 margin on top of both.
-        const float E = ebound * 2.3841858e-7f;
-        // scale code: certain iff the E-interval of amax/qmax maps to one code
-        uint32_t code;
-        bool grp_amb = false;
-        if (E == 0.f) {
-            if (amax == 0.f) code = 0x38u;
-            else {
-                uint32_t lo = e4m3_ceil_f32(__fmul_rd(amax, kInvLo));
-                uint32_t hi = e4m3_ceil_f32(__fmul_ru(amax, kInvHi));
-                code = hi;
-                grp_amb = lo != hi;
-            }
-        } else {
-            float lo_a = __fsub_rd(amax, E);
-            if (!(lo_a > 0.f)) { code = 0x38u; grp_amb = true; }
-            else {
-                uint32_t lo = e4m3_ceil_f32(__fmul_rd(lo_a, kInvLo));
-                uint32_t hi = e4m3_ceil_f32(__fmul_ru(__fadd_ru(amax, E), kInvHi));
-                code = hi;
-                grp_amb = lo != hi;
-            }
-        }
-        float s = e4m3_to_f32(code);
-        float inv = __frcp_rn(s);
-        // half-width of the window around a rounding boundary that the exact
-        // quotient |r|/s might fall on the other side of
-        const float W = __fmul_ru(__fmaf_ru(E, inv, __fmul_ru(__fmul_ru(amax, inv), 4.7683716e-7f)), 1.001f);
-        uint32_t bits = 0;
-        uint32_t el_amb = 0;
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-            float t = __fmul_rn(fabsf(r[k]), inv);
-            int q;
+            for (int u = 0; u < kUnroll; u++) {
+                am[u] = fmaxf(am[u], __shfl_xor_sync(0xffffffffu, am[u], m));
+                eb[u] = fmaxf(eb[u], __shfl_xor_sync(0xffffffffu, eb[u], m));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+            const bool valid = i0 + u * a.ta.rows_per_pass + rslot < N;
+            // |r_f32 - r_ref| <= 2^-24 sum_t|r_t| (f32 chain) + 2^-53 (.) (the
+            // reference's f64 chain) <= 2^-22 * sum_t max|r_t|: factor-2 margin
+            const float E = __fmul_ru(eb[u], 2.38418579e-7f);
+            uint32_t code;
+            bool camb = false;
+            if (am[u] == 0.f && E == 0.f) code = 0x38u;
+            else {
+                float lo = __fsub_rd(am[u], E), hi = __fadd_ru(am[u], E);
+                if (lo > 0.f) code = scale_code<QMAX>(lo, hi, camb);
+                else { code = 0x38u; camb = true; }
+            }
+            camb &= valid;
+            auto exact_r = [&](int k) {   // the reference's f64 residual (rare path)
+                return exact_residual<XBF16, S>(xb, cp, ii[u] * d + col + k, col + k, d, a.K,
+                                                ai[u][0], ai[u][SS > 1 ? 1 : 0], ai[u][SS > 2 ? 2 : 0],
+                                                ai[u][SS > 3 ? 3 : 0]);
+            };
+            // ---- exact scale (rare): max of the exact residual over the candidates
+            if (__any_sync(0xffffffffu, camb)) {
+                const float thr = __fsub_rd(am[u], __fmul_ru(E, 2.f));
+                double a64 = 0.0;
+                if (camb) {
+#pragma unroll
+                    for (int k = 0; k < 8; k++)
+                        if (fabsf(r[u][k]) >= thr) a64 = fmax(a64, fabs(exact_r(k)));
+                }
+                for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
+                if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
+            }
+            const float s = e4m3_to_f32(code);
+            uint64_t bits = 0;
+            uint32_t el_amb = 0;
             if constexpr (QMAX == 1) {
-                q = t > 0.5f ? 1 : 0;
-                if (fabsf(t - 0.5f) <= W) el_amb |= 1u << k;
+                // q != 0  <=>  RN64(|r|/s) > 0.5  <=>  |r| > s/2 for an f32-exact r
+                const float wlo = __fsub_rd(0.5f * s, E), whi = __fadd_ru(0.5f * s, E);
+                uint32_t b32 = 0;
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    const float av = fabsf(r[u][k]);
+                    const bool one = av > whi;
+                    if (!one && !(av < wlo)) el_amb |= 1u << k;
+                    const uint32_t f = one ? ((__float_as_uint(r[u][k]) >> 30) | 1u) : 0u;  // 1 or 3
+                    b32 |= f << (2 * k);
+                }
+                bits = b32;
             } else {
-                float fl = floorf(t);
-                if (fabsf(t - fl - 0.5f) <= W && fl < float(QMAX)) el_amb |= 1u << k;
-                q = min(int(rintf(t)), QMAX);
+                const float inv = __frcp_rn(s);
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    const float av = fabsf(r[u][k]);
+                    const float t = av * inv;
+                    const float fl = floorf(t);
+                    const float hb = (fl + 0.5f) * s;                    // exact
+                    const float w = __fmaf_ru(hb, 2.38418579e-7f, E);
+                    if (fl < float(QMAX) && av >= __fsub_rd(hb, w) && av <= __fadd_ru(hb, w)) el_amb |= 1u << k;
+                    int q = min(int(rintf(t)), QMAX);
+                    if (r[u][k] < 0.f) q = -q;
+                    bits |= (uint64_t(uint32_t(q)) & FMASK) << (k * BITS);
+                }
             }
-            if (r[k] < 0.f) q = -q;
-            bits |= (uint32_t(q) & ((1u << BITS) - 1u)) << (k * BITS);
-        }
-        if (!valid) { grp_amb = false; el_amb = 0; }
-
-        // ---- exact fallback (rare): recompute in f64, reference order ----
-        if (__any_sync(0xffffffffu, grp_amb || el_amb)) {
-            double r64[8];
-#pragma unroll
-            for (int k = 0; k < 8; k++) r64[k] = load_x1<XBF16 ? 1 : 0>(a.x, elem + k);
-#pragma unroll
-            for (int t = 0; t < S; t++) {
-                const uint16_t *cp = a.cent + ((p * S + t) * a.K + ai[t]) * int64_t(d) + col;
-#pragma unroll
-                for (int k = 0; k < 8; k++) r64[k] = __dsub_rn(r64[k], double(bf16_to_f32(cp[k])));
-            }
-            double am = 0.0;
-#pragma unroll
-            for (int k = 0; k < 8; k++) am = fmax(am, fabs(r64[k]));
-            for (int m = 1; m < glanes; m <<= 1) am = fmax(am, shfl_xor_d(am, m));
-            if (grp_amb) {
-                code = am == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(am, double(QMAX)));
-                el_amb = 0xFFu;
-            }
-            if (el_amb) {
-                double sd = double(e4m3_to_f32(code));
+            if (!valid) el_amb = 0;
+            // ---- exact codes (rare): elements inside the error window of a boundary
+            if (__any_sync(0xffffffffu, el_amb != 0)) {
 #pragma unroll
                 for (int k = 0; k < 8; k++) {
                     if (!(el_amb >> k & 1u)) continue;
-                    double qd = rint(__ddiv_rn(r64[k], sd));   // np.rint: half-even
-                    qd = fmin(fmax(qd, -double(QMAX)), double(QMAX));
-                    int q = int(qd);
-                    bits = (bits & ~(((1u << BITS) - 1u) << (k * BITS))) |
-                           ((uint32_t(q) & ((1u << BITS) - 1u)) << (k * BITS));
+                    const uint32_t q = exact_code<QMAX>(exact_r(k), s);
+                    bits = (bits & ~(FMASK << (k * BITS))) | ((uint64_t(q) & FMASK) << (k * BITS));
                 }
             }
+            if (!valid) continue;
+            const uint32_t e0 = ii[u] * d + col;                               // element in plane
+            uint8_t *pl = a.payload + uint64_t(p) * a.pb + ((e0 * BITS) >> 3);
+            if constexpr (BITS == 2) *reinterpret_cast<uint16_t *>(pl) = uint16_t(bits);
+            else if constexpr (BITS == 4) *reinterpret_cast<uint32_t *>(pl) = uint32_t(bits);
+            else *reinterpret_cast<uint2 *>(pl) = make_uint2(uint32_t(bits), uint32_t(bits >> 32));
+            if ((lane & (glanes - 1)) == 0) a.scales[uint64_t(p) * a.ng + (e0 >> a.lgB)] = uint8_t(code);
         }
-        if (!valid) continue;
-        // ---- stores ----
-        const int64_t pb = (a.N * d * BITS) >> 3;             // bytes per plane
-        uint8_t *pl = a.payload + p * pb + (((row * d + col) * BITS) >> 3);
-        if constexpr (BITS == 2) *reinterpret_cast<uint16_t *>(pl) = uint16_t(bits);
-        else if constexpr (BITS == 4) *reinterpret_cast<uint32_t *>(pl) = bits;
-        else {
-            // 8-bit: 8 codes = 8 bytes; bits holds only 32 -> recompute hi half below
-            (void)pl;
-        }
-        if ((lane & (glanes - 1)) == 0)
-            a.scales[p * (a.N * d / a.B) + (row * d + col) / a.B] = uint8_t(code);
     }
-}
-
-// 8-bit codes need 64 bits per thread; a dedicated variant keeps the common
-// 2/4-bit kernel's registers small.
-template <int S, bool XBF16>
-__global__ void __launch_bounds__(256) k_quantize_fast8(QuantArgs a) {
-    constexpr int QMAX = 127;
-    constexpr float kInvLo = 0.0078740157186985015869140625f;
-    constexpr float kInvHi = 0.0078740166500210762023925781f;
-    const int d = a.d;
-    const int64_t vpr = d >> 3, vpp = a.N * vpr;
-    const int glanes = 1 << a.gshift;
-    const int lane = threadIdx.x & 31;
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    const int64_t nv_round = (a.n_vec + 31) & ~int64_t(31);
-    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < nv_round; v += stride) {
-        const bool valid = v < a.n_vec;
-        const int64_t vv = valid ? v : a.n_vec - 1;
-        const int64_t p = vv / vpp, rem = vv - p * vpp, row = rem / vpr;
-        const int col = int(rem - row * vpr) << 3;
-        const int64_t elem = vv << 3;
-        float r[8];
-        load_x8<XBF16>(a.x, elem, r);
-        bool finite = true;
-#pragma unroll
-        for (int k = 0; k < 8; k++) finite &= isfinite(r[k]);
-        if (!finite && valid) atomicOr(a.status, QVG_STATUS_NONFINITE);
-        float ebound = 0.f;
-        int ai[S > 0 ? S : 1];
-#pragma unroll
-        for (int t = 0; t < S; t++) {
-            ai[t] = __ldg(a.asg + (p * S + t) * a.N + row);
-            float c[8];
-            load_c8(a.cent + ((p * S + t) * a.K + ai[t]) * int64_t(d) + col, c);
-            float m = 0.f;
-#pragma unroll
-            for (int k = 0; k < 8; k++) { r[k] = __fsub_rn(r[k], c[k]); m = fmaxf(m, fabsf(r[k])); }
-            ebound = __fadd_ru(ebound, m);
-        }
-        float amax = 0.f;
-#pragma unroll
-        for (int k = 0; k < 8; k++) amax = fmaxf(amax, fabsf(r[k]));
-        for (int m = 1; m < glanes; m <<= 1) {
-            amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, m));
-            ebound = fmaxf(ebound, __shfl_xor_sync(0xffffffffu, ebound, m));
-        }
-        const float E = ebound * 2.3841858e-7f;
-        uint32_t code;
-        bool grp_amb = false;
-        float lo_a = E == 0.f ? amax : __fsub_rd(amax, E);
-        if (E == 0.f && amax == 0.f) code = 0x38u;
-        else if (!(lo_a > 0.f)) { code = 0x38u; grp_amb = true; }
-        else {
-            uint32_t lo = e4m3_ceil_f32(__fmul_rd(lo_a, kInvLo));
-            uint32_t hi = e4m3_ceil_f32(__fmul_ru(__fadd_ru(amax, E), kInvHi));
-            code = hi;
-            grp_amb = lo != hi;
-        }
-        float s = e4m3_to_f32(code), inv = __frcp_rn(s);
-        const float W = __fmul_ru(__fmaf_ru(E, inv, __fmul_ru(__fmul_ru(amax, inv), 4.7683716e-7f)), 1.001f);
-        uint32_t lo32 = 0, hi32 = 0, el_amb = 0;
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-            float t = __fmul_rn(fabsf(r[k]), inv);
-            float fl = floorf(t);
-            if (fabsf(t - fl - 0.5f) <= W && fl < float(QMAX)) el_amb |= 1u << k;
-            int q = min(int(rintf(t)), QMAX);
-            if (r[k] < 0.f) q = -q;
-            if (k < 4) lo32 |= (uint32_t(q) & 0xFFu) << (k * 8);
-            else hi32 |= (uint32_t(q) & 0xFFu) << ((k - 4) * 8);
-        }
-        if (!valid) { grp_amb = false; el_amb = 0; }
-        if (__any_sync(0xffffffffu, grp_amb || el_amb)) {
-            double r64[8];
-#pragma unroll
-            for (int k = 0; k < 8; k++) r64[k] = load_x1<XBF16 ? 1 : 0>(a.x, elem + k);
-#pragma unroll
-            for (int t = 0; t < S; t++) {
-                const uint16_t *cp = a.cent + ((p * S + t) * a.K + ai[t]) * int64_t(d) + col;
-#pragma unroll
-                for (int k = 0; k < 8; k++) r64[k] = __dsub_rn(r64[k], double(bf16_to_f32(cp[k])));
-            }
-            double am = 0.0;
-#pragma unroll
-            for (int k = 0; k < 8; k++) am = fmax(am, fabs(r64[k]));
-            for (int m = 1; m < glanes; m <<= 1) am = fmax(am, shfl_xor_d(am, m));
-            if (grp_amb) {
-                code = am == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(am, double(QMAX)));
-                el_amb = 0xFFu;
-            }
-            if (el_amb) {
-                double sd = double(e4m3_to_f32(code));
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    if (!(el_amb >> k & 1u)) continue;
-                    double qd = fmin(fmax(rint(__ddiv_rn(r64[k], sd)), -127.0), 127.0);
-                    uint32_t u = uint32_t(int(qd)) & 0xFFu;
-                    if (k < 4) lo32 = (lo32 & ~(0xFFu << (k * 8))) | (u << (k * 8));
-                    else hi32 = (hi32 & ~(0xFFu << ((k - 4) * 8))) | (u << ((k - 4) * 8));
-                }
-            }
-        }
-        if (!valid) continue;
-        const int64_t pb = a.N * d;
-        *reinterpret_cast<uint2 *>(a.payload + p * pb + row * d + col) = make_uint2(lo32, hi32);
-        if ((lane & (glanes - 1)) == 0)
-            a.scales[p * (a.N * d / a.B) + (row * d + col) / a.B] = uint8_t(code);
-    }
+    stat = __reduce_or_sync(0xffffffffu, stat);
+    if (stat && lane == 0) atomicOr(a.status, int(stat));
 }
 
 // ------------------------------------------------------------------------
@@ -396,7 +373,7 @@ __global__ void k_quantize_generic_pack(const void *x, const uint16_t *cent, con
 }
 
 // ------------------------------------------------------------------------
-// K6 fast dequantize: d % 8 == 0, B % 8 == 0, S <= 4.
+// K6 dequantize (fast path: d/8 and B powers of two, B % 8 == 0, S <= 4)
 // ------------------------------------------------------------------------
 struct DequantArgs {
     const uint8_t *payload;
@@ -404,82 +381,146 @@ struct DequantArgs {
     const uint16_t *cent;
     const uint8_t *asg;
     void *out;
-    int64_t n_vec;
-    int64_t N;
-    int d, K, B;
+    uint32_t N;
+    int d, K, B, lvpr;
     int32_t *status;
+    uint32_t pb, ng, lgB;
+    TileArgs ta;
+    int v16;                // 16 channels per thread (k_dequant_v4)
 };
 
+// signed b-bit field k of w as an exact float: (u ^ sign) - sign via the
+// 1.5*2^23 magic (used by the rare f64 path)
 template <int BITS>
-__device__ __forceinline__ int unpack_q(uint64_t w, int k) {
+__device__ __forceinline__ float qfield(uint64_t w, int k) {
     constexpr uint32_t mask = (1u << BITS) - 1u, sign = 1u << (BITS - 1);
-    uint32_t u = uint32_t(w >> (k * BITS)) & mask;
-    return int(u ^ sign) - int(sign);
+    const uint32_t u = uint32_t(w >> (k * BITS)) & mask;
+    return __int_as_float(0x4B400000u | (u ^ sign)) - float(0xC00000u + sign);
 }
 
-// exact iff fl(a+b) == a+b; both checks are needed without knowing |a| vs |b|
-__device__ __forceinline__ bool add_exact(float a, float b, float s) {
-    return __fsub_rn(s, a) == b && __fsub_rn(s, b) == a;
+// q*s for field k in one FFMA: with u' = u ^ sign placed at the top of the f32
+// mantissa, f = 1 + u'/2^b and q = u' - 2^(b-1) = 2^b f - 3*2^(b-1), so
+// q*s = fma(f, 2^b s, -3*2^(b-1) s).  Both products of s are exact (s has 4
+// significant bits) and the fused result q*s is representable: exact.
+template <int BITS>
+__device__ __forceinline__ float qs_fma(uint64_t wx, int k, float s_hi, float s_off) {
+    constexpr uint32_t mask = (1u << BITS) - 1u;
+    uint32_t u;
+    if (k * BITS <= 23 - BITS) u = (uint32_t(wx) << (23 - BITS - k * BITS)) & (mask << (23 - BITS));
+    else u = uint32_t(wx >> (k * BITS - (23 - BITS))) & (mask << (23 - BITS));
+    return __fmaf_rn(__uint_as_float(u | 0x3F800000u), s_hi, s_off);
 }
 
-template <int BITS, int S, bool OUT_BF16>
-__global__ void __launch_bounds__(256) k_dequant_fast(DequantArgs a) {
-    const int d = a.d;
-    const int64_t vpr = d >> 3, vpp = a.N * vpr;
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    const int64_t pb = (a.N * d * BITS) >> 3, ng = a.N * d / a.B;
-    for (int64_t v = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < a.n_vec; v += stride) {
-        const int64_t p = v / vpp, rem = v - p * vpp, row = rem / vpr;
-        const int col = int(rem - row * vpr) << 3;
-        const int64_t e = row * d + col;
-        const uint8_t *pl = a.payload + p * pb + ((e * BITS) >> 3);
-        uint64_t w;
-        if constexpr (BITS == 2) w = __ldg(reinterpret_cast<const uint16_t *>(pl));
-        else if constexpr (BITS == 4) w = __ldg(reinterpret_cast<const uint32_t *>(pl));
-        else { uint2 t = __ldg(reinterpret_cast<const uint2 *>(pl)); w = uint64_t(t.x) | (uint64_t(t.y) << 32); }
-        const uint32_t sc = __ldg(a.scales + p * ng + e / a.B);
-        if (sc == 0x7Fu || sc == 0xFFu) atomicOr(a.status, QVG_STATUS_NAN_SCALE);
-        const float s = e4m3_to_f32(sc);
-        float y[8];
+// exact iff fl(x+y) == x+y; both checks are needed without knowing |x| vs |y|
+__device__ __forceinline__ bool add_exact(float x, float y, float s) {
+    return __fsub_rn(s, x) == y && __fsub_rn(s, y) == x;
+}
+
+// f64(q*s) + C_S[pi_S] + ... + C_1[pi_1] -> f32 for one channel, the
+// reference's order (Q/prq.py:123-132); out of line, rare.
+template <int BITS, int S>
+__device__ __noinline__ float exact_addback1(float qs, const uint16_t *cp, uint32_t col, uint32_t d,
+                                             int K, int a0, int a1, int a2, int a3) {
+    const int ai[4] = {a0, a1, a2, a3};
+    double acc = double(qs);
 #pragma unroll
-        for (int k = 0; k < 8; k++) y[k] = float(unpack_q<BITS>(w, k)) * s;  // exact
-        float c[S > 0 ? S : 1][8];
-        bool exact = true;
+    for (int t = S - 1; t >= 0; t--)
+        acc = __dadd_rn(acc, double(bf16_to_f32(cp[uint32_t(t * K + ai[t]) * d + col])));
+    return __double2float_rn(acc);
+}
+
+template <int BITS, int S, bool OBF16>
+__global__ void __launch_bounds__(256) k_dequant_v3(DequantArgs a) {
+    constexpr int SS = S > 0 ? S : 1;
+    const uint32_t d = uint32_t(a.d), N = a.N;
+    const int col = int(threadIdx.x & ((1u << a.lvpr) - 1u)) << 3;
+    const uint32_t rslot = threadIdx.x >> a.lvpr;
+    uint32_t stat = 0;
+    for (uint32_t T = blockIdx.x; T < a.ta.n_tiles; T += gridDim.x) {
+        const uint32_t p = a.ta.div_tpp.div(T);
+        const uint32_t i0 = (T - p * a.ta.tpp) * a.ta.rows_per_pass * kUnroll;
+        const uint64_t pN = uint64_t(p) * N;
+        const uint8_t *pp = a.payload + uint64_t(p) * a.pb;
+        const uint8_t *sp = a.scales + uint64_t(p) * a.ng;
+        const uint8_t *ap = a.asg + pN * S;
+        const uint16_t *cp = a.cent + uint64_t(p) * S * a.K * d;
+        uint64_t w[kUnroll];
+        uint32_t sc[kUnroll], ii[kUnroll];
+        int ai[kUnroll][SS];
+        uint4 cw[kUnroll][SS];
 #pragma unroll
-        for (int t = S - 1; t >= 0; t--) {
-            int ai = __ldg(a.asg + (p * S + t) * a.N + row);
-            if (ai >= a.K) { atomicOr(a.status, QVG_STATUS_BAD_ASSIGN); ai = 0; }
-            load_c8(a.cent + ((p * S + t) * a.K + ai) * int64_t(d) + col, c[t]);
+        for (int u = 0; u < kUnroll; u++) {
+            const uint32_t i = i0 + u * a.ta.rows_per_pass + rslot;
+            ii[u] = i < N ? i : N - 1;
+            const uint32_t e0 = ii[u] * d + col;
+            const uint8_t *pl = pp + ((e0 * BITS) >> 3);
+            if constexpr (BITS == 2) w[u] = __ldg(reinterpret_cast<const uint16_t *>(pl));
+            else if constexpr (BITS == 4) w[u] = __ldg(reinterpret_cast<const uint32_t *>(pl));
+            else { uint2 t = __ldg(reinterpret_cast<const uint2 *>(pl)); w[u] = uint64_t(t.x) | (uint64_t(t.y) << 32); }
+            sc[u] = __ldg(sp + (e0 >> a.lgB));
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                float s2 = __fadd_rn(y[k], c[t][k]);
-                if (t > 0) exact &= add_exact(y[k], c[t][k], s2);
-                y[k] = s2;
+            for (int t = 0; t < S; t++) {
+                int at = __ldg(ap + t * N + ii[u]);
+                if (at >= a.K) { stat |= QVG_STATUS_BAD_ASSIGN; at = 0; }
+                ai[u][t] = at;
             }
         }
-        if (!exact) {   // rare: some partial sum needed more than 24 bits
 #pragma unroll
-            for (int k = 0; k < 8; k++) {
-                double acc = double(float(unpack_q<BITS>(w, k)) * s);
+        for (int u = 0; u < kUnroll; u++)
 #pragma unroll
-                for (int t = S - 1; t >= 0; t--) acc = __dadd_rn(acc, double(c[t][k]));
-                y[k] = __double2float_rn(acc);
+            for (int t = 0; t < S; t++)
+                cw[u][t] = __ldg(reinterpret_cast<const uint4 *>(cp + uint32_t(t * a.K + ai[u][t]) * d + col));
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+            const bool valid = i0 + u * a.ta.rows_per_pass + rslot < N;
+            if ((sc[u] & 0x7Fu) == 0x7Fu) stat |= QVG_STATUS_NAN_SCALE;
+            const float s = e4m3_decode_fast(sc[u]);
+            constexpr uint64_t SIGNS = (BITS == 2 ? 0xAAAAull : (BITS == 4 ? 0x88888888ull : 0x8080808080808080ull));
+            const uint64_t wx = w[u] ^ SIGNS;
+            const float s_hi = s * float(1 << BITS), s_off = s * (-1.5f * float(1 << BITS));
+            float y[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) y[k] = qs_fma<BITS>(wx, k, s_hi, s_off);   // exact q*s
+            uint32_t inexact = 0;
+#pragma unroll
+            for (int t = S - 1; t >= 0; t--) {                 // reversed(stages)
+                const uint4 c4 = cw[u][t];
+                const float c[8] = {bf16_lo(c4.x), bf16_hi(c4.x), bf16_lo(c4.y), bf16_hi(c4.y),
+                                    bf16_lo(c4.z), bf16_hi(c4.z), bf16_lo(c4.w), bf16_hi(c4.w)};
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    const float s2 = __fadd_rn(y[k], c[k]);
+                    if (t > 0 && !add_exact(y[k], c[k], s2)) inexact |= 1u << k;  // non-final sums
+                    y[k] = s2;
+                }
             }
-        }
-        if constexpr (OUT_BF16) {
-            uint4 o;
-            __nv_bfloat162 h;
-            h = __floats2bfloat162_rn(y[0], y[1]); o.x = *reinterpret_cast<uint32_t *>(&h);
-            h = __floats2bfloat162_rn(y[2], y[3]); o.y = *reinterpret_cast<uint32_t *>(&h);
-            h = __floats2bfloat162_rn(y[4], y[5]); o.z = *reinterpret_cast<uint32_t *>(&h);
-            h = __floats2bfloat162_rn(y[6], y[7]); o.w = *reinterpret_cast<uint32_t *>(&h);
-            *reinterpret_cast<uint4 *>(static_cast<uint16_t *>(a.out) + (v << 3)) = o;
-        } else {
-            float4 *o = reinterpret_cast<float4 *>(static_cast<float *>(a.out) + (v << 3));
-            o[0] = make_float4(y[0], y[1], y[2], y[3]);
-            o[1] = make_float4(y[4], y[5], y[6], y[7]);
+            if (inexact) {  // rare: a partial sum needed > 24 bits -> f64 chain
+#pragma unroll
+                for (int k = 0; k < 8; k++)
+                    if (inexact >> k & 1u)
+                        y[k] = exact_addback1<BITS, S>(qs_fma<BITS>(wx, k, s_hi, s_off), cp, col + k, d, a.K,
+                                                       ai[u][0], ai[u][SS > 1 ? 1 : 0], ai[u][SS > 2 ? 2 : 0],
+                                                       ai[u][SS > 3 ? 3 : 0]);
+            }
+            if (!valid) continue;
+            const uint64_t o = (pN + ii[u]) * d + col;
+            if constexpr (OBF16) {
+                uint4 v;
+                __nv_bfloat162 h;
+                h = __floats2bfloat162_rn(y[0], y[1]); v.x = *reinterpret_cast<uint32_t *>(&h);
+                h = __floats2bfloat162_rn(y[2], y[3]); v.y = *reinterpret_cast<uint32_t *>(&h);
+                h = __floats2bfloat162_rn(y[4], y[5]); v.z = *reinterpret_cast<uint32_t *>(&h);
+                h = __floats2bfloat162_rn(y[6], y[7]); v.w = *reinterpret_cast<uint32_t *>(&h);
+                *reinterpret_cast<uint4 *>(static_cast<uint16_t *>(a.out) + o) = v;
+            } else {
+                float4 *op = reinterpret_cast<float4 *>(static_cast<float *>(a.out) + o);
+                op[0] = make_float4(y[0], y[1], y[2], y[3]);
+                op[1] = make_float4(y[4], y[5], y[6], y[7]);
+            }
         }
     }
+    stat = __reduce_or_sync(0xffffffffu, stat);
+    if (stat && (threadIdx.x & 31) == 0) atomicOr(a.status, int(stat));
 }
 
 // Generic exact dequantize: one thread per element, f64 add-back.
@@ -539,24 +580,373 @@ __global__ void k_unpack_codes(const uint8_t *in, int64_t n, int bits, int8_t *o
 }
 
 // ------------------------------------------------------------------------
+// v4 streaming kernels: 16 channels per thread-row (d % 16 == 0, B % 16 == 0),
+// halving the per-row index/address/decode overhead of the 8-channel layout,
+// with the per-element work written to split between the ALU and FMA pipes.
+// ------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));   // (a & b) | c
+    return d;
+}
+
+template <int BITS>
+struct Codes16 {                     // 16 b-bit fields
+    static constexpr int NW = BITS / 2;
+    uint32_t w[NW];
+};
+
+template <int BITS>
+__device__ __forceinline__ Codes16<BITS> load_codes16(const uint8_t *p) {
+    Codes16<BITS> c;
+    if constexpr (BITS == 2) c.w[0] = __ldg(reinterpret_cast<const uint32_t *>(p));
+    else if constexpr (BITS == 4) { uint2 v = __ldg(reinterpret_cast<const uint2 *>(p)); c.w[0] = v.x; c.w[1] = v.y; }
+    else { uint4 v = __ldg(reinterpret_cast<const uint4 *>(p)); c.w[0] = v.x; c.w[1] = v.y; c.w[2] = v.z; c.w[3] = v.w; }
+    return c;
+}
+
+// exact q*s of field k (see qs_fma): field moved to the top of the mantissa
+// with one shift + one LOP3, then one FFMA
+template <int BITS>
+__device__ __forceinline__ float qs16(const Codes16<BITS> &wx, int k, uint32_t mhi, uint32_t one,
+                                      float s_hi, float s_off) {
+    constexpr int POS = 23 - BITS;
+    const int bit = k * BITS, wi = bit >> 5, off = bit & 31;
+    const uint32_t v = off <= POS ? (wx.w[wi] << (POS - off)) : (wx.w[wi] >> (off - POS));
+    return __fmaf_rn(__uint_as_float(lop3_and_or(v, mhi, one)), s_hi, s_off);
+}
+
+__device__ __forceinline__ void cvt16(uint4 a, uint4 b, float c[16]) {
+    c[0] = bf16_lo(a.x); c[1] = bf16_hi(a.x); c[2] = bf16_lo(a.y); c[3] = bf16_hi(a.y);
+    c[4] = bf16_lo(a.z); c[5] = bf16_hi(a.z); c[6] = bf16_lo(a.w); c[7] = bf16_hi(a.w);
+    c[8] = bf16_lo(b.x); c[9] = bf16_hi(b.x); c[10] = bf16_lo(b.y); c[11] = bf16_hi(b.y);
+    c[12] = bf16_lo(b.z); c[13] = bf16_hi(b.z); c[14] = bf16_lo(b.w); c[15] = bf16_hi(b.w);
+}
+
+template <bool XBF16>
+__device__ __forceinline__ void load_x16(const uint8_t *xb, uint32_t e, float r[16]) {
+    if constexpr (XBF16) {
+        const uint4 *p = reinterpret_cast<const uint4 *>(xb + uint64_t(e) * 2);
+        cvt16(__ldg(p), __ldg(p + 1), r);
+    } else {
+        const float4 *p = reinterpret_cast<const float4 *>(xb + uint64_t(e) * 4);
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const float4 v = __ldg(p + j);
+            r[4 * j] = v.x; r[4 * j + 1] = v.y; r[4 * j + 2] = v.z; r[4 * j + 3] = v.w;
+        }
+    }
+}
+
+template <int BITS, int S, bool OBF16>
+__global__ void __launch_bounds__(256) k_dequant_v4(DequantArgs a) {
+    constexpr int SS = S > 0 ? S : 1;
+    constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
+    const uint32_t mhi = ((1u << BITS) - 1u) << (23 - BITS), one = 0x3F800000u;
+    const uint32_t d = uint32_t(a.d), N = a.N;
+    const int col = int(threadIdx.x & ((1u << a.lvpr) - 1u)) << 4;
+    const uint32_t rslot = threadIdx.x >> a.lvpr;
+    bool bad_scale = false, bad_asg = false;
+    for (uint32_t T = blockIdx.x; T < a.ta.n_tiles; T += gridDim.x) {
+        const uint32_t p = a.ta.div_tpp.div(T);
+        const uint32_t i0 = (T - p * a.ta.tpp) * a.ta.rows_per_pass * kUnroll;
+        const uint64_t pN = uint64_t(p) * N;
+        const uint8_t *pp = a.payload + uint64_t(p) * a.pb;
+        const uint8_t *sp = a.scales + uint64_t(p) * a.ng;
+        const uint8_t *ap = a.asg + pN * S;
+        const uint16_t *cp = a.cent + uint64_t(p) * S * a.K * d;
+        Codes16<BITS> w[kUnroll];
+        uint32_t sc[kUnroll], ii[kUnroll];
+        int ai[kUnroll][SS];
+        uint4 cw[kUnroll][SS][2];
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+            const uint32_t i = i0 + u * a.ta.rows_per_pass + rslot;
+            ii[u] = i < N ? i : N - 1;
+            const uint32_t e0 = ii[u] * d + col;
+            w[u] = load_codes16<BITS>(pp + ((e0 * BITS) >> 3));
+            sc[u] = __ldg(sp + (e0 >> a.lgB));
+#pragma unroll
+            for (int t = 0; t < S; t++) {
+                int at = __ldg(ap + t * N + ii[u]);
+                bad_asg |= at >= a.K;
+                ai[u][t] = at < a.K ? at : 0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+            for (int t = 0; t < S; t++) {
+                const uint4 *c4 = reinterpret_cast<const uint4 *>(cp + uint32_t(t * a.K + ai[u][t]) * d + col);
+                cw[u][t][0] = __ldg(c4);
+                cw[u][t][1] = __ldg(c4 + 1);
+            }
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+            const bool valid = i0 + u * a.ta.rows_per_pass + rslot < N;
+            bad_scale |= (sc[u] & 0x7Fu) == 0x7Fu;
+            const float s = e4m3_decode_fast(sc[u]);
+            Codes16<BITS> wx;
+#pragma unroll
+            for (int j = 0; j < Codes16<BITS>::NW; j++) wx.w[j] = w[u].w[j] ^ SIGNS;
+            const float s_hi = s * float(1 << BITS), s_off = s * (-1.5f * float(1 << BITS));
+            float y[16];
+#pragma unroll
+            for (int k = 0; k < 16; k++) y[k] = qs16<BITS>(wx, k, mhi, one, s_hi, s_off);   // exact
+            bool inexact = false;
+#pragma unroll
+            for (int t = S - 1; t >= 0; t--) {                 // reversed(stages)
+                float c[16];
+                cvt16(cw[u][t][0], cw[u][t][1], c);
+#pragma unroll
+                for (int k = 0; k < 16; k++) {
+                    const float s2 = __fadd_rn(y[k], c[k]);
+                    if (t > 0) inexact |= (__fsub_rn(s2, y[k]) != c[k]) | (__fsub_rn(s2, c[k]) != y[k]);
+                    y[k] = s2;
+                }
+            }
+            if (inexact) {  // rare: a non-final partial sum needed > 24 bits -> f64 chain
+#pragma unroll
+                for (int k = 0; k < 16; k++)
+                    y[k] = exact_addback1<BITS, S>(qs16<BITS>(wx, k, mhi, one, s_hi, s_off), cp, col + k, d,
+                                                   a.K, ai[u][0], ai[u][SS > 1 ? 1 : 0],
+                                                   ai[u][SS > 2 ? 2 : 0], ai[u][SS > 3 ? 3 : 0]);
+            }
+            if (!valid) continue;
+            const uint64_t o = (pN + ii[u]) * d + col;
+            if constexpr (OBF16) {
+                uint32_t v[8];
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    __nv_bfloat162 h = __floats2bfloat162_rn(y[2 * j], y[2 * j + 1]);
+                    v[j] = *reinterpret_cast<uint32_t *>(&h);
+                }
+                uint4 *op = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(a.out) + o);
+                op[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                op[1] = make_uint4(v[4], v[5], v[6], v[7]);
+            } else {
+                float4 *op = reinterpret_cast<float4 *>(static_cast<float *>(a.out) + o);
+#pragma unroll
+                for (int j = 0; j < 4; j++) op[j] = make_float4(y[4 * j], y[4 * j + 1], y[4 * j + 2], y[4 * j + 3]);
+            }
+        }
+    }
+    const uint32_t stat = (bad_scale ? QVG_STATUS_NAN_SCALE : 0u) | (bad_asg ? QVG_STATUS_BAD_ASSIGN : 0u);
+    const uint32_t all = __reduce_or_sync(0xffffffffu, stat);
+    if (all && (threadIdx.x & 31) == 0) atomicOr(a.status, int(all));
+}
+
+template <int BITS, int S, bool XBF16>
+__global__ void __launch_bounds__(256) k_quantize_v4(QuantArgs a) {
+    constexpr int QMAX = (1 << (BITS - 1)) - 1;
+    constexpr int SS = S > 0 ? S : 1;
+    const uint32_t d = uint32_t(a.d), N = a.N;
+    const int col = int(threadIdx.x & ((1u << a.lvpr) - 1u)) << 4;
+    const uint32_t rslot = threadIdx.x >> a.lvpr;
+    const int glanes = 1 << a.gshift;     // B / 16 lanes per group
+    const int lane = threadIdx.x & 31;
+    bool nonfinite = false;
+    for (uint32_t T = blockIdx.x; T < a.ta.n_tiles; T += gridDim.x) {
+        const uint32_t p = a.ta.div_tpp.div(T);
+        const uint32_t i0 = (T - p * a.ta.tpp) * a.ta.rows_per_pass * kUnroll;
+        const uint64_t pN = uint64_t(p) * N;
+        const uint8_t *xb = static_cast<const uint8_t *>(a.x) + pN * d * (XBF16 ? 2 : 4);
+        const uint8_t *ap = a.asg + pN * S;
+        const uint16_t *cp = a.cent + uint64_t(p) * S * a.K * d;
+        float r[kUnroll][16];
+        uint32_t ii[kUnroll];
+        int ai[kUnroll][SS];
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+            const uint32_t i = i0 + u * a.ta.rows_per_pass + rslot;
+            ii[u] = i < N ? i : N - 1;
+            load_x16<XBF16>(xb, ii[u] * d + col, r[u]);
+#pragma unroll
+            for (int t = 0; t < S; t++) ai[u][t] = __ldg(ap + t * N + ii[u]);
+        }
+        float eb[kUnroll], am[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+#pragma unroll
+            for (int k = 0; k < 16; k++) nonfinite |= !(fabsf(r[u][k]) <= 3.402823466e38f);
+            float e = 0.f;
+#pragma unroll
+            for (int t = 0; t < S; t++) {
+                const uint4 *c4 = reinterpret_cast<const uint4 *>(cp + uint32_t(t * a.K + ai[u][t]) * d + col);
+                float c[16];
+                cvt16(__ldg(c4), __ldg(c4 + 1), c);
+#pragma unroll
+                for (int k = 0; k < 16; k++) r[u][k] = __fsub_rn(r[u][k], c[k]);
+                if (t < S - 1) {
+                    float m = 0.f;
+#pragma unroll
+                    for (int k = 0; k < 16; k++) m = fmaxf(m, fabsf(r[u][k]));
+                    e = __fadd_ru(e, m);
+                }
+            }
+            float mx = 0.f;
+#pragma unroll
+            for (int k = 0; k < 16; k++) mx = fmaxf(mx, fabsf(r[u][k]));
+            eb[u] = S > 0 ? __fadd_ru(e, mx) : 0.f;
+            am[u] = mx;
+        }
+        for (int m = 1; m < glanes; m <<= 1) {
+#pragma unroll
+            for (int u = 0; u < kUnroll; u++) {
+                am[u] = fmaxf(am[u], __shfl_xor_sync(0xffffffffu, am[u], m));
+                eb[u] = fmaxf(eb[u], __shfl_xor_sync(0xffffffffu, eb[u], m));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+            const bool valid = i0 + u * a.ta.rows_per_pass + rslot < N;
+            // |r_f32 - r_ref| <= 2^-24 sum_t|r_t| (f32 chain) + 2^-53 (.) (the
+            // reference's f64 chain) <= 2^-22 * sum_t max|r_t|: factor-2 margin
+            const float E = __fmul_ru(eb[u], 2.38418579e-7f);
+            uint32_t code;
+            bool camb = false;
+            if (am[u] == 0.f && E == 0.f) code = 0x38u;
+            else {
+                const float lo = __fsub_rd(am[u], E), hi = __fadd_ru(am[u], E);
+                if (lo > 0.f) code = scale_code<QMAX>(lo, hi, camb);
+                else { code = 0x38u; camb = true; }
+            }
+            camb &= valid;
+            auto exact_r = [&](int k) {
+                return exact_residual<XBF16, S>(xb, cp, ii[u] * d + col + k, col + k, d, a.K, ai[u][0],
+                                                ai[u][SS > 1 ? 1 : 0], ai[u][SS > 2 ? 2 : 0],
+                                                ai[u][SS > 3 ? 3 : 0]);
+            };
+            if (__any_sync(0xffffffffu, camb)) {          // exact scale (rare)
+                // every element whose exact |r| could be the group max
+                const float thr = __fsub_rd(am[u], __fmul_ru(E, 2.f));
+                uint32_t cand = 0;
+#pragma unroll
+                for (int k = 0; k < 16; k++) cand |= (camb && fabsf(r[u][k]) >= thr) ? 1u << k : 0u;
+                double a64 = 0.0;
+                while (cand) {
+                    const int k = __ffs(cand) - 1;
+                    cand &= cand - 1;
+                    a64 = fmax(a64, fabs(exact_r(k)));
+                }
+                for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
+                if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
+            }
+            const float s = e4m3_decode_fast(code);
+            uint32_t b32[BITS / 2];
+#pragma unroll
+            for (int j = 0; j < BITS / 2; j++) b32[j] = 0;
+            bool amb = false;
+            if constexpr (QMAX == 1) {
+                // q != 0 <=> RN64(|r|/s) > 0.5 <=> |r| > s/2 (exact r); ambiguous iff
+                // the exact r may lie on the other side: ||r~| - s/2| <= E.  The
+                // difference is exact (Sterbenz) whenever it is that small, given
+                // E < s/8; otherwise every element is rechecked.
+                const float half = 0.5f * s;
+                amb = !(E < 0.125f * s);
+#pragma unroll
+                for (int k = 0; k < 16; k++) {
+                    const float av = fabsf(r[u][k]);
+                    amb |= fabsf(av - half) <= E;
+                    const uint32_t f = av > half ? ((__float_as_uint(r[u][k]) >> 30) | 1u) : 0u;   // 1 or 3
+                    b32[0] |= f << (2 * k);
+                }
+            } else {
+                const float inv = __frcp_rn(s);
+#pragma unroll
+                for (int k = 0; k < 16; k++) {
+                    const float av = fabsf(r[u][k]);
+                    const float t = av * inv;
+                    const float fl = floorf(t);
+                    const float hb = (fl + 0.5f) * s;                    // exact
+                    const float w = __fmaf_ru(hb, 2.38418579e-7f, E);
+                    amb |= fl < float(QMAX) && av >= __fsub_rd(hb, w) && av <= __fadd_ru(hb, w);
+                    int q = min(int(rintf(t)), QMAX);
+                    if (r[u][k] < 0.f) q = -q;
+                    b32[(k * BITS) >> 5] |= (uint32_t(q) & ((1u << BITS) - 1u)) << ((k * BITS) & 31);
+                }
+            }
+            amb &= valid;
+            if (__any_sync(0xffffffffu, amb) && amb) {   // exact codes (rare)
+                // re-derive which elements sit in an error window, then fix them
+                uint32_t todo = 0;
+                const bool all = !(E < 0.125f * s);
+                const float inv = __frcp_rn(s);
+#pragma unroll
+                for (int k = 0; k < 16; k++) {
+                    const float av = fabsf(r[u][k]);
+                    bool in;
+                    if constexpr (QMAX == 1) in = fabsf(av - 0.5f * s) <= E;
+                    else {
+                        const float fl = floorf(av * inv);
+                        const float hb = (fl + 0.5f) * s;
+                        const float w = __fmaf_ru(hb, 2.38418579e-7f, E);
+                        in = fl < float(QMAX) && av >= __fsub_rd(hb, w) && av <= __fadd_ru(hb, w);
+                    }
+                    todo |= (all || in) ? 1u << k : 0u;
+                }
+                while (todo) {
+                    const int k = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    const uint32_t q = exact_code<QMAX>(exact_r(k), s) & ((1u << BITS) - 1u);
+                    const int sh = (k * BITS) & 31, wi = (k * BITS) >> 5;
+#pragma unroll
+                    for (int j = 0; j < BITS / 2; j++)
+                        if (j == wi) b32[j] = (b32[j] & ~(((1u << BITS) - 1u) << sh)) | (q << sh);
+                }
+            }
+            if (!valid) continue;
+            const uint32_t e0 = ii[u] * d + col;
+            uint8_t *pl = a.payload + uint64_t(p) * a.pb + ((e0 * BITS) >> 3);
+            if constexpr (BITS == 2) *reinterpret_cast<uint32_t *>(pl) = b32[0];
+            else if constexpr (BITS == 4) *reinterpret_cast<uint2 *>(pl) = make_uint2(b32[0], b32[1]);
+            else *reinterpret_cast<uint4 *>(pl) = make_uint4(b32[0], b32[1], b32[2], b32[3]);
+            if ((lane & (glanes - 1)) == 0) a.scales[uint64_t(p) * a.ng + (e0 >> a.lgB)] = uint8_t(code);
+        }
+    }
+    const uint32_t all = __reduce_or_sync(0xffffffffu, nonfinite ? uint32_t(QVG_STATUS_NONFINITE) : 0u);
+    if (all && lane == 0) atomicOr(a.status, int(all));
+}
+
+// ------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------
 static int grid_for(int64_t work, int block) {
     int64_t g = (work + block - 1) / block;
-    int64_t cap = 148LL * 16;  // persistent-ish: 16 CTAs of 256 per SM max
+    int64_t cap = 148LL * 16;
     return int(g < 1 ? 1 : (g > cap ? cap : g));
+}
+
+static int ilog2(int v) { int l = 0; while ((1 << l) < v) l++; return l; }
+
+bool quant_fast_ok(int64_t P, int64_t N, int d, int B, int S) {
+    const int vpr = d / 8;
+    return d % 8 == 0 && (vpr & (vpr - 1)) == 0 && vpr <= 32 && B % 8 == 0 &&
+           ((B / 8) & (B / 8 - 1)) == 0 && B / 8 <= vpr && S <= 4 && P * N < (int64_t(1) << 32) &&
+           N * d < (int64_t(1) << 32);
+}
+
+static TileArgs make_tiles(int64_t P, int64_t N, int lvpr) {
+    const uint32_t rpp = 256u >> lvpr;
+    const uint32_t tpp = uint32_t((N + int64_t(rpp) * kUnroll - 1) / (int64_t(rpp) * kUnroll));
+    return TileArgs{uint32_t(P * tpp), tpp, make_fastdiv(tpp), rpp};
+}
+
+static int tile_grid(const TileArgs &t) {
+    // persistent: <= 148 SMs x 4 resident CTAs of 256 threads
+    return int(t.n_tiles < 148u * 4u ? t.n_tiles : 148u * 4u);
 }
 
 template <int BITS, int S>
 static void launch_quant_fast(const QuantArgs &a, bool xbf16, cudaStream_t st) {
-    int g = grid_for(a.n_vec, 256);
-    if constexpr (BITS == 8) {
-        if (xbf16) k_quantize_fast8<S, true><<<g, 256, 0, st>>>(a);
-        else k_quantize_fast8<S, false><<<g, 256, 0, st>>>(a);
-    } else {
-        if (xbf16) k_quantize_fast<BITS, S, true><<<g, 256, 0, st>>>(a);
-        else k_quantize_fast<BITS, S, false><<<g, 256, 0, st>>>(a);
+    const int g = tile_grid(a.ta);
+    if (a.v16) {
+        if (xbf16) k_quantize_v4<BITS, S, true><<<g, 256, 0, st>>>(a);
+        else k_quantize_v4<BITS, S, false><<<g, 256, 0, st>>>(a);
+        return;
     }
+    if (xbf16) k_quantize_v3<BITS, S, true><<<g, 256, 0, st>>>(a);
+    else k_quantize_v3<BITS, S, false><<<g, 256, 0, st>>>(a);
 }
 
 template <int BITS>
@@ -570,19 +960,18 @@ static void dispatch_quant_s(const QuantArgs &a, int S, bool xbf16, cudaStream_t
     }
 }
 
-bool quant_fast_ok(int d, int B, int S) {
-    return d % 8 == 0 && B % 8 == 0 && B <= 256 && ((B / 8) & (B / 8 - 1)) == 0 && S <= 4;
-}
-
 int launch_quantize(const void *x, int xdtype, int64_t P, int64_t N, int d, int bits, int B, int S,
                     int K, const uint16_t *cent, const uint8_t *asg, uint8_t *payload,
                     uint8_t *scales, int32_t *status, cudaStream_t st) {
     const bool xbf16 = xdtype == QVG_DTYPE_BF16;
-    if (xdtype != QVG_DTYPE_F64 && quant_fast_ok(d, B, S)) {
-        QuantArgs a{x, cent, asg, payload, scales, P * N * d / 8, N, d, K, B, 0, status};
-        int gl = B / 8, gs = 0;
-        while ((1 << gs) < gl) gs++;
-        a.gshift = gs;
+    if (xdtype != QVG_DTYPE_F64 && quant_fast_ok(P, N, d, B, S)) {
+        // 16 channels per thread when groups and rows split into 16-channel lanes
+        const bool v16 = d % 16 == 0 && B % 16 == 0 && ((d / 16) & (d / 16 - 1)) == 0;
+        const int lvpr = v16 ? ilog2(d / 16) : ilog2(d / 8);
+        QuantArgs a{x, cent, asg, payload, scales, uint32_t(N), d, K, B, lvpr,
+                    v16 ? ilog2(B / 16) : ilog2(B / 8), status,
+                    uint32_t(N * d * bits / 8), uint32_t(N * d / B), uint32_t(ilog2(B)),
+                    make_tiles(P, N, lvpr), v16 ? 1 : 0};
         if (bits == 2) dispatch_quant_s<2>(a, S, xbf16, st);
         else if (bits == 4) dispatch_quant_s<4>(a, S, xbf16, st);
         else dispatch_quant_s<8>(a, S, xbf16, st);
@@ -602,11 +991,26 @@ int launch_quantize(const void *x, int xdtype, int64_t P, int64_t N, int d, int 
     return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
 }
 
+int launch_pack(const int8_t *q, int64_t n, int bits, uint8_t *out, int32_t *status, cudaStream_t st) {
+    if (n > 0) k_pack_codes<<<grid_for((n * bits + 7) / 8, 256), 256, 0, st>>>(q, n, bits, out, status);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+
+int launch_unpack(const uint8_t *in, int64_t n, int bits, int8_t *out, cudaStream_t st) {
+    if (n > 0) k_unpack_codes<<<grid_for(n, 256), 256, 0, st>>>(in, n, bits, out);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+
 template <int BITS, int S>
 static void launch_deq_fast(const DequantArgs &a, bool obf16, cudaStream_t st) {
-    int g = grid_for(a.n_vec, 256);
-    if (obf16) k_dequant_fast<BITS, S, true><<<g, 256, 0, st>>>(a);
-    else k_dequant_fast<BITS, S, false><<<g, 256, 0, st>>>(a);
+    const int g = tile_grid(a.ta);
+    if (a.v16) {
+        if (obf16) k_dequant_v4<BITS, S, true><<<g, 256, 0, st>>>(a);
+        else k_dequant_v4<BITS, S, false><<<g, 256, 0, st>>>(a);
+        return;
+    }
+    if (obf16) k_dequant_v3<BITS, S, true><<<g, 256, 0, st>>>(a);
+    else k_dequant_v3<BITS, S, false><<<g, 256, 0, st>>>(a);
 }
 
 template <int BITS>
@@ -620,22 +1024,18 @@ static void dispatch_deq_s(const DequantArgs &a, int S, bool obf16, cudaStream_t
     }
 }
 
-int launch_pack(const int8_t *q, int64_t n, int bits, uint8_t *out, int32_t *status, cudaStream_t st) {
-    if (n > 0) k_pack_codes<<<grid_for((n * bits + 7) / 8, 256), 256, 0, st>>>(q, n, bits, out, status);
-    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
-}
-
-int launch_unpack(const uint8_t *in, int64_t n, int bits, int8_t *out, cudaStream_t st) {
-    if (n > 0) k_unpack_codes<<<grid_for(n, 256), 256, 0, st>>>(in, n, bits, out);
-    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
-}
-
 int launch_dequantize(const uint8_t *payload, const uint8_t *scales, const uint16_t *cent,
                       const uint8_t *asg, int64_t P, int64_t N, int d, int bits, int B, int S, int K,
                       void *out, int odtype, int32_t *status, cudaStream_t st) {
     const bool obf16 = odtype == QVG_DTYPE_BF16;
-    if (d % 8 == 0 && B % 8 == 0 && S <= 4) {
-        DequantArgs a{payload, scales, cent, asg, out, P * N * d / 8, N, d, K, B, status};
+    const int vpr = d / 8;
+    if (d % 8 == 0 && (vpr & (vpr - 1)) == 0 && vpr <= 32 && B % 8 == 0 && (B & (B - 1)) == 0 &&
+        S <= 4 && P * N < (int64_t(1) << 32) && N * d < (int64_t(1) << 32)) {
+        const bool v16 = d % 16 == 0 && B % 16 == 0 && ((d / 16) & (d / 16 - 1)) == 0;
+        const int lvpr = v16 ? ilog2(d / 16) : ilog2(vpr);
+        DequantArgs a{payload, scales, cent, asg, out, uint32_t(N), d, K, B, lvpr, status,
+                      uint32_t(N * d * bits / 8), uint32_t(N * d / B), uint32_t(ilog2(B)),
+                      make_tiles(P, N, lvpr), v16 ? 1 : 0};
         if (bits == 2) dispatch_deq_s<2>(a, S, obf16, st);
         else if (bits == 4) dispatch_deq_s<4>(a, S, obf16, st);
         else dispatch_deq_s<8>(a, S, obf16, st);
