@@ -105,8 +105,22 @@ struct TileArgs {
 template <int QMAX>
 __device__ __forceinline__ float grid_val(uint32_t code) { return e4m3_to_f32(code) * float(QMAX); }
 
+// E4M3 "up" code without branches (v >= 0 finite, saturating at 448)
+__device__ __forceinline__ uint32_t e4m3_ceil_f32_bf(float v) {
+    const float vc = fminf(v, 448.f);
+    const uint32_t sub = uint32_t(ceilf(vc * 512.f));                        // subnormal steps
+    const uint32_t nrm = (((__float_as_uint(vc) + 0xFFFFFu) >> 20) - (120u << 3));
+    return vc < 0.015625f ? sub : nrm;
+}
+
 template <int QMAX>
 __device__ __forceinline__ uint32_t scale_code(float lo, float hi, bool &amb) {
+    if constexpr (QMAX == 1) {
+        // code(A) for A in [lo, hi] is certain iff ceil(lo) == ceil(hi)
+        const uint32_t c = e4m3_ceil_f32_bf(hi);
+        amb = c != e4m3_ceil_f32_bf(lo);
+        return c;
+    }
     uint32_t c = e4m3_ceil_f32(QMAX == 1 ? hi : __fmul_ru(hi, 1.0f / QMAX * 1.0000002f));
     if (QMAX > 1) {   // make c the exact ceil code of hi/QMAX
         while (c > 1 && hi <= grid_val<QMAX>(c - 1)) c--;
@@ -159,7 +173,10 @@ struct QuantArgs {
     int32_t *status;
     uint32_t pb, ng, lgB;   // payload bytes / scale bytes per plane, log2(B)
     TileArgs ta;
-    int v16;                // 16 channels per thread (k_quantize_v4)
+    int v16;                // 16 channels per thread (k_quantize_v4/v5)
+    int v5;                 // CTAs per SM for k_quantize_v5 (0: not used)
+    uint32_t P;
+    uint32_t one;           // always 1 (see k_quantize_v5)
 };
 
 template <int BITS, int S, bool XBF16>
@@ -386,7 +403,9 @@ struct DequantArgs {
     int32_t *status;
     uint32_t pb, ng, lgB;
     TileArgs ta;
-    int v16;                // 16 channels per thread (k_dequant_v4)
+    int v16;                // 16 channels per thread (k_dequant_v4/v5)
+    int v5;                 // CTAs per SM for k_dequant_v5 (0: not used)
+    uint32_t P;
 };
 
 // signed b-bit field k of w as an exact float: (u ^ sign) - sign via the
@@ -909,6 +928,349 @@ __global__ void __launch_bounds__(256) k_quantize_v4(QuantArgs a) {
 }
 
 // ------------------------------------------------------------------------
+// v5: persistent CTAs over planes, centroid tables TMA-staged in shared memory
+// (cp.async.bulk, double-buffered on mbarriers) so the per-token centroid
+// gather is an LDS instead of a dependent L2 round trip.
+// ------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return uint32_t(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+struct PlaneLoop {
+    uint32_t P, tbytes;          // planes, centroid-table bytes per plane (S*K*d*2)
+};
+
+// issue the bulk copy of plane p's centroid table into buffer b
+__device__ __forceinline__ void stage_table(const uint16_t *cent, uint32_t p, uint32_t tbytes,
+                                            uint16_t *buf, uint64_t *bar) {
+    mbar_arrive_expect_tx(bar, tbytes);
+    bulk_g2s(buf, reinterpret_cast<const uint8_t *>(cent) + uint64_t(p) * tbytes, tbytes, bar);
+}
+
+template <int BITS, int S, bool OBF16>
+__global__ void __launch_bounds__(256) k_dequant_v5(DequantArgs a, PlaneLoop pl) {
+    constexpr int SS = S > 0 ? S : 1;
+    constexpr int kUnroll = 2;     // rows in flight per thread
+    constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bars[2];
+    uint16_t *const tab0 = reinterpret_cast<uint16_t *>(smem);
+    uint16_t *const tab1 = reinterpret_cast<uint16_t *>(smem + pl.tbytes);
+    const uint32_t mhi = ((1u << BITS) - 1u) << (23 - BITS), one = 0x3F800000u;
+    const uint32_t d = uint32_t(a.d), N = a.N;
+    const int col = int(threadIdx.x & ((1u << a.lvpr) - 1u)) << 4;
+    const uint32_t rslot = threadIdx.x >> a.lvpr, rpp = 256u >> a.lvpr;
+    bool bad_scale = false, bad_asg = false;
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (S > 0 && threadIdx.x == 0 && blockIdx.x < pl.P) stage_table(a.cent, blockIdx.x, pl.tbytes, tab0, &bars[0]);
+    uint32_t j = 0;
+    for (uint32_t p = blockIdx.x; p < pl.P; p += gridDim.x, j++) {
+        const uint32_t b = j & 1u;
+        // prefetch the next plane's table into the other buffer (freed by the
+        // __syncthreads that ended the previous plane)
+        if (S > 0 && threadIdx.x == 0 && p + gridDim.x < pl.P)
+            stage_table(a.cent, p + gridDim.x, pl.tbytes, b ? tab0 : tab1, b ? &bars[0] : &bars[1]);
+        if (S > 0) mbar_wait(b ? &bars[1] : &bars[0], (j >> 1) & 1u);
+        const uint16_t *ct = b ? tab1 : tab0;
+        const uint64_t pN = uint64_t(p) * N;
+        const uint8_t *pp = a.payload + uint64_t(p) * a.pb;
+        const uint8_t *sp = a.scales + uint64_t(p) * a.ng;
+        const uint8_t *ap = a.asg + pN * S;
+        for (uint32_t i0 = 0; i0 < N; i0 += rpp * kUnroll) {       // CTA-uniform
+            Codes16<BITS> w[kUnroll];
+            uint32_t sc[kUnroll], ii[kUnroll];
+            int ai[kUnroll][SS];
+#pragma unroll
+            for (int u = 0; u < kUnroll; u++) {
+                const uint32_t i = i0 + u * rpp + rslot;
+                ii[u] = i < N ? i : N - 1;
+                const uint32_t e0 = ii[u] * d + col;
+                w[u] = load_codes16<BITS>(pp + ((e0 * BITS) >> 3));
+                sc[u] = __ldg(sp + (e0 >> a.lgB));
+#pragma unroll
+                for (int t = 0; t < S; t++) {
+                    int at = __ldg(ap + t * N + ii[u]);
+                    bad_asg |= at >= a.K;
+                    ai[u][t] = at < a.K ? at : 0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; u++) {
+                const bool valid = i0 + u * rpp + rslot < N;
+                bad_scale |= (sc[u] & 0x7Fu) == 0x7Fu;
+                const float s = e4m3_decode_fast(sc[u]);
+                Codes16<BITS> wx;
+#pragma unroll
+                for (int q = 0; q < Codes16<BITS>::NW; q++) wx.w[q] = w[u].w[q] ^ SIGNS;
+                const float s_hi = s * float(1 << BITS), s_off = s * (-1.5f * float(1 << BITS));
+                float y[16];
+#pragma unroll
+                for (int k = 0; k < 16; k++) y[k] = qs16<BITS>(wx, k, mhi, one, s_hi, s_off);   // exact
+                bool inexact = false;
+#pragma unroll
+                for (int t = S - 1; t >= 0; t--) {                 // reversed(stages)
+                    const uint4 *c4 = reinterpret_cast<const uint4 *>(ct + uint32_t(t * a.K + ai[u][t]) * d + col);
+                    float c[16];
+                    cvt16(c4[0], c4[1], c);
+#pragma unroll
+                    for (int k = 0; k < 16; k++) {
+                        const float s2 = __fadd_rn(y[k], c[k]);
+                        if (t > 0) inexact |= (__fsub_rn(s2, y[k]) != c[k]) | (__fsub_rn(s2, c[k]) != y[k]);
+                        y[k] = s2;
+                    }
+                }
+                if (inexact) {  // rare: a non-final partial sum needed > 24 bits -> f64 chain
+#pragma unroll
+                    for (int k = 0; k < 16; k++)
+                        y[k] = exact_addback1<BITS, S>(qs16<BITS>(wx, k, mhi, one, s_hi, s_off), ct, col + k, d,
+                                                       a.K, ai[u][0], ai[u][SS > 1 ? 1 : 0],
+                                                       ai[u][SS > 2 ? 2 : 0], ai[u][SS > 3 ? 3 : 0]);
+                }
+                if (!valid) continue;
+                const uint64_t o = (pN + ii[u]) * d + col;
+                if constexpr (OBF16) {
+                    uint32_t v[8];
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        __nv_bfloat162 h = __floats2bfloat162_rn(y[2 * q], y[2 * q + 1]);
+                        v[q] = *reinterpret_cast<uint32_t *>(&h);
+                    }
+                    uint4 *op = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(a.out) + o);
+                    op[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                    op[1] = make_uint4(v[4], v[5], v[6], v[7]);
+                } else {
+                    float4 *op = reinterpret_cast<float4 *>(static_cast<float *>(a.out) + o);
+#pragma unroll
+                    for (int q = 0; q < 4; q++) op[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
+                }
+            }
+        }
+        __syncthreads();    // everyone is done with tab[b] before it is refilled
+    }
+    const uint32_t stat = (bad_scale ? QVG_STATUS_NAN_SCALE : 0u) | (bad_asg ? QVG_STATUS_BAD_ASSIGN : 0u);
+    const uint32_t all = __reduce_or_sync(0xffffffffu, stat);
+    if (all && (threadIdx.x & 31) == 0) atomicOr(a.status, int(all));
+}
+
+template <int BITS, int S, bool XBF16>
+__global__ void __launch_bounds__(256) k_quantize_v5(QuantArgs a, PlaneLoop pl) {
+    constexpr int QMAX = (1 << (BITS - 1)) - 1;
+    constexpr int SS = S > 0 ? S : 1;
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bars[2];
+    uint16_t *const tab0 = reinterpret_cast<uint16_t *>(smem);
+    uint16_t *const tab1 = reinterpret_cast<uint16_t *>(smem + pl.tbytes);
+    const uint32_t d = uint32_t(a.d), N = a.N;
+    const int col = int(threadIdx.x & ((1u << a.lvpr) - 1u)) << 4;
+    const uint32_t rslot = threadIdx.x >> a.lvpr, rpp = 256u >> a.lvpr;
+    const int glanes = 1 << a.gshift;
+    const int lane = threadIdx.x & 31;
+    bool nonfinite = false;
+    if (threadIdx.x == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (S > 0 && threadIdx.x == 0 && blockIdx.x < pl.P) stage_table(a.cent, blockIdx.x, pl.tbytes, tab0, &bars[0]);
+    uint32_t j = 0;
+    for (uint32_t p = blockIdx.x; p < pl.P; p += gridDim.x, j++) {
+        const uint32_t b = j & 1u;
+        if (S > 0 && threadIdx.x == 0 && p + gridDim.x < pl.P)
+            stage_table(a.cent, p + gridDim.x, pl.tbytes, b ? tab0 : tab1, b ? &bars[0] : &bars[1]);
+        if (S > 0) mbar_wait(b ? &bars[1] : &bars[0], (j >> 1) & 1u);
+        const uint16_t *ct = b ? tab1 : tab0;
+        const uint64_t pN = uint64_t(p) * N;
+        const uint8_t *xb = static_cast<const uint8_t *>(a.x) + pN * d * (XBF16 ? 2 : 4);
+        const uint8_t *ap = a.asg + pN * S;
+        for (uint32_t i0 = 0; i0 < N; i0 += rpp * kUnroll) {
+            float r[kUnroll][16];
+            uint32_t ii[kUnroll];
+            int ai[kUnroll][SS];
+#pragma unroll
+            for (int u = 0; u < kUnroll; u++) {
+                const uint32_t i = i0 + u * rpp + rslot;
+                ii[u] = i < N ? i : N - 1;
+                load_x16<XBF16>(xb, ii[u] * d + col, r[u]);
+#pragma unroll
+                for (int t = 0; t < S; t++) ai[u][t] = __ldg(ap + t * N + ii[u]);
+            }
+            float eb[kUnroll], am[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; u++) {
+                // e = sum_t sum_k |r_t,k| bounds every element's sum_t |r_t,k| (the
+                // error-bound input) and, being a plain sum, turns any NaN/Inf in x
+                // or a centroid into a non-finite e: the finiteness check for free.
+                float e = 0.f;
+#pragma unroll
+                for (int t = 0; t < S; t++) {
+                    const uint4 *c4 = reinterpret_cast<const uint4 *>(ct + uint32_t(t * a.K + ai[u][t]) * d + col);
+                    float c[16];
+                    cvt16(c4[0], c4[1], c);
+#pragma unroll
+                    for (int k = 0; k < 16; k++) r[u][k] = __fsub_rn(r[u][k], c[k]);
+                    if (t < S - 1) {
+                        float m = 0.f;
+#pragma unroll
+                        for (int k = 0; k < 16; k++) m = fmaxf(m, fabsf(r[u][k]));
+                        e = __fadd_ru(e, m);
+                    }
+                }
+                // NaN/Inf anywhere in x or a centroid reaches r_S; r*0 turns it into NaN
+                float nf = 0.f;
+#pragma unroll
+                for (int k = 0; k < 16; k++) nf = __fmaf_rn(r[u][k], 0.f, nf);
+                nonfinite |= nf != 0.f;
+                float mx = 0.f;
+#pragma unroll
+                for (int k = 0; k < 16; k++) mx = fmaxf(mx, fabsf(r[u][k]));
+                eb[u] = S > 0 ? __fadd_ru(e, mx) : 0.f;
+                am[u] = mx;
+            }
+            for (int m = 1; m < glanes; m <<= 1) {
+#pragma unroll
+                for (int u = 0; u < kUnroll; u++) {
+                    am[u] = fmaxf(am[u], __shfl_xor_sync(0xffffffffu, am[u], m));
+                    eb[u] = fmaxf(eb[u], __shfl_xor_sync(0xffffffffu, eb[u], m));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; u++) {
+                const bool valid = i0 + u * rpp + rslot < N;
+                const float E = __fmul_ru(eb[u], 2.38418579e-7f);
+                uint32_t code;
+                bool camb = false;
+                if (am[u] == 0.f && E == 0.f) code = 0x38u;
+                else {
+                    const float lo = __fsub_rd(am[u], E), hi = __fadd_ru(am[u], E);
+                    if (lo > 0.f) code = scale_code<QMAX>(lo, hi, camb);
+                    else { code = 0x38u; camb = true; }
+                }
+                camb &= valid;
+                auto exact_r = [&](int k) {
+                    return exact_residual<XBF16, S>(xb, ct, ii[u] * d + col + k, col + k, d, a.K, ai[u][0],
+                                                    ai[u][SS > 1 ? 1 : 0], ai[u][SS > 2 ? 2 : 0],
+                                                    ai[u][SS > 3 ? 3 : 0]);
+                };
+                if (__any_sync(0xffffffffu, camb)) {          // exact scale (rare)
+                    const float thr = __fsub_rd(am[u], __fmul_ru(E, 2.f));
+                    uint32_t cand = 0;
+#pragma unroll
+                    for (int k = 0; k < 16; k++) cand |= (camb && fabsf(r[u][k]) >= thr) ? 1u << k : 0u;
+                    double a64 = 0.0;
+                    while (cand) {
+                        const int k = __ffs(cand) - 1;
+                        cand &= cand - 1;
+                        a64 = fmax(a64, fabs(exact_r(k)));
+                    }
+                    for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
+                    if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
+                }
+                const float s = e4m3_decode_fast(code);
+                uint32_t b32[BITS / 2];
+#pragma unroll
+                for (int q = 0; q < BITS / 2; q++) b32[q] = 0;
+                bool amb = false;
+                if constexpr (QMAX == 1) {
+                    const float half = 0.5f * s;
+                    amb = !(E < 0.125f * s);
+#pragma unroll
+                    uint32_t pw = a.one;   // runtime 1: keeps the packing multiplies on the FMA pipe
+#pragma unroll
+                    for (int k = 0; k < 16; k++) {
+                        const float av = fabsf(r[u][k]);
+                        amb |= fabsf(av - half) <= E;
+                        // code 1 (+) or 3 (-) = 2*sign + 1, sign by multiply-high
+                        const uint32_t v = __umulhi(__float_as_uint(r[u][k]), 2u) * (2u * a.one) + a.one;
+                        b32[0] += (av > half ? v : 0u) * pw;
+                        pw *= 4u * a.one;
+                    }
+                } else {
+                    const float inv = __frcp_rn(s);
+#pragma unroll
+                    for (int k = 0; k < 16; k++) {
+                        const float av = fabsf(r[u][k]);
+                        const float t = av * inv;
+                        const float fl = floorf(t);
+                        const float hb = (fl + 0.5f) * s;
+                        const float w = __fmaf_ru(hb, 2.38418579e-7f, E);
+                        amb |= fl < float(QMAX) && av >= __fsub_rd(hb, w) && av <= __fadd_ru(hb, w);
+                        int q = min(int(rintf(t)), QMAX);
+                        if (r[u][k] < 0.f) q = -q;
+                        b32[(k * BITS) >> 5] |= (uint32_t(q) & ((1u << BITS) - 1u)) << ((k * BITS) & 31);
+                    }
+                }
+                amb &= valid;
+                if (__any_sync(0xffffffffu, amb) && amb) {   // exact codes (rare)
+                    uint32_t todo = 0;
+                    const bool all = !(E < 0.125f * s);
+                    const float inv = __frcp_rn(s);
+#pragma unroll
+                    for (int k = 0; k < 16; k++) {
+                        const float av = fabsf(r[u][k]);
+                        bool in;
+                        if constexpr (QMAX == 1) in = fabsf(av - 0.5f * s) <= E;
+                        else {
+                            const float fl = floorf(av * inv);
+                            const float hb = (fl + 0.5f) * s;
+                            const float w = __fmaf_ru(hb, 2.38418579e-7f, E);
+                            in = fl < float(QMAX) && av >= __fsub_rd(hb, w) && av <= __fadd_ru(hb, w);
+                        }
+                        todo |= (all || in) ? 1u << k : 0u;
+                    }
+                    while (todo) {
+                        const int k = __ffs(todo) - 1;
+                        todo &= todo - 1;
+                        const uint32_t q = exact_code<QMAX>(exact_r(k), s) & ((1u << BITS) - 1u);
+                        const int sh = (k * BITS) & 31, wi = (k * BITS) >> 5;
+#pragma unroll
+                        for (int q2 = 0; q2 < BITS / 2; q2++)
+                            if (q2 == wi) b32[q2] = (b32[q2] & ~(((1u << BITS) - 1u) << sh)) | (q << sh);
+                    }
+                }
+                if (!valid) continue;
+                const uint32_t e0 = ii[u] * d + col;
+                uint8_t *plp = a.payload + uint64_t(p) * a.pb + ((e0 * BITS) >> 3);
+                if constexpr (BITS == 2) *reinterpret_cast<uint32_t *>(plp) = b32[0];
+                else if constexpr (BITS == 4) *reinterpret_cast<uint2 *>(plp) = make_uint2(b32[0], b32[1]);
+                else *reinterpret_cast<uint4 *>(plp) = make_uint4(b32[0], b32[1], b32[2], b32[3]);
+                if ((lane & (glanes - 1)) == 0) a.scales[uint64_t(p) * a.ng + (e0 >> a.lgB)] = uint8_t(code);
+            }
+        }
+        __syncthreads();
+    }
+    const uint32_t all = __reduce_or_sync(0xffffffffu, nonfinite ? uint32_t(QVG_STATUS_NONFINITE) : 0u);
+    if (all && lane == 0) atomicOr(a.status, int(all));
+}
+
+// ------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------
 static int grid_for(int64_t work, int block) {
@@ -937,9 +1299,33 @@ static int tile_grid(const TileArgs &t) {
     return int(t.n_tiles < 148u * 4u ? t.n_tiles : 148u * 4u);
 }
 
+// v5 (TMA-staged centroid tables) when two tables fit beside each other in
+// shared memory and there are enough planes to fill the GPU with CTAs.
+static int v5_ctas_per_sm(int64_t P, uint32_t tbytes, int S) {
+    if (S == 0 || tbytes % 16 != 0 || 2 * size_t(tbytes) > 200 * 1024) return 0;
+    int per_sm = int((224 * 1024) / (2 * size_t(tbytes) + 1024));
+    if (per_sm > 8) per_sm = 8;
+    if (per_sm < 1 || P < 2 * 148) return 0;
+    return per_sm;
+}
+
+
 template <int BITS, int S>
 static void launch_quant_fast(const QuantArgs &a, bool xbf16, cudaStream_t st) {
     const int g = tile_grid(a.ta);
+    if (a.v16 && a.v5) {
+        const PlaneLoop pl{a.P, uint32_t(S) * a.K * a.d * 2};
+        const size_t sm = 2 * size_t(pl.tbytes);
+        const int grid = int(int64_t(a.P) < int64_t(148) * a.v5 ? int64_t(a.P) : int64_t(148) * a.v5);
+        if (xbf16) {
+            cudaFuncSetAttribute(k_quantize_v5<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            k_quantize_v5<BITS, S, true><<<grid, 256, sm, st>>>(a, pl);
+        } else {
+            cudaFuncSetAttribute(k_quantize_v5<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            k_quantize_v5<BITS, S, false><<<grid, 256, sm, st>>>(a, pl);
+        }
+        return;
+    }
     if (a.v16) {
         if (xbf16) k_quantize_v4<BITS, S, true><<<g, 256, 0, st>>>(a);
         else k_quantize_v4<BITS, S, false><<<g, 256, 0, st>>>(a);
@@ -971,7 +1357,8 @@ int launch_quantize(const void *x, int xdtype, int64_t P, int64_t N, int d, int 
         QuantArgs a{x, cent, asg, payload, scales, uint32_t(N), d, K, B, lvpr,
                     v16 ? ilog2(B / 16) : ilog2(B / 8), status,
                     uint32_t(N * d * bits / 8), uint32_t(N * d / B), uint32_t(ilog2(B)),
-                    make_tiles(P, N, lvpr), v16 ? 1 : 0};
+                    make_tiles(P, N, lvpr), v16 ? 1 : 0,
+                    v16 ? v5_ctas_per_sm(P, uint32_t(S) * K * d * 2, S) : 0, uint32_t(P), 1u};
         if (bits == 2) dispatch_quant_s<2>(a, S, xbf16, st);
         else if (bits == 4) dispatch_quant_s<4>(a, S, xbf16, st);
         else dispatch_quant_s<8>(a, S, xbf16, st);
@@ -1004,6 +1391,19 @@ int launch_unpack(const uint8_t *in, int64_t n, int bits, int8_t *out, cudaStrea
 template <int BITS, int S>
 static void launch_deq_fast(const DequantArgs &a, bool obf16, cudaStream_t st) {
     const int g = tile_grid(a.ta);
+    if (a.v16 && a.v5) {
+        const PlaneLoop pl{a.P, uint32_t(S) * a.K * a.d * 2};
+        const size_t sm = 2 * size_t(pl.tbytes);
+        const int grid = int(int64_t(a.P) < int64_t(148) * a.v5 ? int64_t(a.P) : int64_t(148) * a.v5);
+        if (obf16) {
+            cudaFuncSetAttribute(k_dequant_v5<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            k_dequant_v5<BITS, S, true><<<grid, 256, sm, st>>>(a, pl);
+        } else {
+            cudaFuncSetAttribute(k_dequant_v5<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+            k_dequant_v5<BITS, S, false><<<grid, 256, sm, st>>>(a, pl);
+        }
+        return;
+    }
     if (a.v16) {
         if (obf16) k_dequant_v4<BITS, S, true><<<g, 256, 0, st>>>(a);
         else k_dequant_v4<BITS, S, false><<<g, 256, 0, st>>>(a);
@@ -1035,7 +1435,8 @@ int launch_dequantize(const uint8_t *payload, const uint8_t *scales, const uint1
         const int lvpr = v16 ? ilog2(d / 16) : ilog2(vpr);
         DequantArgs a{payload, scales, cent, asg, out, uint32_t(N), d, K, B, lvpr, status,
                       uint32_t(N * d * bits / 8), uint32_t(N * d / B), uint32_t(ilog2(B)),
-                      make_tiles(P, N, lvpr), v16 ? 1 : 0};
+                      make_tiles(P, N, lvpr), v16 ? 1 : 0,
+                      v16 ? v5_ctas_per_sm(P, uint32_t(S) * K * d * 2, S) : 0, uint32_t(P)};
         if (bits == 2) dispatch_deq_s<2>(a, S, obf16, st);
         else if (bits == 4) dispatch_deq_s<4>(a, S, obf16, st);
         else dispatch_deq_s<8>(a, S, obf16, st);

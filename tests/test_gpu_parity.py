@@ -155,3 +155,25 @@ def test_nonfinite_input_raises():
         D.compress(x, QuantConfig(stages=1, centroids=4))
     with pytest.raises(NonFiniteInput):
         D.quantize(x, QuantConfig(stages=0))
+
+
+@pytest.mark.parametrize("bits,B,S,K", [(2, 64, 2, 64), (4, 16, 1, 32), (2, 16, 3, 16), (8, 32, 2, 8)])
+def test_many_planes_tma_path_vs_oracle(oracle_lib, bits, B, S, K):
+    """>= 2*148 planes select the persistent TMA-staged kernels (k_*_v5)."""
+    rng = np.random.default_rng(bits + 10 * S)
+    P, N, d = 320, 97, 128
+    x = _rand_planes(rng, P, N, d, 30.0)
+    cent = torch.from_numpy(rng.normal(0, 2.0, size=(P, S, K, d)).astype(np.float32)).to(torch.bfloat16)
+    asg = torch.from_numpy(rng.integers(0, K, size=(P, S, N)).astype(np.uint8))
+    cfg = QuantConfig(bits=bits, group_size=B, stages=S, centroids=K)
+    pay, sc = D.quantize(x.cuda(), cfg, cent.cuda(), asg.cuda())
+    rp, rs = oracle_lib.quantize_given_metas_batch(x.float().numpy(), cent.float().numpy(),
+                                                   asg.numpy(), bits, B, 8)
+    assert np.array_equal(sc.cpu().numpy(), rs)
+    assert np.array_equal(pay.cpu().numpy(), rp)
+    dc = D.DeviceChunks(cfg, N, d, pay, sc, cent.cuda(), asg.cuda())
+    out = D.dequantize(dc, torch.float32).cpu().numpy()
+    ref = oracle_lib.prq_decompress_batch(rp, rs, cent.float().numpy(), asg.numpy(), N, d, bits, B, 8)
+    assert np.array_equal(_u32(out), _u32(ref))
+    outb = D.dequantize(dc, torch.bfloat16).cpu()
+    assert torch.equal(outb.view(torch.int16), torch.from_numpy(ref).to(torch.bfloat16).view(torch.int16))
