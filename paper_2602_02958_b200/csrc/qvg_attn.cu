@@ -1,14 +1,420 @@
-// qvg_attn.cu — attention over the quantized cache (placeholder until the
-// tcgen05 kernel lands; returns QVG_ERR_UNSUPPORTED).
+// qvg_attn.cu — attention over the QVG-quantized KV cache on sm_100a.
+//
+// O = softmax(q [Khat ; k_cur]^T * scale) [Vhat ; v_cur] per head, where
+// Khat/Vhat are the one-pass reconstructions (Q/prq.py:113-132) of the head's
+// K and V planes.  No mask: the current chunk attends to every cached token
+// and to itself (block-causal video diffusion).
+//
+// Structure (one CTA = 128 query rows of one head, 128 threads; thread t
+// owns query row t = TMEM lane t):
+//   * the Q tile is staged once in shared memory (UMMA K-major, no swizzle);
+//   * for every 128-token KV block the threads build the K and V operand tiles
+//     in shared memory — dequantizing the packed codes, E4M3 scales and the
+//     per-token centroid add-back in-tile for cached blocks, copying bf16 for
+//     the current chunk (and for the bf16 comparator mode);
+//   * one thread issues tcgen05.mma (kind::f16, M=128, N=128, K=16 steps):
+//     S = Q K^T into TMEM columns [0,128), completion via tcgen05.commit on
+//     an mbarrier;
+//   * softmax (online, exp2 domain, lazy rescale when the running max grows
+//     by more than 2^8) reads S with tcgen05.ld, writes P (bf16) to shared
+//     memory; O (TMEM columns [128,256)) is rescaled in place with
+//     tcgen05.ld/st when needed;
+//   * tcgen05.mma: O += P V, then the next block.
+// Epilogue: O / l -> bf16.
+#include <cstdio>
+
 #include "qvg_common.cuh"
 #include "qvg_internal.h"
 
 namespace qvg {
-size_t attention_workspace_size(int64_t, int64_t, int64_t, int, int, const qvg_config *) { return 0; }
-int run_attention(const uint16_t *, const uint8_t *, const uint8_t *, const uint16_t *,
-                  const uint8_t *, const uint16_t *, const uint16_t *, const uint16_t *, int64_t,
-                  int64_t, int64_t, int, int, const qvg_config *, float, uint16_t *, void *, size_t,
-                  cudaStream_t) {
-    return set_err(QVG_ERR_UNSUPPORTED, "attention kernel not built");
+namespace attn {
+
+constexpr int kTile = 128;                  // query rows per CTA = KV tokens per block
+constexpr int kD = 128;                     // head_dim supported by the tcgen05 path
+constexpr int kTileBytes = kTile * kD * 2;  // one bf16 operand tile (32 KB)
+constexpr uint32_t kSbo = 2048;             // byte stride between 8-row core groups
+constexpr uint32_t kLbo = 128;              // byte stride between 8-column core chunks
+
+// ---- PTX wrappers ----------------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
+
+// UMMA shared-memory matrix descriptor (SWIZZLE_NONE, version 1 for sm_100)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFFu);
+    d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+    d |= uint64_t(1) << 46;                      // version
+    return d;                                    // base_offset 0, lbo_mode 0, layout 0
 }
+
+// instruction descriptor: kind::f16, A=B=bf16, D=f32, M=128, N=128
+__host__ __device__ constexpr uint32_t umma_idesc(bool b_mn_major) {
+    return (1u << 4)                 // c_format F32
+           | (1u << 7)               // a_format BF16
+           | (1u << 10)              // b_format BF16
+           | (0u << 15)              // a K-major
+           | (uint32_t(b_mn_major) << 16)
+           | (uint32_t(kTile >> 3) << 17)   // N
+           | (uint32_t(kTile >> 4) << 24);  // M
+}
+
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void bar_init(uint64_t *bar, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(bar)), "r"(n));
+}
+
+__device__ __forceinline__ void bar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred P1;\nWAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(su32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 32 consecutive 32-bit TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float v[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float v[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+        "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+        "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+        "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+        "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+        "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])), "r"(__float_as_uint(v[17])),
+        "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])), "r"(__float_as_uint(v[20])),
+        "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])), "r"(__float_as_uint(v[23])),
+        "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])), "r"(__float_as_uint(v[26])),
+        "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])), "r"(__float_as_uint(v[29])),
+        "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+        : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// ---- operand-tile layout (UMMA canonical, no swizzle) ----------------------
+// K-major tile, row r (M or N index), 16-byte chunk c of the K dimension.
+__device__ __forceinline__ uint32_t kmaj_off(uint32_t r, uint32_t c) {
+    return (r >> 3) * kSbo + c * kLbo + (r & 7u) * 16u;
+}
+// MN-major tile (B operand of P.V): token k (K index), 8-wide chunk c of the
+// N (= head_dim) index.
+__device__ __forceinline__ uint32_t mnmaj_off(uint32_t k, uint32_t c) {
+    return c * kSbo + (k >> 3) * kLbo + (k & 7u) * 16u;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&h);
+}
+
+struct AttnArgs {
+    const uint16_t *q, *k_cur, *v_cur, *kv_bf16;
+    const uint8_t *payload, *scales, *asg;
+    const uint16_t *cent;
+    uint16_t *out;
+    int64_t nq, n_cache, n_cur;
+    int H, bits, B, S, K;
+    float scale_log2;
+};
+
+// One token row (128 channels) of plane `pl` of the quantized cache,
+// reconstructed (f32 add-back in the reference's order, then bf16 RNE) and
+// written chunk by chunk into an operand tile via `put(c, uint4)`.
+template <int BITS, int S, typename Put>
+__device__ __forceinline__ void dequant_row(const AttnArgs &a, int64_t pl, int64_t tok, Put put) {
+    const int64_t N = a.n_cache;
+    const uint8_t *pp = a.payload + pl * ((N * kD * BITS) >> 3) + ((tok * kD * BITS) >> 3);
+    const uint8_t *sp = a.scales + pl * (N * kD / a.B) + tok * (kD / a.B);
+    const uint16_t *crow[S > 0 ? S : 1];
+#pragma unroll
+    for (int t = 0; t < S; t++) {
+        const int ai = __ldg(a.asg + (pl * S + t) * N + tok);
+        crow[t] = a.cent + ((pl * S + t) * a.K + ai) * kD;
+    }
+    constexpr uint32_t mask = (1u << BITS) - 1u, sign = 1u << (BITS - 1);
+#pragma unroll 4
+    for (int c = 0; c < kD / 8; c++) {
+        // 8 fields = BITS bytes of payload
+        uint64_t w;
+        if constexpr (BITS == 2) w = __ldg(reinterpret_cast<const uint16_t *>(pp) + c);
+        else if constexpr (BITS == 4) w = __ldg(reinterpret_cast<const uint32_t *>(pp) + c);
+        else { const uint2 v = __ldg(reinterpret_cast<const uint2 *>(pp) + c); w = uint64_t(v.x) | (uint64_t(v.y) << 32); }
+        const float s = e4m3_to_f32(__ldg(sp + (c * 8) / a.B));
+        float y[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const uint32_t u = uint32_t(w >> (k * BITS)) & mask;
+            y[k] = float(int(u ^ sign) - int(sign)) * s;
+        }
+#pragma unroll
+        for (int t = S - 1; t >= 0; t--) {
+            const uint4 cv = __ldg(reinterpret_cast<const uint4 *>(crow[t]) + c);
+            y[0] += bf16_lo(cv.x); y[1] += bf16_hi(cv.x); y[2] += bf16_lo(cv.y); y[3] += bf16_hi(cv.y);
+            y[4] += bf16_lo(cv.z); y[5] += bf16_hi(cv.z); y[6] += bf16_lo(cv.w); y[7] += bf16_hi(cv.w);
+        }
+        put(c, make_uint4(pack_bf16(y[0], y[1]), pack_bf16(y[2], y[3]), pack_bf16(y[4], y[5]), pack_bf16(y[6], y[7])));
+    }
+}
+
+template <typename Put>
+__device__ __forceinline__ void copy_row_bf16(const uint16_t *src, Put put) {
+#pragma unroll 4
+    for (int c = 0; c < 16; c++) put(c, __ldg(reinterpret_cast<const uint4 *>(src) + c));
+}
+
+template <int BITS, int S, bool QUANT>
+__global__ void __launch_bounds__(128, 1) k_attention(AttnArgs a) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t *sQ = smem;
+    uint8_t *sK = smem + kTileBytes;
+    uint8_t *sV = smem + 2 * kTileBytes;
+    uint8_t *sP = smem + 3 * kTileBytes;
+    __shared__ uint64_t mbar;
+    __shared__ uint32_t tmem_base_sh;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int h = blockIdx.y;
+    const int64_t q0 = int64_t(blockIdx.x) * kTile;
+    const int64_t H = a.H;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(&tmem_base_sh)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) {
+        bar_init(&mbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    // Q tile: row tid = query q0 + tid of head h (zeros past nq)
+    {
+        const int64_t qi = q0 + tid;
+        auto putq = [&](int c, uint4 v) { *reinterpret_cast<uint4 *>(sQ + kmaj_off(tid, c)) = v; };
+        if (qi < a.nq) copy_row_bf16(a.q + (qi * H + h) * kD, putq);
+        else
+            for (int c = 0; c < 16; c++) putq(c, make_uint4(0, 0, 0, 0));
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = tmem_base_sh;
+    const uint32_t t_lane = uint32_t(warp * 32) << 16;
+    const uint32_t tS = tmem, tO = tmem + 128;
+
+    const uint64_t dQ = umma_desc(su32(sQ), kLbo, kSbo);
+    const uint64_t dK = umma_desc(su32(sK), kLbo, kSbo);
+    const uint64_t dP = umma_desc(su32(sP), kLbo, kSbo);
+    const uint64_t dV = umma_desc(su32(sV), kLbo, kSbo);
+    constexpr uint32_t idK = umma_idesc(false), idV = umma_idesc(true);
+
+    float m_run = -INFINITY, l_run = 0.f;
+    uint32_t phase = 0;
+    const int64_t n_tot = a.n_cache + a.n_cur;
+    const int64_t n_blocks = (a.n_cache + kTile - 1) / kTile + (a.n_cur + kTile - 1) / kTile;
+    const int64_t cache_blocks = (a.n_cache + kTile - 1) / kTile;
+    (void)n_tot;
+
+    for (int64_t jb = 0; jb < n_blocks; jb++) {
+        // ---- build K / V operand tiles for this block (thread tid = token row)
+        const bool in_cache = jb < cache_blocks;
+        const int64_t base = in_cache ? jb * kTile : (jb - cache_blocks) * kTile;
+        const int64_t cnt = in_cache ? a.n_cache : a.n_cur;
+        const int64_t tok = base + tid;
+        const bool valid = tok < cnt;
+        auto putk = [&](int c, uint4 v) { *reinterpret_cast<uint4 *>(sK + kmaj_off(tid, c)) = v; };
+        auto putv = [&](int c, uint4 v) { *reinterpret_cast<uint4 *>(sV + mnmaj_off(tid, c)) = v; };
+        if (!valid) {
+            for (int c = 0; c < 16; c++) { putk(c, make_uint4(0, 0, 0, 0)); putv(c, make_uint4(0, 0, 0, 0)); }
+        } else if (in_cache) {
+            if constexpr (QUANT) {
+                dequant_row<BITS, S>(a, 2 * h, tok, putk);
+                dequant_row<BITS, S>(a, 2 * h + 1, tok, putv);
+            } else {
+                copy_row_bf16(a.kv_bf16 + ((2 * h) * a.n_cache + tok) * kD, putk);
+                copy_row_bf16(a.kv_bf16 + ((2 * h + 1) * a.n_cache + tok) * kD, putv);
+            }
+        } else {
+            copy_row_bf16(a.k_cur + (tok * H + h) * kD, putk);
+            copy_row_bf16(a.v_cur + (tok * H + h) * kD, putv);
+        }
+        fence_proxy_async();
+        fence_before();
+        __syncthreads();
+        // ---- S = Q K^T
+        if (tid == 0) {
+            fence_after();
+#pragma unroll
+            for (int k = 0; k < kD / 16; k++)
+                mma_f16(tS, dQ + uint64_t((k * 2 * kLbo) >> 4), dK + uint64_t((k * 2 * kLbo) >> 4), idK, k > 0);
+            mma_commit(&mbar);
+        }
+        bar_wait(&mbar, phase);
+        phase ^= 1u;
+        fence_after();
+        // ---- online softmax on row tid (exp2 domain); lazy rescale of O
+        const int nvalid = int(cnt - base < kTile ? cnt - base : kTile);
+        float mx = -INFINITY;
+#pragma unroll
+        for (int ch = 0; ch < 4; ch++) {
+            float sv[32];
+            tmem_ld32(tS + t_lane + ch * 32, sv);
+#pragma unroll
+            for (int i = 0; i < 32; i++)
+                if (ch * 32 + i < nvalid) mx = fmaxf(mx, sv[i] * a.scale_log2);
+        }
+        const bool grow = mx > m_run + 8.f;       // rescale only when the max grows by > 2^8
+        const float m_new = grow ? mx : m_run;
+        const float alpha = grow ? exp2f(m_run - m_new) : 1.f;
+        if (__any_sync(0xffffffffu, grow) && jb > 0) {
+#pragma unroll
+            for (int ch = 0; ch < 4; ch++) {
+                float ov[32];
+                tmem_ld32(tO + t_lane + ch * 32, ov);
+#pragma unroll
+                for (int i = 0; i < 32; i++) ov[i] *= alpha;
+                tmem_st32(tO + t_lane + ch * 32, ov);
+            }
+        }
+        l_run *= alpha;
+        m_run = m_new;
+        float lsum = 0.f;
+#pragma unroll
+        for (int ch = 0; ch < 4; ch++) {
+            float sv[32];
+            tmem_ld32(tS + t_lane + ch * 32, sv);
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+                const float p0 = ch * 32 + i < nvalid ? exp2f(sv[i] * a.scale_log2 - m_run) : 0.f;
+                const float p1 = ch * 32 + i + 1 < nvalid ? exp2f(sv[i + 1] * a.scale_log2 - m_run) : 0.f;
+                lsum += p0 + p1;
+                pk[i >> 1] = pack_bf16(p0, p1);
+            }
+#pragma unroll
+            for (int c = 0; c < 4; c++)
+                *reinterpret_cast<uint4 *>(sP + kmaj_off(tid, ch * 4 + c)) =
+                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        }
+        l_run += lsum;
+        fence_proxy_async();
+        fence_before();
+        __syncthreads();
+        // ---- O += P V
+        if (tid == 0) {
+            fence_after();
+#pragma unroll
+            for (int k = 0; k < kTile / 16; k++)
+                mma_f16(tO, dP + uint64_t((k * 2 * kLbo) >> 4), dV + uint64_t((k * 2 * kLbo) >> 4), idV,
+                        (jb > 0 || k > 0) ? 1u : 0u);
+            mma_commit(&mbar);
+        }
+        bar_wait(&mbar, phase);
+        phase ^= 1u;
+        fence_after();
+    }
+    // ---- epilogue: O / l -> bf16
+    const float inv_l = 1.f / l_run;
+    const int64_t qi = q0 + tid;
+#pragma unroll
+    for (int ch = 0; ch < 4; ch++) {
+        float ov[32];
+        tmem_ld32(tO + t_lane + ch * 32, ov);
+        if (qi < a.nq) {
+            uint4 *dst = reinterpret_cast<uint4 *>(a.out + (qi * H + h) * kD + ch * 32);
+#pragma unroll
+            for (int c = 0; c < 4; c++)
+                dst[c] = make_uint4(pack_bf16(ov[8 * c] * inv_l, ov[8 * c + 1] * inv_l),
+                                    pack_bf16(ov[8 * c + 2] * inv_l, ov[8 * c + 3] * inv_l),
+                                    pack_bf16(ov[8 * c + 4] * inv_l, ov[8 * c + 5] * inv_l),
+                                    pack_bf16(ov[8 * c + 6] * inv_l, ov[8 * c + 7] * inv_l));
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+template <int BITS, int S, bool QUANT>
+static int launch(const AttnArgs &a, cudaStream_t st) {
+    const size_t smem = 4 * size_t(kTileBytes) + 1024;
+    auto kern = k_attention<BITS, S, QUANT>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    dim3 grid(unsigned((a.nq + kTile - 1) / kTile), unsigned(a.H));
+    kern<<<grid, 128, smem, st>>>(a);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+
+template <int BITS>
+static int dispatch_s(const AttnArgs &a, cudaStream_t st) {
+    switch (a.S) {
+        case 0: return launch<BITS, 0, true>(a, st);
+        case 1: return launch<BITS, 1, true>(a, st);
+        case 2: return launch<BITS, 2, true>(a, st);
+        case 3: return launch<BITS, 3, true>(a, st);
+        case 4: return launch<BITS, 4, true>(a, st);
+        default: return set_err(QVG_ERR_UNSUPPORTED, "attention supports stages <= 4");
+    }
+}
+
+}  // namespace attn
+
+size_t attention_workspace_size(int64_t, int64_t, int64_t, int, int, const qvg_config *) { return 0; }
+
+int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scales,
+                  const uint16_t *cent, const uint8_t *assign, const uint16_t *kv_bf16,
+                  const uint16_t *k_cur, const uint16_t *v_cur, int64_t nq, int64_t n_cache,
+                  int64_t n_cur, int H, int d, const qvg_config *cfg, float scale, uint16_t *out,
+                  void *, size_t, cudaStream_t st) {
+    using namespace attn;
+    if (d != kD) return set_err(QVG_ERR_UNSUPPORTED, "attention kernel supports head_dim 128, got %d", d);
+    if (n_cur > 0 && (!k_cur || !v_cur)) return set_err(QVG_ERR_BAD_CONFIG, "k_cur/v_cur are NULL");
+    AttnArgs a{q, k_cur, v_cur, kv_bf16, payload, scales, assign, cent, out, nq, n_cache, n_cur, H,
+               cfg->bits, cfg->group_size, cfg->stages, cfg->centroids, scale * 1.4426950408889634f};
+    if (n_cache > 0 && !payload) {
+        if (!kv_bf16) return set_err(QVG_ERR_BAD_CONFIG, "cache is NULL");
+        const int rc = launch<2, 0, false>(a, st);
+        return rc ? set_err(rc, "attention launch failed: %s", cudaGetErrorString(cudaGetLastError())) : QVG_OK;
+    }
+    if (n_cache > 0 && (cfg->group_size % 8 != 0 || (kD % cfg->group_size) != 0))
+        return set_err(QVG_ERR_UNSUPPORTED, "attention needs group_size | 128 and 8 | group_size");
+    int rc;
+    if (cfg->bits == 2) rc = dispatch_s<2>(a, st);
+    else if (cfg->bits == 4) rc = dispatch_s<4>(a, st);
+    else rc = dispatch_s<8>(a, st);
+    if (rc == QVG_ERR_CUDA) return set_err(rc, "attention launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return rc;
+}
+
 }  // namespace qvg

@@ -16,7 +16,10 @@ def device() -> torch.device:
 
 
 def to_dev(a, dtype=None) -> torch.Tensor:
-    t = torch.from_numpy(np.ascontiguousarray(a))
+    a = np.ascontiguousarray(a)
+    if not a.flags.writeable:          # torch needs a writable buffer
+        a = a.copy()
+    t = torch.from_numpy(a)
     if dtype is not None:
         t = t.to(dtype)
     return t.to(device(), non_blocking=False).contiguous()

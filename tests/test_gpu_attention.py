@@ -1,0 +1,80 @@
+"""Attention over the quantized cache vs the fp64 CPU oracle
+(oracle/qvg_oracle.c:qo_attention over the oracle's own dequantized cache).
+
+Tolerance: max-abs <= 2e-2 * max|O_ref| and rel-L2 <= 1e-2
+(bf16 operands / P, fp32 accumulation)."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2602_02958_b200 import device as D  # noqa: E402
+from paper_2602_02958_b200.qvgcodec.types import QuantConfig  # noqa: E402
+from paper_2602_02958_b200.synth import clustered_planes  # noqa: E402
+
+ATOL_REL, RL2 = 2e-2, 1e-2
+
+
+def _check(out, ref):
+    out = out.float().cpu().numpy().astype(np.float64)
+    err = np.abs(out - ref)
+    scale = np.abs(ref).max()
+    rel_l2 = np.linalg.norm(out - ref) / np.linalg.norm(ref)
+    assert err.max() <= ATOL_REL * scale, (err.max(), scale)
+    assert rel_l2 <= RL2, rel_l2
+    return err.max() / scale, rel_l2
+
+
+@pytest.mark.parametrize("H,nq,nc,ncur,cfg", [
+    (2, 200, 300, 150, dict(bits=2, group_size=64, stages=2, centroids=16)),
+    (1, 128, 256, 128, dict(bits=4, group_size=16, stages=1, centroids=32)),
+    (3, 70, 129, 0, dict(bits=2, group_size=64, stages=1, centroids=8)),
+    (2, 130, 0, 200, dict(bits=2, group_size=64, stages=2, centroids=8)),
+])
+def test_quantized_attention_vs_oracle(oracle_lib, H, nq, nc, ncur, cfg):
+    torch.manual_seed(0)
+    cfg = QuantConfig(**cfg)
+    d = 128
+    q = (torch.randn(nq, H, d, device="cuda") * 0.5).to(torch.bfloat16)
+    kc = torch.randn(ncur, H, d, device="cuda").to(torch.bfloat16)
+    vc = torch.randn(ncur, H, d, device="cuda").to(torch.bfloat16)
+    scale = d ** -0.5
+    if nc:
+        planes = clustered_planes(2 * H, nc, d, n_clusters=16, outlier_scale=4.0, seed=1)
+        chunks = D.compress(planes, cfg)
+        out = D.attention(q, chunks, kc, vc, scale)
+        deq = oracle_lib.prq_decompress_batch(chunks.payload.cpu().numpy(), chunks.scales.cpu().numpy(),
+                                              chunks.centroids.float().cpu().numpy(),
+                                              chunks.assignments.cpu().numpy(), nc, d, cfg.bits,
+                                              cfg.group_size, 8)
+        kcache, vcache = deq[0::2], deq[1::2]
+    else:
+        out = D.attention(q, None, kc, vc, scale)
+        kcache = vcache = np.zeros((H, 0, d), np.float32)
+    torch.cuda.synchronize()
+    ref = oracle_lib.attention(q.float().cpu().numpy(), kcache, vcache, kc.float().cpu().numpy(),
+                               vc.float().cpu().numpy(), scale, 8)
+    _check(out, ref)
+
+
+def test_bf16_cache_mode_vs_oracle(oracle_lib):
+    torch.manual_seed(1)
+    H, nq, nc, ncur, d = 2, 256, 384, 128, 128
+    q = torch.randn(nq, H, d, device="cuda").to(torch.bfloat16)
+    kv = torch.randn(2 * H, nc, d, device="cuda").to(torch.bfloat16)
+    kc = torch.randn(ncur, H, d, device="cuda").to(torch.bfloat16)
+    vc = torch.randn(ncur, H, d, device="cuda").to(torch.bfloat16)
+    out = D.attention(q, None, kc, vc, d ** -0.5, kv_bf16=kv)
+    torch.cuda.synchronize()
+    kvf = kv.float().cpu().numpy()
+    ref = oracle_lib.attention(q.float().cpu().numpy(), kvf[0::2], kvf[1::2], kc.float().cpu().numpy(),
+                               vc.float().cpu().numpy(), d ** -0.5, 8)
+    _check(out, ref)
+    # and against torch SDPA on the same bf16 data (library comparator)
+    k_all = torch.cat([kv[0::2].permute(1, 0, 2), kc], 0)      # [nkv, H, d]
+    v_all = torch.cat([kv[1::2].permute(1, 0, 2), vc], 0)
+    sd = torch.nn.functional.scaled_dot_product_attention(
+        q.permute(1, 0, 2)[None].float(), k_all.permute(1, 0, 2)[None].float(),
+        v_all.permute(1, 0, 2)[None].float())[0].permute(1, 0, 2)
+    assert torch.allclose(out.float(), sd, atol=2e-2 * sd.abs().max().item())
