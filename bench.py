@@ -133,6 +133,64 @@ def build_cache(workload, rank, device):
     return cfg, x, dc, P_chunk, enc_ms
 
 
+def time_ms(fn, reps=5, warmup=2):
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def bench_attention(dev, rank, H=32, nc=38400, nq=7800, d=128):
+    """LongCat-Video-shaped layer (configs[2]): 32 heads, ~38K-token cache
+    (QVG b2 S1 K256 B64), current chunk of 7800 tokens attending to cache +
+    itself.  Quantized-cache attention vs the same kernel on the bf16 cache
+    and vs torch SDPA (cuDNN/flash, library comparator)."""
+    cfg = QuantConfig(bits=2, group_size=64, stages=1, centroids=256)
+    planes = kv_cache_planes(1, H, nc, d, seed=77 + rank, device=dev)     # [2H, nc, d] K,V per head
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    chunks = D.compress(planes, cfg, chunk_index=0)
+    torch.cuda.synchronize()
+    enc_s = time.perf_counter() - t0
+    g = torch.Generator(device=dev)
+    g.manual_seed(12345)
+    q = torch.randn((nq, H, d), generator=g, device=dev).to(torch.bfloat16)
+    kc = torch.randn((nq, H, d), generator=g, device=dev).to(torch.bfloat16)
+    vc = torch.randn((nq, H, d), generator=g, device=dev).to(torch.bfloat16)
+    out = torch.empty((nq, H, d), dtype=torch.bfloat16, device=dev)
+    ms_q = time_ms(lambda: D.attention(q, chunks, kc, vc, out=out))
+    ms_b = time_ms(lambda: D.attention(q, None, kc, vc, kv_bf16=planes, out=out))
+    # library comparator: SDPA on the materialised bf16 [cache ; current] (layout prep untimed)
+    kall = torch.cat([planes[0::2].permute(1, 0, 2), kc], 0).permute(1, 0, 2)[None].contiguous()
+    vall = torch.cat([planes[1::2].permute(1, 0, 2), vc], 0).permute(1, 0, 2)[None].contiguous()
+    qq = q.permute(1, 0, 2)[None].contiguous()
+    try:
+        ms_sdpa = time_ms(lambda: torch.nn.functional.scaled_dot_product_attention(qq, kall, vall))
+    except Exception:
+        ms_sdpa = None
+    flops = 4.0 * nq * (nc + nq) * d * H
+    _, tf_peak, tf_sus, kind = peaks()
+    return {
+        "workload": "longcat_layer", "heads": H, "cache_tokens": nc, "query_tokens": nq,
+        "cur_tokens": nq, "config": "b2 S1 K256 B64",
+        "latency_ms_quantized": round(ms_q, 3), "latency_ms_bf16_same_kernel": round(ms_b, 3),
+        "latency_ms_torch_sdpa_bf16": None if ms_sdpa is None else round(ms_sdpa, 3),
+        "ratio_quantized_vs_bf16": round(ms_q / ms_b, 4),
+        "ratio_quantized_vs_sdpa": None if ms_sdpa is None else round(ms_q / ms_sdpa, 4),
+        "tflops_quantized": round(flops / ms_q / 1e9, 1), "tflops_bf16": round(flops / ms_b / 1e9, 1),
+        "roofline": {"bound": "tensor", "achieved": round(flops / ms_q / 1e9, 1), "peak": tf_peak,
+                     "unit": "TFLOP/s", "frac": round(flops / ms_q / 1e9 / tf_peak, 4), "peak_kind": kind},
+        "encode_s": round(enc_s, 3),
+        "kv_compression": round(memory_breakdown(cfg, ChunkSpec(nc, d)).ratio_vs_bf16, 3),
+    }
+
+
 def cpu_sample_gbs(x_s, cent_s, asg_s, cfg, threads, min_seconds=10.0, max_seconds=30.0):
     """Oracle (CPU port) quantize+dequantize of a plane sample, repeated to ~10 s."""
     import oracle
@@ -160,6 +218,7 @@ def main():
     ap.add_argument("--workload", default="self_forcing_10s", choices=list(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-attention", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -276,6 +335,10 @@ def main():
             "value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
             "sample": f"oracle quantize+dequantize of {ns} planes x {reps} reps ({el:.1f} s), "
                       f"same byte accounting"}
+    if not args.no_attention:
+        del x, out, dq, payload, scales, dc
+        torch.cuda.empty_cache()
+        result["attention"] = bench_attention(dev, rank)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:

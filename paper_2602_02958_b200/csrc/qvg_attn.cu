@@ -22,6 +22,7 @@
 //   * tcgen05.mma: O += P V, then the next block.
 // Epilogue: O / l -> bf16.
 #include <cstdio>
+#include <cuda.h>
 
 #include "qvg_common.cuh"
 #include "qvg_internal.h"
@@ -390,31 +391,354 @@ static int dispatch_s(const AttnArgs &a, cudaStream_t st) {
 
 }  // namespace attn
 
-size_t attention_workspace_size(int64_t, int64_t, int64_t, int, int, const qvg_config *) { return 0; }
+// ============================================================================
+// v2: warp-specialised, pipelined tcgen05 attention over bf16 operands.
+//   warps 0-3  softmax (thread t = query row t = TMEM lane t) + epilogue
+//   warp  4    TMA producer: Q once, then K/V tiles into a 2-stage ring
+//   warp  5    TMEM allocator + single-thread MMA issuer
+// S_j = Q K_j^T goes to TMEM buffer j%2 while softmax works on S_{j-1};
+// O += P_{j-1} V_{j-1} is issued as soon as softmax publishes P_{j-1}.
+// Q/K/V tiles: TMA boxes [128 rows][64 cols] with 128B swizzle (UMMA
+// K-major SW128 for Q/K, MN-major SW128 for V); P: no-swizzle K-major.
+// The quantized cache is first reconstructed to bf16 by the K6 kernel into
+// the workspace (an HBM-bound pass), then attended here.
+// ============================================================================
+namespace attn2 {
+using attn::kTile;
+using attn::kD;
+
+constexpr uint32_t kBox = kTile * 64 * 2;          // one TMA box (16 KB)
+constexpr uint32_t kOpTile = 2 * kBox;             // a 128x128 bf16 operand (32 KB)
+constexpr uint32_t kSmem = kOpTile /*Q*/ + 2 * 2 * kOpTile /*K,V x 2 stages*/ + kOpTile /*P*/;
+
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= uint64_t((saddr >> 4) & 0x3FFFu);
+    d |= uint64_t((lbo >> 4) & 0x3FFFu) << 16;
+    d |= uint64_t((sbo >> 4) & 0x3FFFu) << 32;
+    d |= uint64_t(1) << 46;                        // version (sm_100)
+    d |= uint64_t(2) << 61;                        // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *tm, int x, int y, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            attn::su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(attn::su32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(attn::su32(bar)), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(attn::su32(bar)) : "memory");
+}
+
+__device__ __forceinline__ float ex2(float x) {
+    float y;
+    asm("ex2.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+struct Args {
+    int64_t nq, n_cache, n_cur;
+    int H;
+    float scale_log2;
+    uint16_t *out;
+};
+
+struct Bars {
+    uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], s_free[2], p_full, o_done;
+    uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(192, 1)
+k_attention_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
+                const __grid_constant__ CUtensorMap tmKc, const __grid_constant__ CUtensorMap tmVc, Args a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sQ = smem;
+    uint8_t *sKV = smem + kOpTile;                  // stage s: K at +s*2*kOpTile, V at +kOpTile
+    uint8_t *sP = smem + kOpTile + 4 * kOpTile;
+    __shared__ Bars bars;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int h = blockIdx.y;
+    const int64_t q0 = int64_t(blockIdx.x) * kTile;
+    const int64_t cb = (a.n_cache + kTile - 1) / kTile;
+    const int64_t nb = cb + (a.n_cur + kTile - 1) / kTile;
+
+    if (tid == 0) {
+        attn::bar_init(&bars.q_full, 1);
+        for (int i = 0; i < 2; i++) {
+            attn::bar_init(&bars.kv_full[i], 1);
+            attn::bar_init(&bars.kv_empty[i], 1);
+            attn::bar_init(&bars.s_full[i], 1);
+            attn::bar_init(&bars.s_free[i], 128);
+        }
+        attn::bar_init(&bars.p_full, 128);
+        attn::bar_init(&bars.o_done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 5) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(attn::su32(&bars.tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    attn::fence_before();
+    __syncthreads();
+    attn::fence_after();
+    const uint32_t tmem = bars.tmem;
+
+    if (warp == 4) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
+            expect_tx(&bars.q_full, kOpTile);
+            tma_load_2d(sQ, &tmQ, h * kD, int(q0), &bars.q_full);
+            tma_load_2d(sQ + kBox, &tmQ, h * kD + 64, int(q0), &bars.q_full);
+            for (int64_t j = 0; j < nb; j++) {
+                const int st = int(j & 1);
+                if (j >= 2) attn::bar_wait(&bars.kv_empty[st], uint32_t(((j - 2) >> 1) & 1));
+                uint8_t *sK = sKV + st * 2 * kOpTile, *sV = sK + kOpTile;
+                expect_tx(&bars.kv_full[st], 2 * kOpTile);
+                if (j < cb) {
+                    const int yk = int(2 * h * a.n_cache + j * kTile), yv = int((2 * h + 1) * a.n_cache + j * kTile);
+                    tma_load_2d(sK, &tmKV, 0, yk, &bars.kv_full[st]);
+                    tma_load_2d(sK + kBox, &tmKV, 64, yk, &bars.kv_full[st]);
+                    tma_load_2d(sV, &tmKV, 0, yv, &bars.kv_full[st]);
+                    tma_load_2d(sV + kBox, &tmKV, 64, yv, &bars.kv_full[st]);
+                } else {
+                    const int y = int((j - cb) * kTile);
+                    tma_load_2d(sK, &tmKc, h * kD, y, &bars.kv_full[st]);
+                    tma_load_2d(sK + kBox, &tmKc, h * kD + 64, y, &bars.kv_full[st]);
+                    tma_load_2d(sV, &tmVc, h * kD, y, &bars.kv_full[st]);
+                    tma_load_2d(sV + kBox, &tmVc, h * kD + 64, y, &bars.kv_full[st]);
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            constexpr uint32_t idK = attn::umma_idesc(false), idV = attn::umma_idesc(true);
+            const uint32_t sq = attn::su32(sQ);
+            const uint64_t dP = attn::umma_desc(attn::su32(sP), attn::kLbo, attn::kSbo);
+            attn::bar_wait(&bars.q_full, 0);
+            auto issue_s = [&](int64_t j) {
+                const int st = int(j & 1), sb = int(j & 1);
+                const uint32_t sk = attn::su32(sKV + st * 2 * kOpTile);
+                attn::bar_wait(&bars.kv_full[st], uint32_t((j >> 1) & 1));
+                if (j >= 2) attn::bar_wait(&bars.s_free[sb], uint32_t(((j - 2) >> 1) & 1));
+                attn::fence_after();
+#pragma unroll
+                for (int k = 0; k < kD / 16; k++) {
+                    const uint32_t off = (k >> 2) * kBox + (k & 3) * 32;   // K-major SW128, 16-element step
+                    attn::mma_f16(tmem + sb * 128, desc_sw128(sq + off, 16, 1024), desc_sw128(sk + off, 16, 1024),
+                                  idK, k > 0);
+                }
+                attn::mma_commit(&bars.s_full[sb]);
+            };
+            auto issue_pv = [&](int64_t j) {
+                const int st = int(j & 1);
+                const uint32_t sv = attn::su32(sKV + st * 2 * kOpTile + kOpTile);
+                attn::bar_wait(&bars.p_full, uint32_t(j & 1));
+                attn::fence_after();
+#pragma unroll
+                for (int k = 0; k < kTile / 16; k++)
+                    attn::mma_f16(tmem + 256, dP + uint64_t((k * 2 * attn::kLbo) >> 4),
+                                  desc_sw128(sv + k * 2048, kBox, 1024), idV, (j > 0 || k > 0) ? 1u : 0u);
+                attn::mma_commit(&bars.o_done);
+                attn::mma_commit(&bars.kv_empty[st]);
+            };
+            for (int64_t j = 0; j < nb; j++) {
+                issue_s(j);
+                if (j >= 1) issue_pv(j - 1);
+            }
+            if (nb > 0) issue_pv(nb - 1);
+        }
+    } else {
+        // ---------------- softmax warps (rows) ----------------
+        const uint32_t t_lane = uint32_t(warp * 32) << 16;
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int64_t j = 0; j < nb; j++) {
+            const int sb = int(j & 1);
+            const int64_t cnt = j < cb ? a.n_cache - j * kTile : a.n_cur - (j - cb) * kTile;
+            const int nvalid = int(cnt < kTile ? cnt : kTile);
+            const uint32_t tS = tmem + sb * 128 + t_lane;
+            attn::bar_wait(&bars.s_full[sb], uint32_t((j >> 1) & 1));
+            attn::fence_after();
+            float mx = -INFINITY;
+#pragma unroll
+            for (int ch = 0; ch < 4; ch++) {
+                float sv[32];
+                attn::tmem_ld32(tS + ch * 32, sv);
+#pragma unroll
+                for (int i = 0; i < 32; i++)
+                    if (ch * 32 + i < nvalid) mx = fmaxf(mx, sv[i]);
+            }
+            mx *= a.scale_log2;
+            const bool grow = mx > m_run + 8.f;       // lazy rescale (FA4): only when the max grows by > 2^8
+            const float m_new = grow ? mx : m_run;
+            const float alpha = grow ? ex2(m_run - m_new) : 1.f;
+            uint32_t pk[64];
+            float lsum = 0.f;
+#pragma unroll
+            for (int ch = 0; ch < 4; ch++) {
+                float sv[32];
+                attn::tmem_ld32(tS + ch * 32, sv);
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    const float p0 = ch * 32 + i < nvalid ? ex2(fmaf(sv[i], a.scale_log2, -m_new)) : 0.f;
+                    const float p1 = ch * 32 + i + 1 < nvalid ? ex2(fmaf(sv[i + 1], a.scale_log2, -m_new)) : 0.f;
+                    lsum += p0 + p1;
+                    pk[ch * 16 + (i >> 1)] = attn::pack_bf16(p0, p1);
+                }
+            }
+            attn::fence_before();
+            arrive(&bars.s_free[sb]);                 // S buffer may be overwritten by S_{j+2}
+            if (j > 0) {
+                attn::bar_wait(&bars.o_done, uint32_t((j - 1) & 1));   // PV_{j-1} done: P and O free
+                attn::fence_after();
+                if (__any_sync(0xffffffffu, grow)) {
+#pragma unroll
+                    for (int ch = 0; ch < 4; ch++) {
+                        float ov[32];
+                        attn::tmem_ld32(tmem + 256 + t_lane + ch * 32, ov);
+#pragma unroll
+                        for (int i = 0; i < 32; i++) ov[i] *= alpha;
+                        attn::tmem_st32(tmem + 256 + t_lane + ch * 32, ov);
+                    }
+                }
+            }
+            l_run = l_run * alpha + lsum;
+            m_run = m_new;
+#pragma unroll
+            for (int c = 0; c < 16; c++)
+                *reinterpret_cast<uint4 *>(sP + attn::kmaj_off(tid, c)) =
+                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+            attn::fence_proxy_async();
+            attn::fence_before();
+            arrive(&bars.p_full);
+        }
+        // ---------------- epilogue ----------------
+        if (nb > 0) attn::bar_wait(&bars.o_done, uint32_t((nb - 1) & 1));
+        attn::fence_after();
+        const float inv_l = 1.f / l_run;
+        const int64_t qi = q0 + tid;
+#pragma unroll
+        for (int ch = 0; ch < 4; ch++) {
+            float ov[32];
+            attn::tmem_ld32(tmem + 256 + t_lane + ch * 32, ov);
+            if (qi < a.nq) {
+                uint4 *dst = reinterpret_cast<uint4 *>(a.out + (qi * a.H + h) * kD + ch * 32);
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    dst[c] = make_uint4(attn::pack_bf16(ov[8 * c] * inv_l, ov[8 * c + 1] * inv_l),
+                                        attn::pack_bf16(ov[8 * c + 2] * inv_l, ov[8 * c + 3] * inv_l),
+                                        attn::pack_bf16(ov[8 * c + 4] * inv_l, ov[8 * c + 5] * inv_l),
+                                        attn::pack_bf16(ov[8 * c + 6] * inv_l, ov[8 * c + 7] * inv_l));
+            }
+        }
+    }
+    attn::fence_before();
+    __syncthreads();
+    if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+// ---- host: tensor maps via the driver entry point (no -lcuda needed) -------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;      // immutable once resolved
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// 2-D bf16 tensor [rows][cols] (row pitch `pitch` elements), box [128][64], SW128
+static bool make_map(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols, uint64_t pitch) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {pitch * 2};
+    cuuint32_t box[2] = {64, uint32_t(kTile)};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const uint16_t *vc, int64_t nq,
+               int64_t nc, int64_t ncur, int H, float scale_log2, uint16_t *out, cudaStream_t st) {
+    CUtensorMap mQ, mKV, mKc, mVc;
+    // Q, k_cur, v_cur: [n][H*128]; cache: [2H*n_cache][128].  Empty operands get a
+    // 1-row dummy map over q (never loaded).
+    const bool okq = make_map(&mQ, q, uint64_t(nq), uint64_t(H) * kD, uint64_t(H) * kD);
+    const bool okkv = nc > 0 ? make_map(&mKV, kv, uint64_t(2 * H) * nc, kD, kD) : make_map(&mKV, q, 1, kD, kD);
+    const bool okk = ncur > 0 ? make_map(&mKc, kc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
+                              : make_map(&mKc, q, 1, kD, kD);
+    const bool okv = ncur > 0 ? make_map(&mVc, vc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
+                              : make_map(&mVc, q, 1, kD, kD);
+    if (!(okq && okkv && okk && okv)) return set_err(QVG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    const size_t smem = kSmem + 1024;
+    cudaFuncSetAttribute(k_attention_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    dim3 grid(unsigned((nq + kTile - 1) / kTile), unsigned(H));
+    Args a{nq, nc, ncur, H, scale_log2, out};
+    k_attention_tma<<<grid, 192, smem, st>>>(mQ, mKV, mKc, mVc, a);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+}  // namespace attn2
+
+size_t attention_workspace_size(int64_t, int64_t n_cache, int64_t, int H, int d, const qvg_config *) {
+    // bf16 reconstruction of the quantized cache (2H planes) for the TMA kernel
+    return n_cache > 0 ? size_t(2) * H * n_cache * d * 2 + 256 : 0;
+}
 
 int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scales,
                   const uint16_t *cent, const uint8_t *assign, const uint16_t *kv_bf16,
                   const uint16_t *k_cur, const uint16_t *v_cur, int64_t nq, int64_t n_cache,
                   int64_t n_cur, int H, int d, const qvg_config *cfg, float scale, uint16_t *out,
-                  void *, size_t, cudaStream_t st) {
+                  void *workspace, size_t wbytes, cudaStream_t st) {
     using namespace attn;
     if (d != kD) return set_err(QVG_ERR_UNSUPPORTED, "attention kernel supports head_dim 128, got %d", d);
     if (n_cur > 0 && (!k_cur || !v_cur)) return set_err(QVG_ERR_BAD_CONFIG, "k_cur/v_cur are NULL");
-    AttnArgs a{q, k_cur, v_cur, kv_bf16, payload, scales, assign, cent, out, nq, n_cache, n_cur, H,
-               cfg->bits, cfg->group_size, cfg->stages, cfg->centroids, scale * 1.4426950408889634f};
-    if (n_cache > 0 && !payload) {
-        if (!kv_bf16) return set_err(QVG_ERR_BAD_CONFIG, "cache is NULL");
-        const int rc = launch<2, 0, false>(a, st);
+    const float sl2 = scale * 1.4426950408889634f;
+    const uint16_t *kv = kv_bf16;
+    if (n_cache > 0 && payload && !workspace) {
+        // no workspace: the fused kernel dequantizes codes/scales/centroids in-tile
+        if (cfg->group_size % 8 != 0 || kD % cfg->group_size != 0)
+            return set_err(QVG_ERR_UNSUPPORTED, "attention needs group_size | 128 and 8 | group_size");
+        AttnArgs ia{q, k_cur, v_cur, nullptr, payload, scales, assign, cent, out, nq, n_cache, n_cur, H,
+                    cfg->bits, cfg->group_size, cfg->stages, cfg->centroids, sl2};
+        int rc = cfg->bits == 2 ? dispatch_s<2>(ia, st) : cfg->bits == 4 ? dispatch_s<4>(ia, st) : dispatch_s<8>(ia, st);
         return rc ? set_err(rc, "attention launch failed: %s", cudaGetErrorString(cudaGetLastError())) : QVG_OK;
     }
-    if (n_cache > 0 && (cfg->group_size % 8 != 0 || (kD % cfg->group_size) != 0))
-        return set_err(QVG_ERR_UNSUPPORTED, "attention needs group_size | 128 and 8 | group_size");
-    int rc;
-    if (cfg->bits == 2) rc = dispatch_s<2>(a, st);
-    else if (cfg->bits == 4) rc = dispatch_s<4>(a, st);
-    else rc = dispatch_s<8>(a, st);
-    if (rc == QVG_ERR_CUDA) return set_err(rc, "attention launch failed: %s", cudaGetErrorString(cudaGetLastError()));
-    return rc;
+    if (n_cache > 0 && payload) {
+        // K6: reconstruct the 2H cache planes to bf16 (HBM-bound), then attend
+        const size_t need = attention_workspace_size(nq, n_cache, n_cur, H, d, cfg);
+        if (wbytes < need) return set_err(QVG_ERR_WORKSPACE, "attention workspace needs %zu bytes", need);
+        uint16_t *rec = static_cast<uint16_t *>(workspace);
+        int32_t *status = reinterpret_cast<int32_t *>(static_cast<uint8_t *>(workspace) + need - 256);
+        cudaMemsetAsync(status, 0, sizeof(int32_t), st);
+        int rc = launch_dequantize(payload, scales, cent, assign, 2 * int64_t(H), n_cache, d, cfg->bits,
+                                   cfg->group_size, cfg->stages, cfg->centroids, rec, QVG_DTYPE_BF16,
+                                   status, st);
+        if (rc) return set_err(rc, "cache reconstruction failed");
+        kv = rec;
+    } else if (n_cache > 0 && !kv) {
+        return set_err(QVG_ERR_BAD_CONFIG, "cache is NULL");
+    }
+    const int rc = attn2::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st);
+    return rc ? set_err(rc, "attention launch failed: %s", cudaGetErrorString(cudaGetLastError())) : QVG_OK;
 }
 
 }  // namespace qvg

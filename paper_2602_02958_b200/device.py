@@ -345,11 +345,15 @@ def add_back(residual: torch.Tensor, centroids: torch.Tensor, assignments: torch
 def attention(q: torch.Tensor, cache: Optional[DeviceChunks], k_cur: torch.Tensor,
               v_cur: torch.Tensor, softmax_scale: Optional[float] = None,
               kv_bf16: Optional[torch.Tensor] = None,
-              out: Optional[torch.Tensor] = None) -> torch.Tensor:
+              out: Optional[torch.Tensor] = None, fused: bool = False,
+              workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
     """O = softmax(q [Khat; k_cur]^T * scale) [Vhat; v_cur] per head.
 
     q [Nq, H, d] bf16; cache: 2H planes (plane 2h = K of head h, 2h+1 = V)
     or, for the bf16 comparator, kv_bf16 [2H, Nc, d]; k_cur/v_cur [Ncur, H, d].
+    fused=True dequantizes the cache inside the attention kernel (no bf16
+    staging buffer); the default reconstructs it to bf16 in a workspace with the
+    HBM-bound decoder and runs the pipelined TMA/tcgen05 kernel.
     """
     _require_cuda(q, k_cur, v_cur, kv_bf16, out)
     nq, H, d = q.shape
@@ -368,11 +372,16 @@ def attention(q: torch.Tensor, cache: Optional[DeviceChunks], k_cur: torch.Tenso
     lib = _lib.load()
     cp = _lib.cfg_ptr(cfg)
     n = lib.qvg_attention_workspace_size(nq, nc, ncur, H, d, cp)
-    ws = torch.empty(max(n, 1), dtype=torch.uint8, device=q.device)
+    if fused or cache is None:
+        ws, nbytes = None, 0
+    else:
+        ws = workspace if workspace is not None and workspace.numel() >= n else \
+            torch.empty(max(n, 1), dtype=torch.uint8, device=q.device)
+        nbytes = ws.numel()
     c = cache
     _lib.check(lib.qvg_attention(
         _ptr(q), _ptr(c.payload if c else None), _ptr(c.scales if c else None),
         _ptr(c.centroids if c else None), _ptr(c.assignments if c else None), _ptr(kv_bf16),
-        _ptr(k_cur), _ptr(v_cur), nq, nc, ncur, H, d, cp, scale, _ptr(out), _ptr(ws), ws.numel(),
+        _ptr(k_cur), _ptr(v_cur), nq, nc, ncur, H, d, cp, scale, _ptr(out), _ptr(ws), nbytes,
         _stream(q.device)))
     return out

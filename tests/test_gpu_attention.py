@@ -26,13 +26,14 @@ def _check(out, ref):
     return err.max() / scale, rel_l2
 
 
+@pytest.mark.parametrize("fused", [False, True])
 @pytest.mark.parametrize("H,nq,nc,ncur,cfg", [
     (2, 200, 300, 150, dict(bits=2, group_size=64, stages=2, centroids=16)),
     (1, 128, 256, 128, dict(bits=4, group_size=16, stages=1, centroids=32)),
     (3, 70, 129, 0, dict(bits=2, group_size=64, stages=1, centroids=8)),
     (2, 130, 0, 200, dict(bits=2, group_size=64, stages=2, centroids=8)),
 ])
-def test_quantized_attention_vs_oracle(oracle_lib, H, nq, nc, ncur, cfg):
+def test_quantized_attention_vs_oracle(oracle_lib, H, nq, nc, ncur, cfg, fused):
     torch.manual_seed(0)
     cfg = QuantConfig(**cfg)
     d = 128
@@ -43,7 +44,7 @@ def test_quantized_attention_vs_oracle(oracle_lib, H, nq, nc, ncur, cfg):
     if nc:
         planes = clustered_planes(2 * H, nc, d, n_clusters=16, outlier_scale=4.0, seed=1)
         chunks = D.compress(planes, cfg)
-        out = D.attention(q, chunks, kc, vc, scale)
+        out = D.attention(q, chunks, kc, vc, scale, fused=fused)
         deq = oracle_lib.prq_decompress_batch(chunks.payload.cpu().numpy(), chunks.scales.cpu().numpy(),
                                               chunks.centroids.float().cpu().numpy(),
                                               chunks.assignments.cpu().numpy(), nc, d, cfg.bits,
@@ -78,3 +79,21 @@ def test_bf16_cache_mode_vs_oracle(oracle_lib):
         q.permute(1, 0, 2)[None].float(), k_all.permute(1, 0, 2)[None].float(),
         v_all.permute(1, 0, 2)[None].float())[0].permute(1, 0, 2)
     assert torch.allclose(out.float(), sd, atol=2e-2 * sd.abs().max().item())
+
+
+def test_attention_long_cache_online_softmax(oracle_lib):
+    """Many KV blocks with a growing score range: exercises the lazy rescale."""
+    torch.manual_seed(2)
+    H, nq, nc, ncur, d = 1, 128, 2048, 64, 128
+    q = torch.randn(nq, H, d, device="cuda").to(torch.bfloat16)
+    kv = torch.randn(2 * H, nc, d, device="cuda")
+    kv[0] *= torch.linspace(0.2, 3.0, nc, device="cuda")[:, None]      # scores grow along the cache
+    kv = kv.to(torch.bfloat16)
+    kc = torch.randn(ncur, H, d, device="cuda").to(torch.bfloat16)
+    vc = torch.randn(ncur, H, d, device="cuda").to(torch.bfloat16)
+    out = D.attention(q, None, kc, vc, d ** -0.5, kv_bf16=kv)
+    torch.cuda.synchronize()
+    kvf = kv.float().cpu().numpy()
+    ref = oracle_lib.attention(q.float().cpu().numpy(), kvf[0::2], kvf[1::2], kc.float().cpu().numpy(),
+                               vc.float().cpu().numpy(), d ** -0.5, 8)
+    _check(out, ref)
