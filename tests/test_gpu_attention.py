@@ -97,3 +97,26 @@ def test_attention_long_cache_online_softmax(oracle_lib):
     ref = oracle_lib.attention(q.float().cpu().numpy(), kvf[0::2], kvf[1::2], kc.float().cpu().numpy(),
                                vc.float().cpu().numpy(), d ** -0.5, 8)
     _check(out, ref)
+
+
+def test_head_sharding_is_bit_identical():
+    """A rank computing only its heads (shard.head_range) reproduces the
+    1-GPU output for those heads byte for byte (no cross-head coupling)."""
+    from paper_2602_02958_b200.shard import head_range
+    torch.manual_seed(3)
+    H, nq, nc, ncur, d = 4, 130, 260, 70, 128
+    cfg = QuantConfig(bits=2, group_size=64, stages=2, centroids=8)
+    planes = clustered_planes(2 * H, nc, d, n_clusters=8, outlier_scale=4.0, seed=5)
+    chunks = D.compress(planes, cfg)
+    q = torch.randn(nq, H, d, device="cuda").to(torch.bfloat16)
+    kc = torch.randn(ncur, H, d, device="cuda").to(torch.bfloat16)
+    vc = torch.randn(ncur, H, d, device="cuda").to(torch.bfloat16)
+    full = D.attention(q, chunks, kc, vc)
+    for world in (2, 3):
+        for r in range(world):
+            h0, h1 = head_range(H, world, r)
+            sl = lambda t: t[:, h0:h1].contiguous()
+            local_cache = D.compress(planes[2 * h0:2 * h1].contiguous(), cfg)
+            assert torch.equal(local_cache.payload, chunks.payload[2 * h0:2 * h1])
+            local = D.attention(sl(q), local_cache, sl(kc), sl(vc))
+            assert torch.equal(local, full[:, h0:h1])
