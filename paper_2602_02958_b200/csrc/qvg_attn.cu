@@ -698,6 +698,258 @@ static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const 
 }
 }  // namespace attn2
 
+// ============================================================================
+// v3 (FA4-style ping-pong): one CTA = 2 query tiles (256 rows) of one head.
+//   warps 0-3 / 4-7  softmax of tile A / tile B (thread = TMEM lane = row)
+//   warp  8          TMA producer (Q_A, Q_B once; K/V 2-stage ring)
+//   warp  9          TMEM allocator + MMA issuer
+// TMEM (512 cols): S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512).
+// P (bf16 pairs) is written back over the first 64 columns of its S tile and
+// consumed as the TMEM A operand of O += P V.  MMAs issue in the order
+//   S_A(j) S_B(j) PV_A(j) PV_B(j) S_A(j+1) ...
+// so the tensor core computes S_B while softmax A runs and PV_A/S_A(j+1)
+// while softmax B runs; because tcgen05 MMAs complete in issue order, the
+// arrival of S_X(j) also certifies PV_X(j-1) done, which is what makes the
+// in-place O rescale and the P aliasing safe without extra barriers.
+// ============================================================================
+namespace attn3 {
+using attn::kTile;
+using attn::kD;
+using attn2::kBox;
+using attn2::kOpTile;
+constexpr uint32_t kSmem = 2 * kOpTile /*Q_A,Q_B*/ + 2 * 2 * kOpTile /*K,V x 2 stages*/;
+
+__device__ __forceinline__ void mma_f16_tmem_a(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st32u(uint32_t taddr, const uint32_t v[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+        "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+        "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+
+struct Bars {
+    uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], p_full[2], o_final;
+    uint32_t tmem;
+};
+
+__global__ void __launch_bounds__(320, 1)
+k_attention_pp(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
+               const __grid_constant__ CUtensorMap tmKc, const __grid_constant__ CUtensorMap tmVc, attn2::Args a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sQ = smem;                              // tile A at +0, tile B at +kOpTile
+    uint8_t *sKV = smem + 2 * kOpTile;               // stage s: K at +s*2*kOpTile, V at +kOpTile
+    __shared__ Bars bars;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int h = blockIdx.y;
+    const int64_t q0 = int64_t(blockIdx.x) * 2 * kTile;
+    const int64_t cb = (a.n_cache + kTile - 1) / kTile;
+    const int64_t nb = cb + (a.n_cur + kTile - 1) / kTile;
+
+    if (tid == 0) {
+        attn::bar_init(&bars.q_full, 1);
+        for (int i = 0; i < 2; i++) {
+            attn::bar_init(&bars.kv_full[i], 1);
+            attn::bar_init(&bars.kv_empty[i], 1);
+            attn::bar_init(&bars.s_full[i], 1);
+            attn::bar_init(&bars.p_full[i], 128);
+        }
+        attn::bar_init(&bars.o_final, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 9) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(attn::su32(&bars.tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    attn::fence_before();
+    __syncthreads();
+    attn::fence_after();
+    const uint32_t tmem = bars.tmem;
+
+    if (warp == 8) {
+        if (lane == 0) {                              // ---- TMA producer
+            attn2::expect_tx(&bars.q_full, 2 * kOpTile);
+            for (int t = 0; t < 2; t++) {
+                attn2::tma_load_2d(sQ + t * kOpTile, &tmQ, h * kD, int(q0 + t * kTile), &bars.q_full);
+                attn2::tma_load_2d(sQ + t * kOpTile + kBox, &tmQ, h * kD + 64, int(q0 + t * kTile), &bars.q_full);
+            }
+            for (int64_t j = 0; j < nb; j++) {
+                const int st = int(j & 1);
+                if (j >= 2) attn::bar_wait(&bars.kv_empty[st], uint32_t(((j - 2) >> 1) & 1));
+                uint8_t *sK = sKV + st * 2 * kOpTile, *sV = sK + kOpTile;
+                attn2::expect_tx(&bars.kv_full[st], 2 * kOpTile);
+                if (j < cb) {
+                    const int yk = int(2 * h * a.n_cache + j * kTile), yv = int((2 * h + 1) * a.n_cache + j * kTile);
+                    attn2::tma_load_2d(sK, &tmKV, 0, yk, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sK + kBox, &tmKV, 64, yk, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sV, &tmKV, 0, yv, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sV + kBox, &tmKV, 64, yv, &bars.kv_full[st]);
+                } else {
+                    const int y = int((j - cb) * kTile);
+                    attn2::tma_load_2d(sK, &tmKc, h * kD, y, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sK + kBox, &tmKc, h * kD + 64, y, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sV, &tmVc, h * kD, y, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sV + kBox, &tmVc, h * kD + 64, y, &bars.kv_full[st]);
+                }
+            }
+        }
+    } else if (warp == 9) {
+        if (lane == 0) {                              // ---- MMA issuer
+            constexpr uint32_t idK = attn::umma_idesc(false), idV = attn::umma_idesc(true);
+            attn::bar_wait(&bars.q_full, 0);
+            for (int64_t j = 0; j < nb; j++) {
+                const int st = int(j & 1);
+                const uint32_t sk = attn::su32(sKV + st * 2 * kOpTile), sv = sk + kOpTile;
+                attn::bar_wait(&bars.kv_full[st], uint32_t((j >> 1) & 1));
+                attn::fence_after();
+                for (int t = 0; t < 2; t++) {         // S_t = Q_t K_j^T
+                    const uint32_t sq = attn::su32(sQ + t * kOpTile);
+#pragma unroll
+                    for (int k = 0; k < kD / 16; k++) {
+                        const uint32_t off = (k >> 2) * kBox + (k & 3) * 32;
+                        attn::mma_f16(tmem + t * 128, attn2::desc_sw128(sq + off, 16, 1024),
+                                      attn2::desc_sw128(sk + off, 16, 1024), idK, k > 0);
+                    }
+                    attn::mma_commit(&bars.s_full[t]);
+                }
+                for (int t = 0; t < 2; t++) {         // O_t += P_t V_j  (P in TMEM over S_t)
+                    attn::bar_wait(&bars.p_full[t], uint32_t(j & 1));
+                    attn::fence_after();
+#pragma unroll
+                    for (int k = 0; k < kTile / 16; k++)
+                        mma_f16_tmem_a(tmem + 256 + t * 128, tmem + t * 128 + k * 8,
+                                       attn2::desc_sw128(sv + k * 2048, kBox, 1024), idV, (j > 0 || k > 0) ? 1u : 0u);
+                }
+                attn::mma_commit(&bars.kv_empty[st]);
+            }
+            attn::mma_commit(&bars.o_final);
+        }
+    } else {
+        // ---- softmax (tile t = warp / 4) ----
+        const int t = warp >> 2;
+        const uint32_t t_lane = uint32_t((warp & 3) * 32) << 16;
+        const uint32_t tS = tmem + t * 128 + t_lane, tO = tmem + 256 + t * 128 + t_lane;
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int64_t j = 0; j < nb; j++) {
+            const int64_t cnt = j < cb ? a.n_cache - j * kTile : a.n_cur - (j - cb) * kTile;
+            const int nvalid = int(cnt < kTile ? cnt : kTile);
+            attn::bar_wait(&bars.s_full[t], uint32_t(j & 1));
+            attn::fence_after();
+            float mx = -INFINITY;
+#pragma unroll
+            for (int ch = 0; ch < 4; ch++) {
+                float sv[32];
+                attn::tmem_ld32(tS + ch * 32, sv);
+                if (nvalid == kTile) {
+#pragma unroll
+                    for (int i = 0; i < 32; i++) mx = fmaxf(mx, sv[i]);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 32; i++)
+                        if (ch * 32 + i < nvalid) mx = fmaxf(mx, sv[i]);
+                }
+            }
+            mx *= a.scale_log2;
+            const bool grow = mx > m_run + 8.f;      // lazy rescale: only when the max grows by > 2^8
+            const float m_new = grow ? mx : m_run;
+            const float alpha = grow ? attn2::ex2(m_run - m_new) : 1.f;
+            // S_t(j) arrived => PV_t(j-1) (issued earlier) has completed: O_t is quiescent
+            if (j > 0 && __any_sync(0xffffffffu, grow)) {
+#pragma unroll
+                for (int ch = 0; ch < 4; ch++) {
+                    float ov[32];
+                    attn::tmem_ld32(tO + ch * 32, ov);
+#pragma unroll
+                    for (int i = 0; i < 32; i++) ov[i] *= alpha;
+                    attn::tmem_st32(tO + ch * 32, ov);
+                }
+            }
+            float lsum = 0.f;
+#pragma unroll
+            for (int half = 0; half < 2; half++) {
+                uint32_t pk[32];
+#pragma unroll
+                for (int cc = 0; cc < 2; cc++) {
+                    const int ch = half * 2 + cc;
+                    float sv[32];
+                    attn::tmem_ld32(tS + ch * 32, sv);
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2) {
+                        float p0 = attn2::ex2(fmaf(sv[i], a.scale_log2, -m_new));
+                        float p1 = attn2::ex2(fmaf(sv[i + 1], a.scale_log2, -m_new));
+                        if (nvalid != kTile) {
+                            p0 = ch * 32 + i < nvalid ? p0 : 0.f;
+                            p1 = ch * 32 + i + 1 < nvalid ? p1 : 0.f;
+                        }
+                        lsum += p0 + p1;
+                        pk[cc * 16 + (i >> 1)] = attn::pack_bf16(p0, p1);
+                    }
+                }
+                // P columns [32*half, 32*half+32) overwrite S columns already consumed
+                tmem_st32u(tS + half * 32, pk);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            l_run = l_run * alpha + lsum;
+            m_run = m_new;
+            attn::fence_before();
+            attn2::arrive(&bars.p_full[t]);
+        }
+        // ---- epilogue ----
+        attn::bar_wait(&bars.o_final, 0);
+        attn::fence_after();
+        const float inv_l = 1.f / l_run;
+        const int64_t qi = q0 + t * kTile + (tid & 127);
+#pragma unroll
+        for (int ch = 0; ch < 4; ch++) {
+            float ov[32];
+            attn::tmem_ld32(tO + ch * 32, ov);
+            if (qi < a.nq) {
+                uint4 *dst = reinterpret_cast<uint4 *>(a.out + (qi * a.H + h) * kD + ch * 32);
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    dst[c] = make_uint4(attn::pack_bf16(ov[8 * c] * inv_l, ov[8 * c + 1] * inv_l),
+                                        attn::pack_bf16(ov[8 * c + 2] * inv_l, ov[8 * c + 3] * inv_l),
+                                        attn::pack_bf16(ov[8 * c + 4] * inv_l, ov[8 * c + 5] * inv_l),
+                                        attn::pack_bf16(ov[8 * c + 6] * inv_l, ov[8 * c + 7] * inv_l));
+            }
+        }
+    }
+    attn::fence_before();
+    __syncthreads();
+    if (warp == 9) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const uint16_t *vc, int64_t nq,
+               int64_t nc, int64_t ncur, int H, float scale_log2, uint16_t *out, cudaStream_t st) {
+    CUtensorMap mQ, mKV, mKc, mVc;
+    const bool okq = attn2::make_map(&mQ, q, uint64_t(nq), uint64_t(H) * kD, uint64_t(H) * kD);
+    const bool okkv = nc > 0 ? attn2::make_map(&mKV, kv, uint64_t(2 * H) * nc, kD, kD)
+                             : attn2::make_map(&mKV, q, 1, kD, kD);
+    const bool okk = ncur > 0 ? attn2::make_map(&mKc, kc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
+                              : attn2::make_map(&mKc, q, 1, kD, kD);
+    const bool okv = ncur > 0 ? attn2::make_map(&mVc, vc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
+                              : attn2::make_map(&mVc, q, 1, kD, kD);
+    if (!(okq && okkv && okk && okv)) return set_err(QVG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    const size_t smem = kSmem + 1024;
+    cudaFuncSetAttribute(k_attention_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    dim3 grid(unsigned((nq + 2 * kTile - 1) / (2 * kTile)), unsigned(H));
+    attn2::Args args{nq, nc, ncur, H, scale_log2, out};
+    k_attention_pp<<<grid, 320, smem, st>>>(mQ, mKV, mKc, mVc, args);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+}  // namespace attn3
+
 size_t attention_workspace_size(int64_t, int64_t n_cache, int64_t, int H, int d, const qvg_config *) {
     // bf16 reconstruction of the quantized cache (2H planes) for the TMA kernel
     return n_cache > 0 ? size_t(2) * H * n_cache * d * 2 + 256 : 0;
@@ -737,7 +989,7 @@ int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scal
     } else if (n_cache > 0 && !kv) {
         return set_err(QVG_ERR_BAD_CONFIG, "cache is NULL");
     }
-    const int rc = attn2::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st);
+    const int rc = attn3::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st);
     return rc ? set_err(rc, "attention launch failed: %s", cudaGetErrorString(cudaGetLastError())) : QVG_OK;
 }
 
