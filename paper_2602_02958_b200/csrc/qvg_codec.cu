@@ -17,167 +17,15 @@
 //    checked for exactness (then the f64 chain is exact too, and the final
 //    f32 rounding of the last addition equals RN32(RN64(.)));
 //    an inexact element is recomputed in f64.
+#include <cstdlib>
+#include <cstring>
+
 #include "qvg_common.cuh"
 #include "qvg_internal.h"
+#include "qvg_codec_dev.cuh"
 
 namespace qvg {
 
-// ------------------------------------------------------------------------
-// helpers
-// ------------------------------------------------------------------------
-
-// E4M3 "up" code of a finite v >= 0, from the float bits (equivalent to
-// e4m3_encode_up for every f32 input; the mantissa ceiling is one add+mask).
-__device__ __forceinline__ uint32_t e4m3_ceil_f32(float v) {
-    if (v >= 448.f) return 0x7Eu;
-    if (v < 0.015625f) return uint32_t(ceilf(v * 512.f));  // subnormal steps of 2^-9
-    uint32_t u = (__float_as_uint(v) + 0xFFFFFu) & 0xFFF00000u;
-    return (((u >> 23) - 120u) << 3) | ((u >> 20) & 7u);
-}
-
-// Branch-free exact E4M3 -> f32: the 7 magnitude bits placed at f32 bit 20
-// read as 2^(e-127)(1+m/8) (or the denormal m*2^-129 when e == 0); scaling by
-// 2^120 (exact) gives (8+m)*2^(e-10), resp. m*2^-9.
-__device__ __forceinline__ float e4m3_decode_fast(uint32_t b) {
-    const float mag = __uint_as_float((b & 0x7Fu) << 20) * 1.329227995784916e36f;   // 2^120
-    return __uint_as_float(__float_as_uint(mag) | ((b & 0x80u) << 24));
-}
-
-template <bool XBF16>
-__device__ __forceinline__ void load_x8(const void *x, int64_t elem, float r[8]) {
-    if constexpr (XBF16) {
-        uint4 w = __ldg(reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(x) + elem));
-        r[0] = bf16_lo(w.x); r[1] = bf16_hi(w.x); r[2] = bf16_lo(w.y); r[3] = bf16_hi(w.y);
-        r[4] = bf16_lo(w.z); r[5] = bf16_hi(w.z); r[6] = bf16_lo(w.w); r[7] = bf16_hi(w.w);
-    } else {
-        const float4 *p = reinterpret_cast<const float4 *>(static_cast<const float *>(x) + elem);
-        float4 a = __ldg(p), b = __ldg(p + 1);
-        r[0] = a.x; r[1] = a.y; r[2] = a.z; r[3] = a.w; r[4] = b.x; r[5] = b.y; r[6] = b.z; r[7] = b.w;
-    }
-}
-
-__device__ __forceinline__ void load_c8(const uint16_t *c, float r[8]) {
-    uint4 w = __ldg(reinterpret_cast<const uint4 *>(c));
-    r[0] = bf16_lo(w.x); r[1] = bf16_hi(w.x); r[2] = bf16_lo(w.y); r[3] = bf16_hi(w.y);
-    r[4] = bf16_lo(w.z); r[5] = bf16_hi(w.z); r[6] = bf16_lo(w.w); r[7] = bf16_hi(w.w);
-}
-
-// XK: 0 f32, 1 bf16, 2 f64
-template <int XK>
-__device__ __forceinline__ double load_x1(const void *x, int64_t elem) {
-    if constexpr (XK == 1) return double(bf16_to_f32(static_cast<const uint16_t *>(x)[elem]));
-    else if constexpr (XK == 2) return static_cast<const double *>(x)[elem];
-    else return double(static_cast<const float *>(x)[elem]);
-}
-
-// ------------------------------------------------------------------------
-// index helpers: n / N for the flattened [P*N] row space (< 2^32 rows) with a
-// multiply-high (Granlund-Montgomery "round-up" variant, exact for all u32 n)
-// ------------------------------------------------------------------------
-struct FastDiv {
-    uint32_t m, l;
-    __device__ __forceinline__ uint32_t div(uint32_t n) const {
-        return uint32_t((uint64_t(__umulhi(n, m)) + n) >> l);
-    }
-};
-
-static FastDiv make_fastdiv(uint32_t d) {
-    uint32_t l = 0;
-    while ((uint64_t(1) << l) < d) l++;
-    uint64_t m = ((uint64_t(1) << 32) * ((uint64_t(1) << l) - d)) / d + 1;
-    return FastDiv{uint32_t(m), l};
-}
-
-// Tile mapping shared by K5/K6.  A tile is kUnroll*256/VPR consecutive rows
-// of ONE plane (VPR = d/8 threads per row, each owning 8 channels), so the
-// plane index is one division per tile and every in-plane offset is 32-bit.
-// The tile loop is block-uniform, so every lane reaches every shuffle.
-constexpr int kUnroll = 2;
-
-struct TileArgs {
-    uint32_t n_tiles, tpp;       // tiles in total / per plane
-    FastDiv div_tpp;
-    uint32_t rows_per_pass;      // 256 >> lvpr
-};
-
-// E4M3 code of RN64(A/QMAX) for every A in [lo, hi] (f32, lo > 0), or
-// ambiguous.  Products QMAX * grid value are exact in f32 (<= 11 bits).
-template <int QMAX>
-__device__ __forceinline__ float grid_val(uint32_t code) { return e4m3_to_f32(code) * float(QMAX); }
-
-// E4M3 "up" code without branches (v >= 0 finite, saturating at 448)
-__device__ __forceinline__ uint32_t e4m3_ceil_f32_bf(float v) {
-    const float vc = fminf(v, 448.f);
-    const uint32_t sub = uint32_t(ceilf(vc * 512.f));                        // subnormal steps
-    const uint32_t nrm = (((__float_as_uint(vc) + 0xFFFFFu) >> 20) - (120u << 3));
-    return vc < 0.015625f ? sub : nrm;
-}
-
-template <int QMAX>
-__device__ __forceinline__ uint32_t scale_code(float lo, float hi, bool &amb) {
-    if constexpr (QMAX == 1) {
-        // code(A) for A in [lo, hi] is certain iff ceil(lo) == ceil(hi)
-        const uint32_t c = e4m3_ceil_f32_bf(hi);
-        amb = c != e4m3_ceil_f32_bf(lo);
-        return c;
-    }
-    uint32_t c = e4m3_ceil_f32(QMAX == 1 ? hi : __fmul_ru(hi, 1.0f / QMAX * 1.0000002f));
-    if (QMAX > 1) {   // make c the exact ceil code of hi/QMAX
-        while (c > 1 && hi <= grid_val<QMAX>(c - 1)) c--;
-        while (c < 0x7Eu && hi > grid_val<QMAX>(c)) c++;
-    }
-    if (c == 0x7Eu) amb = !(lo > float(QMAX) * 416.f);        // saturating band (416, 448]
-    else amb = c > 0 && !(lo > grid_val<QMAX>(c - 1));
-    return c;
-}
-
-
-template <bool XBF16>
-__device__ __forceinline__ float load_x1f(const void *x, uint64_t e) {
-    if constexpr (XBF16) return bf16_to_f32(static_cast<const uint16_t *>(x)[e]);
-    else return static_cast<const float *>(x)[e];
-}
-
-// Rare-path helpers, kept out of line so the compiler cannot hoist their
-// address arithmetic into the streaming loop.
-// The reference's float64 residual x - C_1[pi_1] - ... (Q/smoothing.py:40).
-template <bool XBF16, int S>
-__device__ __noinline__ double exact_residual(const uint8_t *xb, const uint16_t *cp, uint32_t e,
-                                             uint32_t col, uint32_t d, int K, int a0, int a1,
-                                             int a2, int a3) {
-    double v = double(load_x1f<XBF16>(xb, e));
-    const int ai[4] = {a0, a1, a2, a3};
-#pragma unroll
-    for (int t = 0; t < S; t++) v = __dsub_rn(v, double(bf16_to_f32(cp[uint32_t(t * K + ai[t]) * d + col])));
-    return v;
-}
-
-// q = clip(rint(RN64(r / s))) (Q/quant.py:53-54)
-template <int QMAX>
-__device__ __noinline__ uint32_t exact_code(double r, float s) {
-    const double qd = fmin(fmax(rint(__ddiv_rn(r, double(s))), -double(QMAX)), double(QMAX));
-    return uint32_t(int(qd));
-}
-
-// ------------------------------------------------------------------------
-// K5 quantize (fast path: d/8 a power of two <= 32, B/8 a power of two, S <= 4)
-// ------------------------------------------------------------------------
-struct QuantArgs {
-    const void *x;
-    const uint16_t *cent;   // [P][S][K][d]
-    const uint8_t *asg;     // [P][S][N]
-    uint8_t *payload;       // [P][PB]
-    uint8_t *scales;        // [P][N*d/B]
-    uint32_t N;
-    int d, K, B, lvpr, gshift;
-    int32_t *status;
-    uint32_t pb, ng, lgB;   // payload bytes / scale bytes per plane, log2(B)
-    TileArgs ta;
-    int v16;                // 16 channels per thread (k_quantize_v4/v5)
-    int v5;                 // CTAs per SM for k_quantize_v5 (0: not used)
-    uint32_t P;
-    uint32_t one;           // always 1 (see k_quantize_v5)
-};
 
 template <int BITS, int S, bool XBF16>
 __global__ void __launch_bounds__(256) k_quantize_v3(QuantArgs a) {
@@ -392,21 +240,6 @@ __global__ void k_quantize_generic_pack(const void *x, const uint16_t *cent, con
 // ------------------------------------------------------------------------
 // K6 dequantize (fast path: d/8 and B powers of two, B % 8 == 0, S <= 4)
 // ------------------------------------------------------------------------
-struct DequantArgs {
-    const uint8_t *payload;
-    const uint8_t *scales;
-    const uint16_t *cent;
-    const uint8_t *asg;
-    void *out;
-    uint32_t N;
-    int d, K, B, lvpr;
-    int32_t *status;
-    uint32_t pb, ng, lgB;
-    TileArgs ta;
-    int v16;                // 16 channels per thread (k_dequant_v4/v5)
-    int v5;                 // CTAs per SM for k_dequant_v5 (0: not used)
-    uint32_t P;
-};
 
 // signed b-bit field k of w as an exact float: (u ^ sign) - sign via the
 // 1.5*2^23 magic (used by the rare f64 path)
@@ -603,60 +436,6 @@ __global__ void k_unpack_codes(const uint8_t *in, int64_t n, int bits, int8_t *o
 // halving the per-row index/address/decode overhead of the 8-channel layout,
 // with the per-element work written to split between the ALU and FMA pipes.
 // ------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t lop3_and_or(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t d;
-    asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(b), "r"(c));   // (a & b) | c
-    return d;
-}
-
-template <int BITS>
-struct Codes16 {                     // 16 b-bit fields
-    static constexpr int NW = BITS / 2;
-    uint32_t w[NW];
-};
-
-template <int BITS>
-__device__ __forceinline__ Codes16<BITS> load_codes16(const uint8_t *p) {
-    Codes16<BITS> c;
-    if constexpr (BITS == 2) c.w[0] = __ldg(reinterpret_cast<const uint32_t *>(p));
-    else if constexpr (BITS == 4) { uint2 v = __ldg(reinterpret_cast<const uint2 *>(p)); c.w[0] = v.x; c.w[1] = v.y; }
-    else { uint4 v = __ldg(reinterpret_cast<const uint4 *>(p)); c.w[0] = v.x; c.w[1] = v.y; c.w[2] = v.z; c.w[3] = v.w; }
-    return c;
-}
-
-// exact q*s of field k (see qs_fma): field moved to the top of the mantissa
-// with one shift + one LOP3, then one FFMA
-template <int BITS>
-__device__ __forceinline__ float qs16(const Codes16<BITS> &wx, int k, uint32_t mhi, uint32_t one,
-                                      float s_hi, float s_off) {
-    constexpr int POS = 23 - BITS;
-    const int bit = k * BITS, wi = bit >> 5, off = bit & 31;
-    const uint32_t v = off <= POS ? (wx.w[wi] << (POS - off)) : (wx.w[wi] >> (off - POS));
-    return __fmaf_rn(__uint_as_float(lop3_and_or(v, mhi, one)), s_hi, s_off);
-}
-
-__device__ __forceinline__ void cvt16(uint4 a, uint4 b, float c[16]) {
-    c[0] = bf16_lo(a.x); c[1] = bf16_hi(a.x); c[2] = bf16_lo(a.y); c[3] = bf16_hi(a.y);
-    c[4] = bf16_lo(a.z); c[5] = bf16_hi(a.z); c[6] = bf16_lo(a.w); c[7] = bf16_hi(a.w);
-    c[8] = bf16_lo(b.x); c[9] = bf16_hi(b.x); c[10] = bf16_lo(b.y); c[11] = bf16_hi(b.y);
-    c[12] = bf16_lo(b.z); c[13] = bf16_hi(b.z); c[14] = bf16_lo(b.w); c[15] = bf16_hi(b.w);
-}
-
-template <bool XBF16>
-__device__ __forceinline__ void load_x16(const uint8_t *xb, uint32_t e, float r[16]) {
-    if constexpr (XBF16) {
-        const uint4 *p = reinterpret_cast<const uint4 *>(xb + uint64_t(e) * 2);
-        cvt16(__ldg(p), __ldg(p + 1), r);
-    } else {
-        const float4 *p = reinterpret_cast<const float4 *>(xb + uint64_t(e) * 4);
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const float4 v = __ldg(p + j);
-            r[4 * j] = v.x; r[4 * j + 1] = v.y; r[4 * j + 2] = v.z; r[4 * j + 3] = v.w;
-        }
-    }
-}
-
 template <int BITS, int S, bool OBF16>
 __global__ void __launch_bounds__(256) k_dequant_v4(DequantArgs a) {
     constexpr int SS = S > 0 ? S : 1;
@@ -932,43 +711,6 @@ __global__ void __launch_bounds__(256) k_quantize_v4(QuantArgs a) {
 // (cp.async.bulk, double-buffered on mbarriers) so the per-token centroid
 // gather is an LDS instead of a dependent L2 round trip.
 // ------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return uint32_t(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n.reg .pred P1;\nWAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-struct PlaneLoop {
-    uint32_t P, tbytes;          // planes, centroid-table bytes per plane (S*K*d*2)
-};
-
-// issue the bulk copy of plane p's centroid table into buffer b
-__device__ __forceinline__ void stage_table(const uint16_t *cent, uint32_t p, uint32_t tbytes,
-                                            uint16_t *buf, uint64_t *bar) {
-    mbar_arrive_expect_tx(bar, tbytes);
-    bulk_g2s(buf, reinterpret_cast<const uint8_t *>(cent) + uint64_t(p) * tbytes, tbytes, bar);
-}
-
 template <int BITS, int S, bool OBF16>
 __global__ void __launch_bounds__(256) k_dequant_v5(DequantArgs a, PlaneLoop pl) {
     constexpr int SS = S > 0 ? S : 1;
@@ -1271,6 +1013,496 @@ __global__ void __launch_bounds__(256) k_quantize_v5(QuantArgs a, PlaneLoop pl) 
 }
 
 // ------------------------------------------------------------------------
+// v6: the per-plane centroid tables are widened ONCE to f32 in shared memory
+// (XOR-swizzled so the 8 threads of a row read 8 distinct bank groups), next
+// to per-(stage, centroid, 16-channel chunk) metadata {ulp of the smallest
+// non-zero |c|, max |c|}.  The element loop is then pure packed f32x2
+// arithmetic (FADD2/FFMA2) plus 3-input max/min reductions:
+//  * quantize: codes come from the magic-number rounding fma(r, 1/s, 1.5*2^23
+//    + 2^(b-1)) whose float bits carry q + 2^(b-1) in the low mantissa, and
+//    are packed with one integer multiply-add per element; the ambiguity
+//    test is one reduction per row (2-bit: min |r^2 - (s/2)^2|, b>2: max
+//    distance to the rounded value), and the residual error bound comes
+//    from the metadata instead of a per-element max;
+//  * dequantize: the exactness of the non-final f32 partial sums is
+//    certified per row from the metadata (every term is a multiple of the
+//    smallest ulp and the sum stays below 2^24 of it); a row without the
+//    certificate is recomputed with the reference's float64 chain.
+// ------------------------------------------------------------------------
+struct V6Plane {
+    uint32_t P;        // planes
+    uint32_t tbytes;   // bf16 table bytes per plane (S*K*d*2)
+    uint32_t nchunk;   // S*K*d/16 metadata entries per plane
+    uint32_t lchunk;   // log2(d/16)
+    uint32_t ipp;      // work items (row ranges) per plane
+    uint32_t rpi;      // rows per item
+    uint32_t n_items;  // P * ipp; CTA b owns the contiguous items [b*n/G, (b+1)*n/G)
+};
+
+// swizzled float offset of channel ch inside a table row: 16-byte chunk L
+// goes to L ^ ((L >> 3) & 3)
+__device__ __forceinline__ uint32_t v6_swz(uint32_t ch) {
+    const uint32_t L = ch >> 2;
+    return ((L ^ ((L >> 3) & 3u)) << 2) | (ch & 3u);
+}
+
+__device__ __forceinline__ float max3_nan_abs(float m, float a, float b) {
+    float t, d;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(t) : "f"(fabsf(a)), "f"(fabsf(b)));
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(m), "f"(t));
+    return d;
+}
+
+// widen the staged bf16 tables [S*K][d] to swizzled f32 + chunk metadata
+__device__ __forceinline__ void v6_widen(const uint16_t *stg, float *tab, float2 *meta, const V6Plane &pl,
+                                         uint32_t d) {
+    const uint32_t cmask = (1u << pl.lchunk) - 1u;
+    for (uint32_t q = threadIdx.x; q < pl.nchunk; q += blockDim.x) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(stg + size_t(q) * 16);
+        float c[16];
+        cvt16(src[0], src[1], c);
+        float mx = 0.f, mn = __int_as_float(0x7F800000);
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            const float a = fabsf(c[k]);
+            mx = fmaxf(mx, a);
+            mn = a > 0.f ? fminf(mn, a) : mn;
+        }
+        float *dst = tab + size_t(q >> pl.lchunk) * d;
+        const uint32_t ch0 = (q & cmask) << 4;
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            *reinterpret_cast<float4 *>(dst + v6_swz(ch0 + 4 * j)) =
+                make_float4(c[4 * j], c[4 * j + 1], c[4 * j + 2], c[4 * j + 3]);
+        // ulp of a bf16 value with the exponent of mn: 2^(e-7); 0 when that is
+        // not a normal float (certificate then fails, conservatively); +inf
+        // when the chunk is all zero (no constraint)
+        float unit;
+        if (mn == __int_as_float(0x7F800000)) unit = mn;
+        else {
+            const uint32_t eb = __float_as_uint(mn) & 0x7F800000u;
+            unit = eb > (7u << 23) ? __uint_as_float(eb - (7u << 23)) : 0.f;
+        }
+        // NaN/Inf anywhere in the chunk: max is NaN/Inf, which fails every
+        // certificate below (comparisons with NaN are false)
+        meta[q] = make_float2(unit, mx);
+    }
+}
+
+// item-loop prologue shared by K5/K6 v6 on a plane change: wait for plane
+// p's staged table, widen it, then stage the next plane this CTA will visit
+__device__ __forceinline__ void v6_plane_tables(const uint16_t *cent, uint32_t j, int64_t next_p,
+                                                const V6Plane &pl, uint16_t *stg, float *tab, float2 *meta,
+                                                uint64_t *bar, uint32_t d) {
+    __syncthreads();                          // everyone done with the previous plane's tables
+    mbar_wait(bar, j & 1u);
+    v6_widen(stg, tab, meta, pl, d);
+    __syncthreads();                          // tables ready; staging buffer free
+    if (threadIdx.x == 0 && next_p >= 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        stage_table(cent, uint32_t(next_p), pl.tbytes, stg, bar);
+    }
+}
+
+// this CTA's contiguous item range
+__device__ __forceinline__ void v6_items(const V6Plane &pl, uint32_t &it0, uint32_t &it1) {
+    it0 = uint32_t((uint64_t(blockIdx.x) * pl.n_items) / gridDim.x);
+    it1 = uint32_t((uint64_t(blockIdx.x + 1) * pl.n_items) / gridDim.x);
+}
+
+// the reference's float64 add-back for one element (Q/prq.py:113-132), f32 table
+template <int S>
+__device__ __noinline__ float v6_exact_addback(float qs, const float *tab, uint32_t off, uint32_t d, int K,
+                                               int a0, int a1, int a2, int a3) {
+    const int ai[4] = {a0, a1, a2, a3};
+    double acc = double(qs);
+#pragma unroll
+    for (int t = S - 1; t >= 0; t--) acc = __dadd_rn(acc, double(tab[uint32_t(t * K + ai[t]) * d + off]));
+    return __double2float_rn(acc);
+}
+
+// the reference's float64 residual x - C_1[pi_1] - ... (Q/smoothing.py:40), f32 table
+template <bool XBF16, int S>
+__device__ __noinline__ double v6_exact_residual(const uint8_t *xb, const float *tab, uint32_t e, uint32_t off,
+                                                 uint32_t d, int K, int a0, int a1, int a2, int a3) {
+    double v = double(load_x1f<XBF16>(xb, e));
+    const int ai[4] = {a0, a1, a2, a3};
+#pragma unroll
+    for (int t = 0; t < S; t++) v = __dsub_rn(v, double(tab[uint32_t(t * K + ai[t]) * d + off]));
+    return v;
+}
+
+template <int BITS, int S, bool OBF16>
+__global__ void __launch_bounds__(256, 2) k_dequant_v6(DequantArgs a, V6Plane pl) {
+    constexpr int SS = S > 0 ? S : 1;
+    constexpr int U = 2;
+    constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bar;
+    uint16_t *const stg = reinterpret_cast<uint16_t *>(smem);
+    float *const tab = reinterpret_cast<float *>(smem + pl.tbytes);
+    float2 *const meta = reinterpret_cast<float2 *>(smem + 3 * size_t(pl.tbytes));
+    const uint32_t mhi = ((1u << BITS) - 1u) << (23 - BITS), one = 0x3F800000u;
+    const uint32_t d = uint32_t(a.d), N = a.N;
+    const uint32_t c = threadIdx.x & ((1u << a.lvpr) - 1u);
+    const int col = int(c) << 4;
+    const uint32_t rslot = threadIdx.x >> a.lvpr, rpp = 256u >> a.lvpr;
+    uint32_t off[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) off[j] = v6_swz(uint32_t(col + 4 * j));
+    bool bad_scale = false, bad_asg = false;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t it0, it1;
+    v6_items(pl, it0, it1);
+    if (S > 0 && threadIdx.x == 0 && it0 < it1) stage_table(a.cent, it0 / pl.ipp, pl.tbytes, stg, &bar);
+    uint32_t jp = 0, cur = 0xFFFFFFFFu;
+    for (uint32_t it = it0; it < it1; it++) {
+        const uint32_t p = it / pl.ipp;
+        const uint32_t r0 = (it - p * pl.ipp) * pl.rpi, r1 = min(N, r0 + pl.rpi);
+        if (p != cur) {
+            const int64_t nxt = int64_t(p + 1) * pl.ipp < int64_t(it1) ? int64_t(p + 1) : -1;
+            if (S > 0) v6_plane_tables(a.cent, jp, nxt, pl, stg, tab, meta, &bar, d);
+            cur = p;
+            jp++;
+        }
+        const uint64_t pN = uint64_t(p) * N;
+        const uint8_t *pp = a.payload + uint64_t(p) * a.pb;
+        const uint8_t *sp = a.scales + uint64_t(p) * a.ng;
+        const uint8_t *ap = a.asg + pN * S;
+        for (uint32_t i0 = r0; i0 < r1; i0 += rpp * U) {
+            Codes16<BITS> w[U];
+            uint32_t sc[U], ii[U];
+            int ai[U][SS];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t i = i0 + u * rpp + rslot;
+                ii[u] = i < r1 ? i : r1 - 1;
+                const uint32_t e0 = ii[u] * d + col;
+                w[u] = load_codes16<BITS>(pp + ((e0 * BITS) >> 3));
+                sc[u] = __ldg(sp + (e0 >> a.lgB));
+#pragma unroll
+                for (int t = 0; t < S; t++) {
+                    const int at = __ldg(ap + t * N + ii[u]);
+                    bad_asg |= at >= a.K;
+                    ai[u][t] = at < a.K ? at : 0;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const bool valid = i0 + u * rpp + rslot < r1;
+                bad_scale |= (sc[u] & 0x7Fu) == 0x7Fu;
+                const float s = e4m3_decode_fast(sc[u]);
+                Codes16<BITS> wx;
+#pragma unroll
+                for (int q = 0; q < Codes16<BITS>::NW; q++) wx.w[q] = w[u].w[q] ^ SIGNS;
+                const float2 s_hi = make_float2(s * float(1 << BITS), s * float(1 << BITS));
+                const float2 s_off = make_float2(s * (-1.5f * float(1 << BITS)), s * (-1.5f * float(1 << BITS)));
+                float2 y[8];
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    const int k0 = 2 * k, k1 = 2 * k + 1;
+                    constexpr int POS = 23 - BITS;
+                    const int b0 = k0 * BITS, b1 = k1 * BITS;
+                    const uint32_t v0 = (b0 & 31) <= POS ? (wx.w[b0 >> 5] << (POS - (b0 & 31))) : (wx.w[b0 >> 5] >> ((b0 & 31) - POS));
+                    const uint32_t v1 = (b1 & 31) <= POS ? (wx.w[b1 >> 5] << (POS - (b1 & 31))) : (wx.w[b1 >> 5] >> ((b1 & 31) - POS));
+                    const float2 f = make_float2(__uint_as_float(lop3_and_or(v0, mhi, one)),
+                                                 __uint_as_float(lop3_and_or(v1, mhi, one)));
+                    y[k] = __ffma2_rn(f, s_hi, s_off);          // q*s, exact
+                }
+                // certificate: every non-final partial sum exact in f32
+                bool cert = true;
+                if constexpr (S >= 2) {
+                    float unit = fmaxf(__uint_as_float((__float_as_uint(s) & 0x7F800000u) - (3u << 23)), 0.001953125f);
+                    float bound = s * float(1 << (BITS - 1));
+#pragma unroll
+                    for (int t = 1; t < S; t++) {
+                        const float2 m = meta[(uint32_t(t * a.K + ai[u][t]) << pl.lchunk) + c];
+                        unit = fminf(unit, m.x);
+                        bound = __fadd_ru(bound, m.y);
+                    }
+                    cert = bound < unit * 16777216.f;
+                }
+#pragma unroll
+                for (int t = S - 1; t >= 0; t--) {                 // reversed(stages)
+                    const float *row = tab + uint32_t(t * a.K + ai[u][t]) * d;
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        const float4 cv = *reinterpret_cast<const float4 *>(row + off[j]);
+                        y[2 * j] = __fadd2_rn(y[2 * j], make_float2(cv.x, cv.y));
+                        y[2 * j + 1] = __fadd2_rn(y[2 * j + 1], make_float2(cv.z, cv.w));
+                    }
+                }
+                if (!cert) {   // rare: recompute the row with the float64 chain
+#pragma unroll
+                    for (int k = 0; k < 16; k++) {
+                        const int b = k * BITS, wi = b >> 5, o = b & 31;
+                        constexpr int POS = 23 - BITS;
+                        const uint32_t v = o <= POS ? (wx.w[wi] << (POS - o)) : (wx.w[wi] >> (o - POS));
+                        const float qs = __fmaf_rn(__uint_as_float(lop3_and_or(v, mhi, one)), s_hi.x, s_off.x);
+                        const float r = v6_exact_addback<S>(qs, tab, off[k >> 2] + (k & 3), d, a.K, ai[u][0],
+                                                            ai[u][SS > 1 ? 1 : 0], ai[u][SS > 2 ? 2 : 0],
+                                                            ai[u][SS > 3 ? 3 : 0]);
+                        if (k & 1) y[k >> 1].y = r; else y[k >> 1].x = r;
+                    }
+                }
+                if (!valid) continue;
+                const uint64_t o = (pN + ii[u]) * d + col;
+                if constexpr (OBF16) {
+                    uint32_t v[8];
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        __nv_bfloat162 h = __floats2bfloat162_rn(y[q].x, y[q].y);
+                        v[q] = *reinterpret_cast<uint32_t *>(&h);
+                    }
+                    uint4 *op = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(a.out) + o);
+                    op[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                    op[1] = make_uint4(v[4], v[5], v[6], v[7]);
+                } else {
+                    float4 *op = reinterpret_cast<float4 *>(static_cast<float *>(a.out) + o);
+#pragma unroll
+                    for (int q = 0; q < 4; q++) op[q] = make_float4(y[2 * q].x, y[2 * q].y, y[2 * q + 1].x, y[2 * q + 1].y);
+                }
+            }
+        }
+    }
+    const uint32_t stat = (bad_scale ? QVG_STATUS_NAN_SCALE : 0u) | (bad_asg ? QVG_STATUS_BAD_ASSIGN : 0u);
+    const uint32_t all = __reduce_or_sync(0xffffffffu, stat);
+    if (all && (threadIdx.x & 31) == 0) atomicOr(a.status, int(all));
+}
+
+// packing constant: sum over the fields of one word of 0x4B400000 << (b*k)
+template <int BITS>
+__host__ __device__ constexpr uint32_t v6_magic_sum() {
+    uint32_t acc = 0;
+    for (int k = 0; k < 32 / BITS; k++) acc += 0x4B400000u << (BITS * k);
+    return acc;
+}
+
+template <int BITS, int S, bool XBF16>
+__global__ void __launch_bounds__(256, 2) k_quantize_v6(QuantArgs a, V6Plane pl) {
+    constexpr int QMAX = (1 << (BITS - 1)) - 1;
+    constexpr int SS = S > 0 ? S : 1;
+    constexpr int U = 2;
+    constexpr int FPW = 32 / BITS;                       // fields per payload word
+    constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
+    constexpr float MAGIC = 12582912.f + float(1 << (BITS - 1));   // 1.5*2^23 + bias
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bar;
+    uint16_t *const stg = reinterpret_cast<uint16_t *>(smem);
+    float *const tab = reinterpret_cast<float *>(smem + pl.tbytes);
+    float2 *const meta = reinterpret_cast<float2 *>(smem + 3 * size_t(pl.tbytes));
+    const uint32_t d = uint32_t(a.d), N = a.N;
+    const uint32_t c = threadIdx.x & ((1u << a.lvpr) - 1u);
+    const int col = int(c) << 4;
+    const uint32_t rslot = threadIdx.x >> a.lvpr, rpp = 256u >> a.lvpr;
+    const int glanes = 1 << a.gshift;
+    const int lane = threadIdx.x & 31;
+    uint32_t off[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) off[j] = v6_swz(uint32_t(col + 4 * j));
+    bool nonfinite = false;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t it0, it1;
+    v6_items(pl, it0, it1);
+    if (S > 0 && threadIdx.x == 0 && it0 < it1) stage_table(a.cent, it0 / pl.ipp, pl.tbytes, stg, &bar);
+    uint32_t jp = 0, cur = 0xFFFFFFFFu;
+    for (uint32_t it = it0; it < it1; it++) {
+        const uint32_t p = it / pl.ipp;
+        const uint32_t r0 = (it - p * pl.ipp) * pl.rpi, r1 = min(N, r0 + pl.rpi);
+        if (p != cur) {
+            const int64_t nxt = int64_t(p + 1) * pl.ipp < int64_t(it1) ? int64_t(p + 1) : -1;
+            if (S > 0) v6_plane_tables(a.cent, jp, nxt, pl, stg, tab, meta, &bar, d);
+            cur = p;
+            jp++;
+        }
+        const uint64_t pN = uint64_t(p) * N;
+        const uint8_t *xb = static_cast<const uint8_t *>(a.x) + pN * d * (XBF16 ? 2 : 4);
+        const uint8_t *ap = a.asg + pN * S;
+        for (uint32_t i0 = r0; i0 < r1; i0 += rpp * U) {
+            float2 r[U][8];
+            uint32_t ii[U];
+            int ai[U][SS];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const uint32_t i = i0 + u * rpp + rslot;
+                ii[u] = i < r1 ? i : r1 - 1;
+                load_x16<XBF16>(xb, ii[u] * d + col, reinterpret_cast<float *>(r[u]));
+#pragma unroll
+                for (int t = 0; t < S; t++) ai[u][t] = __ldg(ap + t * N + ii[u]);
+            }
+            float eb[U], am[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                // sum_t max|r_t| <= S*max|r_S| + sum_t t*max|c_{t+1}| (|r_t| <= |r_S| + sum_{v>t}|c_v|)
+                float cb = 0.f;
+#pragma unroll
+                for (int t = 0; t < S; t++) {
+                    const float *row = tab + uint32_t(t * a.K + ai[u][t]) * d;
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        const float4 cv = *reinterpret_cast<const float4 *>(row + off[j]);
+                        r[u][2 * j] = __fadd2_rn(r[u][2 * j], make_float2(-cv.x, -cv.y));
+                        r[u][2 * j + 1] = __fadd2_rn(r[u][2 * j + 1], make_float2(-cv.z, -cv.w));
+                    }
+                    if (t > 0) cb = __fmaf_ru(float(t), meta[(uint32_t(t * a.K + ai[u][t]) << pl.lchunk) + c].y, cb);
+                }
+                // max|r| with NaN propagation: NaN/Inf in x or a centroid -> non-finite am
+                float mx = 0.f;
+#pragma unroll
+                for (int k = 0; k < 8; k++) mx = max3_nan_abs(mx, r[u][k].x, r[u][k].y);
+                nonfinite |= !(mx <= 3.402823466e38f) || !(cb <= 3.402823466e38f);
+                am[u] = mx;
+                eb[u] = S > 0 ? __fmaf_ru(float(S), mx, cb) : 0.f;
+            }
+            for (int m = 1; m < glanes; m <<= 1) {
+#pragma unroll
+                for (int u = 0; u < U; u++) {
+                    am[u] = fmaxf(am[u], __shfl_xor_sync(0xffffffffu, am[u], m));
+                    eb[u] = fmaxf(eb[u], __shfl_xor_sync(0xffffffffu, eb[u], m));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; u++) {
+                const bool valid = i0 + u * rpp + rslot < r1;
+                const float E = __fmul_ru(eb[u], 2.38418579e-7f);      // 2^-22
+                uint32_t code;
+                bool camb = false;
+                if (am[u] == 0.f && E == 0.f) code = 0x38u;
+                else {
+                    const float lo = __fsub_rd(am[u], E), hi = __fadd_ru(am[u], E);
+                    if (lo > 0.f) code = scale_code<QMAX>(lo, hi, camb);
+                    else { code = 0x38u; camb = true; }
+                }
+                camb &= valid;
+                const float *rf = reinterpret_cast<const float *>(r[u]);
+                auto exact_r = [&](int k) {
+                    return v6_exact_residual<XBF16, S>(xb, tab, ii[u] * d + col + k, off[k >> 2] + (k & 3), d,
+                                                       a.K, ai[u][0], ai[u][SS > 1 ? 1 : 0],
+                                                       ai[u][SS > 2 ? 2 : 0], ai[u][SS > 3 ? 3 : 0]);
+                };
+                if (__any_sync(0xffffffffu, camb)) {          // exact scale (rare)
+                    const float thr = __fsub_rd(am[u], __fmul_ru(E, 2.f));
+                    uint32_t cand = 0;
+#pragma unroll
+                    for (int k = 0; k < 16; k++) cand |= (camb && fabsf(rf[k]) >= thr) ? 1u << k : 0u;
+                    double a64 = 0.0;
+                    while (cand) {
+                        const int k = __ffs(cand) - 1;
+                        cand &= cand - 1;
+                        a64 = fmax(a64, fabs(exact_r(k)));
+                    }
+                    for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
+                    if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
+                }
+                const float s = e4m3_decode_fast(code);
+                const float inv = __frcp_rn(s);
+                const float2 inv2 = make_float2(inv, inv);
+                // codes: bits of fma(r, 1/s, MAGIC) = 0x4B400000 + q + 2^(b-1)
+                uint32_t acc[BITS / 2];
+#pragma unroll
+                for (int q = 0; q < BITS / 2; q++) acc[q] = 0u;
+                float2 yv[8];
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    yv[k] = __ffma2_rn(r[u][k], inv2, make_float2(MAGIC, MAGIC));
+                    const int k0 = 2 * k, k1 = 2 * k + 1;
+                    acc[k0 / FPW] += __float_as_uint(yv[k].x) << (BITS * (k0 % FPW));
+                    acc[k1 / FPW] += __float_as_uint(yv[k].y) << (BITS * (k1 % FPW));
+                }
+                uint32_t b32[BITS / 2];
+#pragma unroll
+                for (int q = 0; q < BITS / 2; q++) b32[q] = (acc[q] - v6_magic_sum<BITS>()) ^ SIGNS;
+                // ambiguity: an element whose exact code could differ.  The
+                // per-element predicate in_window(k) is evaluated once as a row
+                // reduction and again, identically, to pick the elements to fix.
+                const bool all = !(E < 0.125f * s) || code == 0x7Eu;    // loose bound / saturation: check all
+                float2 pa, pb;    // predicate constants
+                float thr;
+                if constexpr (QMAX == 1) {
+                    // ||r| - s/2| <= W  =>  |r^2 - (s/2)^2| <= W (s + W) (up to rounding),
+                    // W = E + the 1/s rounding of the decision
+                    const float h = 0.5f * s;
+                    const float W = __fmaf_ru(h, 2.38418579e-7f, E);
+                    thr = __fmul_ru(__fmul_ru(W, __fadd_ru(s, W)), 1.00000095367f);
+                    pa = make_float2(-h * h, -h * h);
+                    pb = pa;
+                } else {
+                    // |t - rint(t)| >= 1/2 - delta, t = r/s; delta covers E/s, the
+                    // 1/s rounding and the reference's float64 division
+                    const float delta = __fmaf_ru(__fmul_ru(E, inv), 1.0000002f, float(QMAX + 1) * 2.38418579e-7f);
+                    thr = __fsub_rd(0.5f, delta);
+                    pa = make_float2(-MAGIC, -MAGIC);
+                    pb = pa;
+                }
+                (void)pb;
+                auto window = [&](int k) -> float2 {     // |g| (2-bit) or |t - q| (b > 2) of pair k
+                    if constexpr (QMAX == 1) {
+                        const float2 g = __ffma2_rn(r[u][k], r[u][k], pa);
+                        return make_float2(fabsf(g.x), fabsf(g.y));
+                    } else {
+                        const float2 qf = __fadd2_rn(yv[k], pa);
+                        const float2 dist = __ffma2_rn(r[u][k], inv2, make_float2(-qf.x, -qf.y));
+                        return make_float2(fabsf(dist.x), fabsf(dist.y));
+                    }
+                };
+                bool amb;
+                if constexpr (QMAX == 1) {
+                    float gmin = __int_as_float(0x7F800000);
+#pragma unroll
+                    for (int k = 0; k < 8; k++) { const float2 g = window(k); gmin = fminf(gmin, fminf(g.x, g.y)); }
+                    amb = all || gmin <= thr;
+                } else {
+                    float dmax = 0.f;
+#pragma unroll
+                    for (int k = 0; k < 8; k++) { const float2 g = window(k); dmax = fmaxf(dmax, fmaxf(g.x, g.y)); }
+                    amb = all || dmax >= thr;
+                }
+                amb &= valid;
+                if (__any_sync(0xffffffffu, amb) && amb) {   // exact codes (rare)
+                    uint32_t todo = 0;
+#pragma unroll
+                    for (int k = 0; k < 8; k++) {
+                        const float2 g = window(k);
+                        bool in0, in1;
+                        if constexpr (QMAX == 1) { in0 = g.x <= thr; in1 = g.y <= thr; }
+                        else { in0 = g.x >= thr; in1 = g.y >= thr; }
+                        in0 |= all || !(fabsf(r[u][k].x) <= 3.402823466e38f);
+                        in1 |= all || !(fabsf(r[u][k].y) <= 3.402823466e38f);
+                        todo |= (in0 ? 1u << (2 * k) : 0u) | (in1 ? 2u << (2 * k) : 0u);
+                    }
+                    while (todo) {
+                        const int k = __ffs(todo) - 1;
+                        todo &= todo - 1;
+                        const uint32_t q = exact_code<QMAX>(exact_r(k), s) & ((1u << BITS) - 1u);
+                        const int sh = (k * BITS) & 31, wi = (k * BITS) >> 5;
+#pragma unroll
+                        for (int q2 = 0; q2 < BITS / 2; q2++)
+                            if (q2 == wi) b32[q2] = (b32[q2] & ~(((1u << BITS) - 1u) << sh)) | (q << sh);
+                    }
+                }
+                if (!valid) continue;
+                const uint32_t e0 = ii[u] * d + col;
+                uint8_t *plp = a.payload + uint64_t(p) * a.pb + ((e0 * BITS) >> 3);
+                if constexpr (BITS == 2) *reinterpret_cast<uint32_t *>(plp) = b32[0];
+                else if constexpr (BITS == 4) *reinterpret_cast<uint2 *>(plp) = make_uint2(b32[0], b32[1]);
+                else *reinterpret_cast<uint4 *>(plp) = make_uint4(b32[0], b32[1], b32[2], b32[3]);
+                if ((lane & (glanes - 1)) == 0) a.scales[uint64_t(p) * a.ng + (e0 >> a.lgB)] = uint8_t(code);
+            }
+        }
+    }
+    const uint32_t all = __reduce_or_sync(0xffffffffu, nonfinite ? uint32_t(QVG_STATUS_NONFINITE) : 0u);
+    if (all && lane == 0) atomicOr(a.status, int(all));
+}
+
+// ------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------
 static int grid_for(int64_t work, int block) {
@@ -1310,10 +1542,71 @@ static int v5_ctas_per_sm(int64_t P, uint32_t tbytes, int S) {
 }
 
 
+// warp-specialised TMA streaming kernels (qvg_stream.cu); return 0 when the
+// configuration does not fit them
+int launch_quantize_stream(const QuantArgs &a, int64_t P, int bits, int S, bool xbf16, cudaStream_t st);
+int launch_dequantize_stream(const DequantArgs &a, int64_t P, int bits, int S, bool obf16, cudaStream_t st);
+// per-warp TMA rings (qvg_wring.cu)
+int launch_quantize_wring(const QuantArgs &a, int64_t P, int bits, int S, bool xbf16, cudaStream_t st);
+
+// QVG_CODEC_KERNEL=wring|stream|v6|v5|v4 restricts the fast-path choice (A/B
+// measurements); unset = best available
+static int codec_kernel_pref() {
+    static int pref = -1;
+    if (pref < 0) {
+        const char *e = getenv("QVG_CODEC_KERNEL");
+        pref = !e ? 0 : !strcmp(e, "wring") ? 0 : !strcmp(e, "stream") ? 1 : !strcmp(e, "v6") ? 6 : !strcmp(e, "v5") ? 5 : !strcmp(e, "v4") ? 4 : 0;
+    }
+    return pref;
+}
+
+// v6 geometry: smem = staged bf16 table + f32 table + chunk metadata; work
+// items = planes split into row ranges so that every CTA has >= ~8 items
+struct V6Launch {
+    V6Plane pl;
+    size_t smem;
+    int grid;
+};
+static bool v6_plan(int64_t P, int64_t N, int d, int S, int K, V6Launch &L) {
+    if (S < 1 || d % 16 != 0 || N < 1) return false;
+    const size_t tbytes = size_t(S) * K * d * 2;
+    const size_t nchunk = size_t(S) * K * d / 16;
+    const size_t smem = 3 * tbytes + nchunk * 8;
+    if (smem > 200 * 1024) return false;
+    int per_sm = int((227 * 1024) / (smem + 2048));
+    if (per_sm > 2) per_sm = 2;                 // __launch_bounds__(256, 2)
+    const int64_t ctas = int64_t(148) * per_sm;
+    const int64_t rows_min = 512;               // keep the table widening amortised
+    int64_t ipp = 1;
+    while (P * ipp < 8 * ctas && N / (ipp * 2) >= rows_min) ipp *= 2;
+    const int64_t rpi = (N + ipp - 1) / ipp;
+    const int64_t n_items = P * ipp;
+    if (n_items >= (int64_t(1) << 31)) return false;
+    L.pl = V6Plane{uint32_t(P), uint32_t(tbytes), uint32_t(nchunk), uint32_t(ilog2(d / 16)), uint32_t(ipp),
+                   uint32_t(rpi), uint32_t(n_items)};
+    L.smem = smem;
+    L.grid = int(n_items < ctas ? n_items : ctas);
+    return true;
+}
+
 template <int BITS, int S>
 static void launch_quant_fast(const QuantArgs &a, bool xbf16, cudaStream_t st) {
     const int g = tile_grid(a.ta);
-    if (a.v16 && a.v5) {
+    const int pref = codec_kernel_pref();
+    if (S > 0 && a.v16 && pref == 0 && launch_quantize_wring(a, a.P, BITS, S, xbf16, st)) return;
+    if (S > 0 && a.v16 && pref <= 1 && launch_quantize_stream(a, a.P, BITS, S, xbf16, st)) return;
+    V6Launch L;
+    if (S > 0 && a.v16 && (pref <= 1 || pref == 6) && v6_plan(a.P, a.N, a.d, S, a.K, L)) {
+        if (xbf16) {
+            cudaFuncSetAttribute(k_quantize_v6<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
+            k_quantize_v6<BITS, S, true><<<L.grid, 256, L.smem, st>>>(a, L.pl);
+        } else {
+            cudaFuncSetAttribute(k_quantize_v6<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
+            k_quantize_v6<BITS, S, false><<<L.grid, 256, L.smem, st>>>(a, L.pl);
+        }
+        return;
+    }
+    if (a.v16 && a.v5 && pref != 4) {
         const PlaneLoop pl{a.P, uint32_t(S) * a.K * a.d * 2};
         const size_t sm = 2 * size_t(pl.tbytes);
         const int grid = int(int64_t(a.P) < int64_t(148) * a.v5 ? int64_t(a.P) : int64_t(148) * a.v5);
@@ -1391,7 +1684,20 @@ int launch_unpack(const uint8_t *in, int64_t n, int bits, int8_t *out, cudaStrea
 template <int BITS, int S>
 static void launch_deq_fast(const DequantArgs &a, bool obf16, cudaStream_t st) {
     const int g = tile_grid(a.ta);
-    if (a.v16 && a.v5) {
+    const int pref = codec_kernel_pref();
+    if (S > 0 && a.v16 && pref <= 1 && launch_dequantize_stream(a, a.P, BITS, S, obf16, st)) return;
+    V6Launch L;
+    if (S > 0 && a.v16 && (pref <= 1 || pref == 6) && v6_plan(a.P, a.N, a.d, S, a.K, L)) {
+        if (obf16) {
+            cudaFuncSetAttribute(k_dequant_v6<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
+            k_dequant_v6<BITS, S, true><<<L.grid, 256, L.smem, st>>>(a, L.pl);
+        } else {
+            cudaFuncSetAttribute(k_dequant_v6<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
+            k_dequant_v6<BITS, S, false><<<L.grid, 256, L.smem, st>>>(a, L.pl);
+        }
+        return;
+    }
+    if (a.v16 && a.v5 && pref != 4) {
         const PlaneLoop pl{a.P, uint32_t(S) * a.K * a.d * 2};
         const size_t sm = 2 * size_t(pl.tbytes);
         const int grid = int(int64_t(a.P) < int64_t(148) * a.v5 ? int64_t(a.P) : int64_t(148) * a.v5);

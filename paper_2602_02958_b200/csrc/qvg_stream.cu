@@ -1,0 +1,668 @@
+// qvg_stream.cu — K5 quantize / K6 dequantize as warp-specialised TMA
+// streaming kernels (the "v7" fast path for the HBM-bound codec).
+//
+// One persistent CTA per SM = 16 consumer warps + 1 producer warp.
+//  * The producer streams the row-major inputs of the CTA's work items
+//    (plane, row range) through an NST-stage shared-memory ring: the big
+//    stream (bf16/f32 K/V rows for K5, packed code rows for K6) with one
+//    cp.async.bulk per stage, the small byte streams (assignments, scales)
+//    with 4-byte cp.async, all completing on the stage's mbarrier.  Bytes in
+//    flight per SM = the ring, independent of how many warps compute.
+//  * The consumers widen each plane's bf16 centroid tables (staged by TMA one
+//    plane ahead) ONCE to f32 in a padded, bank-conflict-free layout plus
+//    per-(stage, centroid, 16-channel chunk) metadata {ulp of the smallest
+//    non-zero |c|, max|c|}, then run the packed f32x2 element loop:
+//      K5: r = x - C_1[pi_1] - ... (FADD2), amax by 3-input max, E4M3 "up"
+//          scale with the certified error bound, codes from the magic-number
+//          rounding fma(r, 1/s, 1.5*2^23 + 2^(b-1)) packed by integer
+//          multiply-add, one reduction per row for the ambiguity test;
+//      K6: q*s (FFMA2), + C_S[pi_S] ... + C_1[pi_1] (FADD2) with a per-row
+//          exactness certificate for the non-final partial sums, bf16/f32 out.
+//    Rows whose fast result is not certified are recomputed in float64 in
+//    the reference's order (Q/smoothing.py:40, Q/quant.py:40-55,
+//    Q/prq.py:113-132), so the outputs are bit-identical to the reference.
+#include "qvg_stream_dev.cuh"
+
+namespace qvg {
+namespace stream {
+
+// ============================================================================
+// K5 quantize
+// ============================================================================
+template <int BITS, int S, bool XBF16>
+__global__ void __launch_bounds__(kThreads, 1) k_quantize_stream(QuantArgs a, Geo g) {
+    constexpr int QMAX = (1 << (BITS - 1)) - 1;
+    constexpr int SS = S > 0 ? S : 1;
+    constexpr int FPW = 32 / BITS;
+    constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
+    constexpr float MAGIC = 12582912.f + float(1 << (BITS - 1));   // 1.5*2^23 + bias
+    constexpr uint32_t XB = XBF16 ? 2 : 4;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ Bars bars;
+    uint16_t *const stg = reinterpret_cast<uint16_t *>(smem);
+    float *const tab = reinterpret_cast<float *>(smem + g.off_tab);
+    float2 *const meta = reinterpret_cast<float2 *>(smem + g.off_meta);
+    uint8_t *const ring = smem + g.off_ring;
+    __shared__ float rcp_tab[128];          // RN32(1 / e4m3(code)) for the 128 magnitude codes
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t d = g.d, N = g.N;
+
+    if (threadIdx.x < 128) rcp_tab[threadIdx.x] = __frcp_rn(e4m3_decode_fast(threadIdx.x));
+    if (threadIdx.x == 0) {
+        for (uint32_t k = 0; k < g.nst; k++) {
+            mbar_init(&bars.full[k], 1 + 32);
+            mbar_init(&bars.empty[k], kCW);
+        }
+        mbar_init(&bars.tab, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    Sched sc;
+    sc.init(g);
+
+    if (warp == kCW) {
+        // ---------------- producer ----------------
+        uint32_t s = 0, k = 0, ph = 0;                  // stage, slot, slot phase
+        for (; sc.valid(); sc.next(g), s++, k = k + 1 == g.nst ? (ph ^= 1u, 0u) : k + 1) {
+            if (s >= g.nst) mbar_wait(&bars.empty[k], ph ^ 1u);
+            const uint32_t nr = min(g.R, sc.r1 - sc.i0);
+            uint8_t *st = ring + k * g.stage_bytes;
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&bars.full[k], nr * g.big_row);
+                bulk_g2s_cta(st, static_cast<const uint8_t *>(a.x) + (uint64_t(sc.p) * N + sc.i0) * g.big_row,
+                             nr * g.big_row, &bars.full[k]);
+            }
+            // assignments: S streams of nr bytes (nr % 4 == 0), 4 bytes per cp.async
+            const uint32_t nw = nr >> 2;
+#pragma unroll
+            for (int t = 0; t < S; t++)
+                for (uint32_t q = lane; q < nw; q += 32)
+                    cp_async4(st + g.off_small + t * g.R + 4 * q,
+                              a.asg + (uint64_t(sc.p) * S + t) * N + sc.i0 + 4 * q);
+            cp_async_arrive_noinc(&bars.full[k]);
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    const uint32_t lvpr = g.lchunk;                 // log2(threads per row)
+    const uint32_t c = threadIdx.x & ((1u << lvpr) - 1u);
+    const uint32_t col = c << 4;
+    const uint32_t coff = blk_off(c);
+    const uint32_t rslot = threadIdx.x >> lvpr, rpp = (kCW * 32) >> lvpr;
+    const int glanes = 1 << a.gshift;
+    bool nonfinite = false;
+    uint32_t cur = 0xFFFFFFFFu, jp = 0, k = 0, ph = 0;
+    if (S > 0 && threadIdx.x == 0 && sc.valid()) stage_table(a.cent, sc.p, g.tbytes, stg, &bars.tab);
+    for (; sc.valid(); sc.next(g), k = k + 1 == g.nst ? (ph ^= 1u, 0u) : k + 1) {
+        const uint32_t p = sc.p;
+        if (S > 0 && p != cur) {
+            named_sync_consumers();
+            mbar_wait(&bars.tab, jp & 1u);
+            widen(stg, tab, meta, g);
+            named_sync_consumers();
+            if (threadIdx.x == 0) {
+                const int64_t nx = sc.next_plane(g);
+                if (nx >= 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    stage_table(a.cent, uint32_t(nx), g.tbytes, stg, &bars.tab);
+                }
+            }
+            jp++;
+        }
+        cur = p;
+        mbar_wait(&bars.full[k], ph);
+        if (g.dbg == 1) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars.empty[k]);
+            continue;
+        }
+        const uint8_t *st = ring + k * g.stage_bytes;
+        const uint32_t nr = min(g.R, sc.r1 - sc.i0);
+        float2 r[kU][8];
+        uint32_t lr[kU];
+        int ai[kU][SS];
+        float xmin[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            const uint32_t l = u * rpp + rslot;
+            lr[u] = l < nr ? l : nr - 1;
+            const uint8_t *xr = st + lr[u] * g.big_row + col * XB;
+            xmin[u] = 0.f;
+            if constexpr (XBF16) {
+                const uint4 w0 = *reinterpret_cast<const uint4 *>(xr);
+                const uint4 w1 = *reinterpret_cast<const uint4 *>(xr + 16);
+                cvt16(w0, w1, reinterpret_cast<float *>(r[u]));
+                float mv[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) mv[q] = fminf(fabsf(r[u][q].x), fabsf(r[u][q].y));
+#pragma unroll
+                for (int span = 1; span < 8; span *= 2)
+#pragma unroll
+                    for (int q = 0; q < 8; q += 2 * span) mv[q] = fminf(mv[q], mv[q + span]);
+                xmin[u] = mv[0];
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const float4 v = *reinterpret_cast<const float4 *>(xr + 16 * j);
+                    r[u][2 * j] = make_float2(v.x, v.y);
+                    r[u][2 * j + 1] = make_float2(v.z, v.w);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < S; t++) ai[u][t] = st[g.off_small + t * g.R + lr[u]];
+        }
+        float eb[kU], am[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            // error bound input: sum_t max|r_t| <= S*max|r_S| + sum_t t*max|c_{t+1}|
+            // exactness certificate (bf16 x): every term of x - C_1 - ... - C_S is a
+            // multiple of `unit` and the sum of magnitudes < 2^24 unit => the f32
+            // chain is exact (== the reference's float64 residual), E = 0
+            float cb = 0.f, csum = 0.f, cunit = __int_as_float(0x7F800000);
+#pragma unroll
+            for (int t = 0; t < S; t++) {
+                const float *row = tab + uint32_t(t * int(g.K) + ai[u][t]) * g.pitch + coff;
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const float4 cv = *reinterpret_cast<const float4 *>(row + 4 * j);
+                    r[u][2 * j] = __fadd2_rn(r[u][2 * j], make_float2(-cv.x, -cv.y));
+                    r[u][2 * j + 1] = __fadd2_rn(r[u][2 * j + 1], make_float2(-cv.z, -cv.w));
+                }
+                const float2 m = meta[(uint32_t(t * int(g.K) + ai[u][t]) << lvpr) + c];
+                if (t > 0) cb = __fmaf_ru(float(t), m.y, cb);
+                csum = __fadd_ru(csum, m.y);
+                cunit = fminf(cunit, m.x);
+            }
+            float mv[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) mv[q] = max3_nan_abs(0.f, r[u][q].x, r[u][q].y);
+#pragma unroll
+            for (int span = 1; span < 8; span *= 2)
+#pragma unroll
+                for (int q = 0; q < 8; q += 2 * span) mv[q] = max_nan(mv[q], mv[q + span]);
+            const float mx = mv[0];
+            nonfinite |= !(mx <= 3.402823466e38f) || !(cb <= 3.402823466e38f);
+            am[u] = mx;
+            bool cert = false;
+            if constexpr (XBF16) {
+                const uint32_t eb8 = __float_as_uint(xmin[u]) & 0x7F800000u;
+                const float xunit = eb8 > (7u << 23) ? __uint_as_float(eb8 - (7u << 23)) : 0.f;
+                // |partials| <= max|x| + sum max|c| <= max|r_S| + 2 sum max|c|
+                const float bound = __fmaf_ru(2.f, csum, mx);
+                cert = bound < fminf(xunit, cunit) * 16777216.f;
+            }
+            eb[u] = (S > 0 && !cert) ? __fmaf_ru(float(S), mx, cb) : 0.f;
+        }
+        for (int m = 1; m < glanes; m <<= 1) {
+#pragma unroll
+            for (int u = 0; u < kU; u++) {
+                am[u] = fmaxf(am[u], __shfl_xor_sync(0xffffffffu, am[u], m));
+                eb[u] = fmaxf(eb[u], __shfl_xor_sync(0xffffffffu, eb[u], m));
+            }
+        }
+        // ---- scale codes for every row (branch-free), then the rare exact fix
+        bool valid[kU], camb[kU];
+        float E[kU];
+        uint32_t code[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            valid[u] = u * rpp + rslot < nr;
+            E[u] = __fmul_ru(eb[u], 2.38418579e-7f);      // 2^-22
+            const float lo = __fsub_rd(am[u], E[u]), hi = __fadd_ru(am[u], E[u]);
+            bool cb = false;
+            const uint32_t cc = scale_code<QMAX>(lo > 0.f ? lo : hi, hi, cb);
+            const bool zero = am[u] == 0.f && E[u] == 0.f;
+            code[u] = zero || !(lo > 0.f) ? 0x38u : cc;
+            camb[u] = valid[u] && !zero && (cb || !(lo > 0.f));
+        }
+        if (__any_sync(0xffffffffu, camb[0] || camb[kU - 1])) {      // exact scale (rare, out of line)
+#pragma unroll
+            for (int u = 0; u < kU; u++)
+                code[u] = fix_scale<QMAX, S, XBF16>(st + lr[u] * g.big_row + col * XB, tab, g.pitch, coff, int(g.K),
+                                                    ai[u][0], ai[u][SS > 1 ? 1 : 0], ai[u][SS > 2 ? 2 : 0],
+                                                    ai[u][SS > 3 ? 3 : 0], am[u], E[u], camb[u], glanes, code[u]);
+        }
+        // ---- codes: bits of fma(r, 1/s, MAGIC) = 0x4B400000 + q + 2^(b-1), packed by
+        // a multiply-add tree; the ambiguity window reduced over the row
+        Words4 b32[kU];
+        float sv[kU], inv[kU], thr[kU];
+        bool amb[kU], allv[kU];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            sv[u] = e4m3_decode_fast(code[u]);
+            inv[u] = rcp_tab[code[u] & 0x7Fu];
+            const float2 inv2 = make_float2(inv[u], inv[u]);
+            uint32_t f[16];
+            float2 yv[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                yv[q] = __ffma2_rn(r[u][q], inv2, make_float2(MAGIC, MAGIC));
+                f[2 * q] = __float_as_uint(yv[q].x);
+                f[2 * q + 1] = __float_as_uint(yv[q].y);
+            }
+#pragma unroll
+            for (int w = 0; w < BITS / 2; w++) {
+                uint32_t v[FPW];
+#pragma unroll
+                for (int k2 = 0; k2 < FPW; k2++) v[k2] = f[w * FPW + k2];
+#pragma unroll
+                for (int span = 1; span < FPW; span *= 2)
+#pragma unroll
+                    for (int k2 = 0; k2 < FPW; k2 += 2 * span) v[k2] += v[k2 + span] << (BITS * span);
+                b32[u].w[w] = (v[0] - magic_sum<BITS>()) ^ SIGNS;
+            }
+            allv[u] = !(E[u] < 0.125f * sv[u]) || code[u] == 0x7Eu;
+            thr[u] = window_thr<QMAX>(sv[u], inv[u], E[u]);
+            float wv[8];
+            if constexpr (QMAX == 1) {
+                const float h = 0.5f * sv[u];
+                const float2 pa = make_float2(-h * h, -h * h);
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const float2 gg = __ffma2_rn(r[u][q], r[u][q], pa);
+                    wv[q] = fminf(fabsf(gg.x), fabsf(gg.y));
+                }
+#pragma unroll
+                for (int span = 1; span < 8; span *= 2)
+#pragma unroll
+                    for (int q = 0; q < 8; q += 2 * span) wv[q] = fminf(wv[q], wv[q + span]);
+                amb[u] = allv[u] || wv[0] <= thr[u];
+            } else {
+                const float2 pa = make_float2(-MAGIC, -MAGIC);
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    const float2 qf = __fadd2_rn(yv[q], pa);
+                    const float2 dist = __ffma2_rn(r[u][q], inv2, make_float2(-qf.x, -qf.y));
+                    wv[q] = fmaxf(fabsf(dist.x), fabsf(dist.y));
+                }
+#pragma unroll
+                for (int span = 1; span < 8; span *= 2)
+#pragma unroll
+                    for (int q = 0; q < 8; q += 2 * span) wv[q] = fmaxf(wv[q], wv[q + span]);
+                amb[u] = allv[u] || wv[0] >= thr[u];
+            }
+            amb[u] &= valid[u];
+        }
+        if (amb[0] || amb[kU - 1]) {      // exact codes (rare, out of line)
+#pragma unroll
+            for (int u = 0; u < kU; u++)
+                if (amb[u])
+                    b32[u] = fix_codes<BITS, S, XBF16>(st + lr[u] * g.big_row + col * XB, tab, g.pitch, coff,
+                                                       int(g.K), ai[u][0], ai[u][SS > 1 ? 1 : 0],
+                                                       ai[u][SS > 2 ? 2 : 0], ai[u][SS > 3 ? 3 : 0], sv[u], inv[u],
+                                                       E[u], thr[u], allv[u], b32[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            if (!valid[u]) continue;
+            const uint32_t e0 = (sc.i0 + lr[u]) * d + col;
+            uint8_t *plp = a.payload + uint64_t(p) * a.pb + ((e0 * BITS) >> 3);
+            if constexpr (BITS == 2) *reinterpret_cast<uint32_t *>(plp) = b32[u].w[0];
+            else if constexpr (BITS == 4) *reinterpret_cast<uint2 *>(plp) = make_uint2(b32[u].w[0], b32[u].w[1]);
+            else *reinterpret_cast<uint4 *>(plp) = make_uint4(b32[u].w[0], b32[u].w[1], b32[u].w[2], b32[u].w[3]);
+            if ((lane & (glanes - 1)) == 0) a.scales[uint64_t(p) * a.ng + (e0 >> a.lgB)] = uint8_t(code[u]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.empty[k]);
+    }
+    const uint32_t all = __reduce_or_sync(0xffffffffu, nonfinite ? uint32_t(QVG_STATUS_NONFINITE) : 0u);
+    if (all && lane == 0) atomicOr(a.status, int(all));
+}
+
+// ============================================================================
+// K6 dequantize
+// ============================================================================
+template <int BITS, int S, bool OBF16>
+__global__ void __launch_bounds__(kThreads, 1) k_dequant_stream(DequantArgs a, Geo g) {
+    constexpr int SS = S > 0 ? S : 1;
+    constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
+    constexpr int POS = 23 - BITS;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ Bars bars;
+    uint16_t *const stg = reinterpret_cast<uint16_t *>(smem);
+    float *const tab = reinterpret_cast<float *>(smem + g.off_tab);
+    float2 *const meta = reinterpret_cast<float2 *>(smem + g.off_meta);
+    uint8_t *const ring = smem + g.off_ring;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t d = g.d, N = g.N;
+
+    if (threadIdx.x == 0) {
+        for (uint32_t k = 0; k < g.nst; k++) {
+            mbar_init(&bars.full[k], 1 + 32);
+            mbar_init(&bars.empty[k], kCW);
+        }
+        mbar_init(&bars.tab, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    Sched sc;
+    sc.init(g);
+
+    if (warp == kCW) {
+        // ---------------- producer ----------------
+        uint32_t s = 0, k = 0, ph = 0;                  // stage, slot, slot phase
+        for (; sc.valid(); sc.next(g), s++, k = k + 1 == g.nst ? (ph ^= 1u, 0u) : k + 1) {
+            if (s >= g.nst) mbar_wait(&bars.empty[k], ph ^ 1u);
+            const uint32_t nr = min(g.R, sc.r1 - sc.i0);
+            uint8_t *st = ring + k * g.stage_bytes;
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&bars.full[k], nr * g.big_row);
+                bulk_g2s_cta(st, a.payload + uint64_t(sc.p) * a.pb + uint64_t(sc.i0) * g.big_row,
+                             nr * g.big_row, &bars.full[k]);
+            }
+            // scales: nr * small_row bytes; assignments: S streams of nr bytes
+            const uint32_t nws = (nr * g.small_row) >> 2;
+            for (uint32_t q = lane; q < nws; q += 32)
+                cp_async4(st + g.off_small + 4 * q,
+                          a.scales + (uint64_t(sc.p) * N + sc.i0) * g.small_row + 4 * q);
+            const uint32_t nw = nr >> 2;
+            uint8_t *sa = st + g.off_small + g.R * g.small_row;
+#pragma unroll
+            for (int t = 0; t < S; t++)
+                for (uint32_t q = lane; q < nw; q += 32)
+                    cp_async4(sa + t * g.R + 4 * q, a.asg + (uint64_t(sc.p) * S + t) * N + sc.i0 + 4 * q);
+            cp_async_arrive_noinc(&bars.full[k]);
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    const uint32_t lvpr = g.lchunk;
+    const uint32_t c = threadIdx.x & ((1u << lvpr) - 1u);
+    const uint32_t col = c << 4;
+    const uint32_t coff = blk_off(c);
+    const uint32_t rslot = threadIdx.x >> lvpr, rpp = (kCW * 32) >> lvpr;
+    const uint32_t mhi = ((1u << BITS) - 1u) << POS, one = 0x3F800000u;
+    bool bad_scale = false, bad_asg = false;
+    uint32_t cur = 0xFFFFFFFFu, jp = 0, k = 0, ph = 0;
+    if (S > 0 && threadIdx.x == 0 && sc.valid()) stage_table(a.cent, sc.p, g.tbytes, stg, &bars.tab);
+    for (; sc.valid(); sc.next(g), k = k + 1 == g.nst ? (ph ^= 1u, 0u) : k + 1) {
+        const uint32_t p = sc.p;
+        if (S > 0 && p != cur) {
+            named_sync_consumers();
+            mbar_wait(&bars.tab, jp & 1u);
+            widen(stg, tab, meta, g);
+            named_sync_consumers();
+            if (threadIdx.x == 0) {
+                const int64_t nx = sc.next_plane(g);
+                if (nx >= 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    stage_table(a.cent, uint32_t(nx), g.tbytes, stg, &bars.tab);
+                }
+            }
+            jp++;
+        }
+        cur = p;
+        mbar_wait(&bars.full[k], ph);
+        const uint8_t *st = ring + k * g.stage_bytes;
+        const uint8_t *sa = st + g.off_small + g.R * g.small_row;
+        const uint32_t nr = min(g.R, sc.r1 - sc.i0);
+        Codes16<BITS> w[kU];
+        uint32_t scb[kU], lr[kU];
+        int ai[kU][SS];
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            const uint32_t l = u * rpp + rslot;
+            lr[u] = l < nr ? l : nr - 1;
+            const uint8_t *cr = st + lr[u] * g.big_row + ((col * BITS) >> 3);
+            if constexpr (BITS == 2) w[u].w[0] = *reinterpret_cast<const uint32_t *>(cr);
+            else if constexpr (BITS == 4) {
+                const uint2 v = *reinterpret_cast<const uint2 *>(cr);
+                w[u].w[0] = v.x; w[u].w[1] = v.y;
+            } else {
+                const uint4 v = *reinterpret_cast<const uint4 *>(cr);
+                w[u].w[0] = v.x; w[u].w[1] = v.y; w[u].w[2] = v.z; w[u].w[3] = v.w;
+            }
+            scb[u] = st[g.off_small + lr[u] * g.small_row + (col >> a.lgB)];
+#pragma unroll
+            for (int t = 0; t < S; t++) {
+                const int at = sa[t * g.R + lr[u]];
+                bad_asg |= at >= int(g.K);
+                ai[u][t] = at < int(g.K) ? at : 0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; u++) {
+            const bool valid = u * rpp + rslot < nr;
+            bad_scale |= (scb[u] & 0x7Fu) == 0x7Fu;
+            const float sv = e4m3_decode_fast(scb[u]);
+            Codes16<BITS> wx;
+#pragma unroll
+            for (int q = 0; q < Codes16<BITS>::NW; q++) wx.w[q] = w[u].w[q] ^ SIGNS;
+            const float2 s_hi = make_float2(sv * float(1 << BITS), sv * float(1 << BITS));
+            const float2 s_off = make_float2(sv * (-1.5f * float(1 << BITS)), sv * (-1.5f * float(1 << BITS)));
+            float2 y[8];
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                const int b0 = 2 * q * BITS, b1 = (2 * q + 1) * BITS;
+                const uint32_t v0 = (b0 & 31) <= POS ? (wx.w[b0 >> 5] << (POS - (b0 & 31))) : (wx.w[b0 >> 5] >> ((b0 & 31) - POS));
+                const uint32_t v1 = (b1 & 31) <= POS ? (wx.w[b1 >> 5] << (POS - (b1 & 31))) : (wx.w[b1 >> 5] >> ((b1 & 31) - POS));
+                const float2 f = make_float2(__uint_as_float(lop3_and_or(v0, mhi, one)),
+                                             __uint_as_float(lop3_and_or(v1, mhi, one)));
+                y[q] = __ffma2_rn(f, s_hi, s_off);          // q*s, exact
+            }
+            // every non-final partial sum exact in f32 <= all terms multiples of
+            // `unit` and sum of magnitudes < 2^24 unit
+            // (a row whose codes are all zero has q*s == 0: only the centroid terms count)
+            bool cert = true;
+            if constexpr (S >= 2) {
+                uint32_t anyq = 0;
+#pragma unroll
+                for (int q = 0; q < Codes16<BITS>::NW; q++) anyq |= w[u].w[q];
+                float unit = anyq ? fmaxf(__uint_as_float((__float_as_uint(sv) & 0x7F800000u) - (3u << 23)), 0.001953125f)
+                                  : __int_as_float(0x7F800000);
+                float bound = anyq ? sv * float(1 << (BITS - 1)) : 0.f;
+#pragma unroll
+                for (int t = 1; t < S; t++) {
+                    const float2 m = meta[(uint32_t(t * int(g.K) + ai[u][t]) << lvpr) + c];
+                    unit = fminf(unit, m.x);
+                    bound = __fadd_ru(bound, m.y);
+                }
+                cert = S == 2 && !anyq ? true : bound < unit * 16777216.f;
+            }
+#pragma unroll
+            for (int t = S - 1; t >= 0; t--) {                 // reversed(stages)
+                const float *row = tab + uint32_t(t * int(g.K) + ai[u][t]) * g.pitch + coff;
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const float4 cv = *reinterpret_cast<const float4 *>(row + 4 * j);
+                    y[2 * j] = __fadd2_rn(y[2 * j], make_float2(cv.x, cv.y));
+                    y[2 * j + 1] = __fadd2_rn(y[2 * j + 1], make_float2(cv.z, cv.w));
+                }
+            }
+            if constexpr (S >= 2) {
+                if (!cert) {
+                    // per element: each non-final partial sum P' = P + c is exact iff
+                    // (P' - P) - c == 0 and (P' - c) - P == 0 (Fast2Sum from the larger
+                    // operand gives the non-zero rounding error otherwise)
+                    uint32_t bad = 0;
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        const int b0 = 2 * q * BITS, b1 = (2 * q + 1) * BITS;
+                        const uint32_t v0 = (b0 & 31) <= POS ? (wx.w[b0 >> 5] << (POS - (b0 & 31))) : (wx.w[b0 >> 5] >> ((b0 & 31) - POS));
+                        const uint32_t v1 = (b1 & 31) <= POS ? (wx.w[b1 >> 5] << (POS - (b1 & 31))) : (wx.w[b1 >> 5] >> ((b1 & 31) - POS));
+                        float2 P = __ffma2_rn(make_float2(__uint_as_float(lop3_and_or(v0, mhi, one)),
+                                                          __uint_as_float(lop3_and_or(v1, mhi, one))), s_hi, s_off);
+                        bool e0 = false, e1 = false;
+#pragma unroll
+                        for (int t = S - 1; t >= 1; t--) {
+                            const float2 cc = *reinterpret_cast<const float2 *>(
+                                tab + uint32_t(t * int(g.K) + ai[u][t]) * g.pitch + coff + 2 * q);
+                            const float2 P2 = __fadd2_rn(P, cc);
+                            const float2 d1 = __fadd2_rn(__fadd2_rn(P2, make_float2(-P.x, -P.y)), make_float2(-cc.x, -cc.y));
+                            const float2 d2 = __fadd2_rn(__fadd2_rn(P2, make_float2(-cc.x, -cc.y)), make_float2(-P.x, -P.y));
+                            e0 |= d1.x != 0.f || d2.x != 0.f;
+                            e1 |= d1.y != 0.f || d2.y != 0.f;
+                            P = P2;
+                        }
+                        bad |= (e0 ? 1u << (2 * q) : 0u) | (e1 ? 2u << (2 * q) : 0u);
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < 16; kk++) {   // rare: the element in the reference's float64 chain
+                        if (!((bad >> kk) & 1u)) continue;
+                        const int b = kk * BITS, wi = b >> 5, o = b & 31;
+                        const uint32_t v = o <= POS ? (wx.w[wi] << (POS - o)) : (wx.w[wi] >> (o - POS));
+                        const float qs = __fmaf_rn(__uint_as_float(lop3_and_or(v, mhi, one)), s_hi.x, s_off.x);
+                        const float rr = exact_addback<S>(qs, tab, g.pitch, coff + kk, int(g.K), ai[u][0],
+                                                          ai[u][SS > 1 ? 1 : 0], ai[u][SS > 2 ? 2 : 0],
+                                                          ai[u][SS > 3 ? 3 : 0]);
+                        if (kk & 1) y[kk >> 1].y = rr; else y[kk >> 1].x = rr;
+                    }
+                }
+            }
+            if (!valid) continue;
+            const uint64_t o = (uint64_t(p) * N + sc.i0 + lr[u]) * d + col;
+            if constexpr (OBF16) {
+                uint32_t v[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) {
+                    __nv_bfloat162 h = __floats2bfloat162_rn(y[q].x, y[q].y);
+                    v[q] = *reinterpret_cast<uint32_t *>(&h);
+                }
+                uint4 *op = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(a.out) + o);
+                op[0] = make_uint4(v[0], v[1], v[2], v[3]);
+                op[1] = make_uint4(v[4], v[5], v[6], v[7]);
+            } else {
+                float4 *op = reinterpret_cast<float4 *>(static_cast<float *>(a.out) + o);
+#pragma unroll
+                for (int q = 0; q < 4; q++) op[q] = make_float4(y[2 * q].x, y[2 * q].y, y[2 * q + 1].x, y[2 * q + 1].y);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.empty[k]);
+    }
+    const uint32_t stat = (bad_scale ? QVG_STATUS_NAN_SCALE : 0u) | (bad_asg ? QVG_STATUS_BAD_ASSIGN : 0u);
+    const uint32_t all = __reduce_or_sync(0xffffffffu, stat);
+    if (all && lane == 0) atomicOr(a.status, int(all));
+}
+
+// ============================================================================
+// host: geometry and dispatch
+// ============================================================================
+static int ilog2i(int v) { int l = 0; while ((1 << l) < v) l++; return l; }
+
+// smem: [bf16 staging][f32 padded tables][metadata][ring]; false when the
+// configuration does not fit this kernel (callers fall back to v4/v5/v6)
+static bool plan(bool quant, int64_t P, int64_t N, int d, int S, int K, int bits, int B, int xbytes,
+                 uintptr_t align_probe, Geo &g, size_t &smem, int &grid) {
+    if (S < 1 || S > 4 || d % 16 != 0 || d > 512 || N < 4 || N % 4 != 0) return false;
+    const int n = d / 16;
+    if (n & (n - 1)) return false;
+    if ((align_probe & 3u) != 0) return false;
+    if (P * N >= (int64_t(1) << 31) || N * d >= (int64_t(1) << 31)) return false;
+    const uint32_t R = uint32_t(kCW * 32 / n * kU);
+    const uint32_t pitch = uint32_t(16 * n + 4 * ((n + 1) / 2));
+    const size_t tbytes = size_t(S) * K * d * 2;
+    const size_t tabb = size_t(S) * K * pitch * 4;
+    const size_t nchunk = size_t(S) * K * n;
+    size_t off_tab = (tbytes + 127) & ~size_t(127);
+    size_t off_meta = off_tab + ((tabb + 127) & ~size_t(127));
+    size_t off_ring = off_meta + ((nchunk * 8 + 1023) & ~size_t(1023));
+    uint32_t big_row, small_row;
+    if (quant) {
+        big_row = uint32_t(d * xbytes);
+        small_row = 0;
+    } else {
+        if ((size_t(d) * bits) % 128 != 0) return false;       // 16-byte code rows
+        big_row = uint32_t(d * bits / 8);
+        small_row = uint32_t(d / B);
+        if ((N * small_row) % 4 != 0) return false;
+    }
+    const size_t big = size_t(R) * big_row;
+    const size_t small = size_t(R) * small_row + size_t(S) * R;
+    const size_t stage = (big + ((small + 15) & ~size_t(15)) + 127) & ~size_t(127);
+    const size_t budget = 227 * 1024 - 1024;
+    if (off_ring + 2 * stage > budget) return false;
+    uint32_t nst = uint32_t((budget - off_ring) / stage);
+    if (nst > 8) nst = 8;
+    // work items: planes split into row ranges (multiples of R) until every
+    // CTA has several
+    const int64_t ctas = 148;
+    int64_t ipp = 1;
+    while (P * ipp < 6 * ctas && (N + ipp * 2 - 1) / (ipp * 2) >= int64_t(4 * R)) ipp *= 2;
+    int64_t rpi = (N + ipp - 1) / ipp;
+    rpi = (rpi + R - 1) / R * R;
+    ipp = (N + rpi - 1) / rpi;
+    g = Geo{uint32_t(P), uint32_t(N), uint32_t(d), uint32_t(K), R, nst, pitch, uint32_t(tbytes),
+            uint32_t(nchunk), uint32_t(ilog2i(n)), uint32_t(ipp), uint32_t(rpi), uint32_t(P * ipp),
+            uint32_t(off_tab), uint32_t(off_meta), uint32_t(off_ring), uint32_t(stage), big_row, small_row,
+            uint32_t(big), 0u};
+    if (const char *e = getenv("QVG_STREAM_DBG")) g.dbg = uint32_t(atoi(e));
+    if (const char *e = getenv("QVG_STREAM_NST")) { const uint32_t v = uint32_t(atoi(e)); if (v >= 2 && v < nst) nst = v; g.nst = nst; }
+    smem = off_ring + nst * stage;
+    grid = int(P * ipp < ctas ? P * ipp : ctas);
+    return true;
+}
+
+template <int BITS, int S>
+static int launch_q(const QuantArgs &a, bool xbf16, const Geo &g, size_t smem, int grid, cudaStream_t st) {
+    if (xbf16) {
+        cudaFuncSetAttribute(k_quantize_stream<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_quantize_stream<BITS, S, true><<<grid, kThreads, smem, st>>>(a, g);
+    } else {
+        cudaFuncSetAttribute(k_quantize_stream<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_quantize_stream<BITS, S, false><<<grid, kThreads, smem, st>>>(a, g);
+    }
+    return 1;
+}
+
+template <int BITS, int S>
+static int launch_d(const DequantArgs &a, bool obf16, const Geo &g, size_t smem, int grid, cudaStream_t st) {
+    if (obf16) {
+        cudaFuncSetAttribute(k_dequant_stream<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_dequant_stream<BITS, S, true><<<grid, kThreads, smem, st>>>(a, g);
+    } else {
+        cudaFuncSetAttribute(k_dequant_stream<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_dequant_stream<BITS, S, false><<<grid, kThreads, smem, st>>>(a, g);
+    }
+    return 1;
+}
+
+}  // namespace stream
+
+// returns 1 when the streaming kernel was launched, 0 when the caller must
+// use another kernel for this configuration
+int launch_quantize_stream(const QuantArgs &a, int64_t P, int bits, int S, bool xbf16, cudaStream_t st) {
+    using namespace stream;
+    Geo g;
+    size_t smem;
+    int grid;
+    const uintptr_t probe = reinterpret_cast<uintptr_t>(a.asg) | reinterpret_cast<uintptr_t>(a.x);
+    if (!plan(true, P, a.N, a.d, S, a.K, bits, a.B, xbf16 ? 2 : 4, probe, g, smem, grid)) return 0;
+    if ((reinterpret_cast<uintptr_t>(a.x) & 15u) != 0) return 0;
+#define QV_Q(BB)                                                      \
+    switch (S) {                                                      \
+        case 1: return launch_q<BB, 1>(a, xbf16, g, smem, grid, st); \
+        case 2: return launch_q<BB, 2>(a, xbf16, g, smem, grid, st); \
+        case 3: return launch_q<BB, 3>(a, xbf16, g, smem, grid, st); \
+        default: return launch_q<BB, 4>(a, xbf16, g, smem, grid, st); \
+    }
+    if (bits == 2) { QV_Q(2) }
+    if (bits == 4) { QV_Q(4) }
+    QV_Q(8)
+#undef QV_Q
+}
+
+int launch_dequantize_stream(const DequantArgs &a, int64_t P, int bits, int S, bool obf16, cudaStream_t st) {
+    using namespace stream;
+    Geo g;
+    size_t smem;
+    int grid;
+    const uintptr_t probe = reinterpret_cast<uintptr_t>(a.asg) | reinterpret_cast<uintptr_t>(a.scales);
+    if (!plan(false, P, a.N, a.d, S, a.K, bits, a.B, 0, probe, g, smem, grid)) return 0;
+    if ((reinterpret_cast<uintptr_t>(a.payload) & 15u) != 0 || (a.pb % 16) != 0) return 0;
+#define QV_D(BB)                                                      \
+    switch (S) {                                                      \
+        case 1: return launch_d<BB, 1>(a, obf16, g, smem, grid, st); \
+        case 2: return launch_d<BB, 2>(a, obf16, g, smem, grid, st); \
+        case 3: return launch_d<BB, 3>(a, obf16, g, smem, grid, st); \
+        default: return launch_d<BB, 4>(a, obf16, g, smem, grid, st); \
+    }
+    if (bits == 2) { QV_D(2) }
+    if (bits == 4) { QV_D(4) }
+    QV_D(8)
+#undef QV_D
+}
+
+}  // namespace qvg

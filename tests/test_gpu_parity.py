@@ -177,3 +177,84 @@ def test_many_planes_tma_path_vs_oracle(oracle_lib, bits, B, S, K):
     assert np.array_equal(_u32(out), _u32(ref))
     outb = D.dequantize(dc, torch.bfloat16).cpu()
     assert torch.equal(outb.view(torch.int16), torch.from_numpy(ref).to(torch.bfloat16).view(torch.int16))
+
+
+def test_quantize_boundary_cases_with_stages(oracle_lib):
+    """The same boundary residuals reached through a centroid subtraction
+    (S >= 1 selects the f32-table kernels): exact ties at s/2 and at the
+    half-integers of the 4/8-bit grids, zero / tiny / saturating groups."""
+    rng = np.random.default_rng(11)
+    P, N, d, B = 2, 300, 128, 64
+    x = rng.normal(size=(P, N, d)).astype(np.float32)
+    s = np.float32(0.15625)
+    x[0, 0, :B] = 0.0
+    x[0, 1, :B] = 0.0
+    x[0, 1, 0] = 1e-7
+    x[0, 2, :B] = 3000.0
+    x[0, 3, :B] = s / 2
+    x[0, 3, 0] = s
+    x[0, 4, :B] = np.nextafter(s / 2, np.float32(1))
+    x[0, 4, 0] = s
+    x[1, 5, :B] = np.float32(7.0) * np.arange(B, dtype=np.float32) / 8   # many grid half-points
+    x[1, 5, 0] = 7.0
+    xb = torch.from_numpy(x).to(torch.bfloat16)
+    for S in (1, 2):
+        cent = np.zeros((P, S, 3, d), np.float32)
+        cent[:, :, 1, :] = 0.5
+        cent[:, :, 2, ::3] = -0.25
+        asg = rng.integers(0, 3, size=(P, S, N)).astype(np.uint8)
+        asg[:, :, :6] = 0                               # boundary rows keep their exact values
+        ct = torch.from_numpy(cent).to(torch.bfloat16)
+        for bits in (2, 4, 8):
+            cfg = QuantConfig(bits=bits, group_size=B, stages=S, centroids=3)
+            for xt in (torch.from_numpy(x), xb):
+                pay, sc = D.quantize(xt.cuda(), cfg, ct.cuda(), torch.from_numpy(asg).cuda())
+                rp, rs = oracle_lib.quantize_given_metas_batch(xt.float().numpy(), ct.float().numpy(), asg,
+                                                               bits, B, 4)
+                assert np.array_equal(sc.cpu().numpy(), rs), (S, bits, xt.dtype)
+                assert np.array_equal(pay.cpu().numpy(), rp), (S, bits, xt.dtype)
+
+
+@pytest.mark.parametrize("bits,S", [(2, 2), (2, 3), (4, 2), (8, 4)])
+def test_dequant_exactness_certificate_stress(oracle_lib, bits, S):
+    """Centroid tables mixing magnitudes 1e-30 .. 1e4 (and zeros) make the
+    non-final f32 partial sums inexact for many rows: those rows must take
+    the float64 chain and still match the oracle bit for bit."""
+    rng = np.random.default_rng(bits * 7 + S)
+    P, N, d, K, B = 4, 400, 128, 8, 64
+    mags = np.array([0.0, 1e-30, 1e-8, 3e-3, 0.7, 1.0, 55.0, 1e4], np.float32)
+    cent = (rng.choice(mags, size=(P, S, K, d)) * rng.choice([-1, 1], size=(P, S, K, d))).astype(np.float32)
+    ct = torch.from_numpy(cent).to(torch.bfloat16)
+    asg = rng.integers(0, K, size=(P, S, N)).astype(np.uint8)
+    x = _rand_planes(rng, P, N, d, 30.0)
+    cfg = QuantConfig(bits=bits, group_size=B, stages=S, centroids=K)
+    pay, sc = D.quantize(x.cuda(), cfg, ct.cuda(), torch.from_numpy(asg).cuda())
+    rp, rs = oracle_lib.quantize_given_metas_batch(x.float().numpy(), ct.float().numpy(), asg, bits, B, 4)
+    assert np.array_equal(sc.cpu().numpy(), rs)
+    assert np.array_equal(pay.cpu().numpy(), rp)
+    dc = D.DeviceChunks(cfg, N, d, pay, sc, ct.cuda(), torch.from_numpy(asg).cuda())
+    ref = oracle_lib.prq_decompress_batch(rp, rs, ct.float().numpy(), asg, N, d, bits, B, 4)
+    out = D.dequantize(dc, torch.float32).cpu().numpy()
+    assert np.array_equal(_u32(out), _u32(ref))
+    outb = D.dequantize(dc, torch.bfloat16).cpu()
+    assert torch.equal(outb.view(torch.int16), torch.from_numpy(ref).to(torch.bfloat16).view(torch.int16))
+
+
+@pytest.mark.parametrize("P,N", [(1, 9001), (3, 6000), (2, 40000)])
+def test_planes_split_into_row_ranges(oracle_lib, P, N):
+    """Few long planes: the kernels split each plane into row ranges (work
+    items) spread over the CTAs; results equal the oracle."""
+    rng = np.random.default_rng(P * N)
+    d, K, S, B, bits = 128, 64, 2, 64, 2
+    x = _rand_planes(rng, P, N, d, 20.0)
+    cent = torch.from_numpy(rng.normal(0, 2.0, size=(P, S, K, d)).astype(np.float32)).to(torch.bfloat16)
+    asg = rng.integers(0, K, size=(P, S, N)).astype(np.uint8)
+    cfg = QuantConfig(bits=bits, group_size=B, stages=S, centroids=K)
+    pay, sc = D.quantize(x.cuda(), cfg, cent.cuda(), torch.from_numpy(asg).cuda())
+    rp, rs = oracle_lib.quantize_given_metas_batch(x.float().numpy(), cent.float().numpy(), asg, bits, B, 8)
+    assert np.array_equal(sc.cpu().numpy(), rs)
+    assert np.array_equal(pay.cpu().numpy(), rp)
+    dc = D.DeviceChunks(cfg, N, d, pay, sc, cent.cuda(), torch.from_numpy(asg).cuda())
+    ref = oracle_lib.prq_decompress_batch(rp, rs, cent.float().numpy(), asg, N, d, bits, B, 8)
+    outb = D.dequantize(dc, torch.bfloat16).cpu()
+    assert torch.equal(outb.view(torch.int16), torch.from_numpy(ref).to(torch.bfloat16).view(torch.int16))
