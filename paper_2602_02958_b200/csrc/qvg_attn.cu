@@ -22,6 +22,9 @@
 //   * tcgen05.mma: O += P V, then the next block.
 // Epilogue: O / l -> bf16.
 #include <cstdio>
+#include <type_traits>
+#include <cstdlib>
+#include <cstring>
 #include <cuda.h>
 
 #include "qvg_common.cuh"
@@ -950,6 +953,305 @@ static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const 
 }
 }  // namespace attn3
 
+// ============================================================================
+// v4: the v3 ping-pong with (1) the MMA order PV_A(j) S_A(j+1) PV_B(j)
+// S_B(j+1), so that each softmax phase overlaps two MMAs of the other tile,
+// (2) the S row loaded from TMEM once (128 registers, one wait::ld), (3) packed
+// f32x2 arithmetic for scale/shift and row sums, and (4) 3/8 of the exp2 on
+// the FMA pipe (degree-3 polynomial on the rounded-off fraction, exponent
+// added in the integer domain) to relieve the 16/clk/SM MUFU.
+// ============================================================================
+namespace attn4 {
+using attn::kTile;
+using attn::kD;
+using attn2::kBox;
+using attn2::kOpTile;
+using attn3::Bars;
+constexpr uint32_t kSmem = attn3::kSmem;
+
+__device__ __forceinline__ void tmem_ld128(uint32_t taddr, float v[128]) {
+    uint32_t *r = reinterpret_cast<uint32_t *>(v);
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[32 * c + 0]), "=r"(r[32 * c + 1]), "=r"(r[32 * c + 2]), "=r"(r[32 * c + 3]),
+              "=r"(r[32 * c + 4]), "=r"(r[32 * c + 5]), "=r"(r[32 * c + 6]), "=r"(r[32 * c + 7]),
+              "=r"(r[32 * c + 8]), "=r"(r[32 * c + 9]), "=r"(r[32 * c + 10]), "=r"(r[32 * c + 11]),
+              "=r"(r[32 * c + 12]), "=r"(r[32 * c + 13]), "=r"(r[32 * c + 14]), "=r"(r[32 * c + 15]),
+              "=r"(r[32 * c + 16]), "=r"(r[32 * c + 17]), "=r"(r[32 * c + 18]), "=r"(r[32 * c + 19]),
+              "=r"(r[32 * c + 20]), "=r"(r[32 * c + 21]), "=r"(r[32 * c + 22]), "=r"(r[32 * c + 23]),
+              "=r"(r[32 * c + 24]), "=r"(r[32 * c + 25]), "=r"(r[32 * c + 26]), "=r"(r[32 * c + 27]),
+              "=r"(r[32 * c + 28]), "=r"(r[32 * c + 29]), "=r"(r[32 * c + 30]), "=r"(r[32 * c + 31])
+            : "r"(taddr + 32 * c));
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ float ex2_mufu(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// 2^x for a pair, x >= -126: x = j + f, j = rint(x) (magic-number add),
+// 2^f by a degree-3 polynomial on [-1/2, 1/2] (max rel. error 7.5e-5, far
+// below the bf16 rounding of P), 2^j added to the exponent field
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+    const float2 M = make_float2(12582912.f, 12582912.f);
+    const float2 xm = __fadd2_rn(x, M);
+    const float2 jf = __fadd2_rn(xm, make_float2(-12582912.f, -12582912.f));
+    const float2 f = __fadd2_rn(x, make_float2(-jf.x, -jf.y));
+    float2 p = __ffma2_rn(make_float2(0.05517162f, 0.05517162f), f, make_float2(0.24261117f, 0.24261117f));
+    p = __ffma2_rn(p, f, make_float2(0.693261f, 0.693261f));
+    p = __ffma2_rn(p, f, make_float2(0.99992806f, 0.99992806f));
+    uint32_t r0, r1;   // bits(p) + (bits(xm) << 23) on the FMA pipe (IMAD)
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r0) : "r"(__float_as_uint(xm.x)), "r"(1u << 23), "r"(__float_as_uint(p.x)));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r1) : "r"(__float_as_uint(xm.y)), "r"(1u << 23), "r"(__float_as_uint(p.y)));
+    return make_float2(__uint_as_float(r0), __uint_as_float(r1));
+}
+
+// columns [POLY_FROM, 128) of each S row use the polynomial exp2
+template <int POLY_FROM>
+__global__ void __launch_bounds__(320, 1)
+k_attention_pp4(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
+                const __grid_constant__ CUtensorMap tmKc, const __grid_constant__ CUtensorMap tmVc, attn2::Args a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sQ = smem;
+    uint8_t *sKV = smem + 2 * kOpTile;
+    __shared__ Bars bars;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int h = blockIdx.y;
+    const int64_t q0 = int64_t(blockIdx.x) * 2 * kTile;
+    const int64_t cb = (a.n_cache + kTile - 1) / kTile;
+    const int64_t nb = cb + (a.n_cur + kTile - 1) / kTile;
+
+    if (tid == 0) {
+        attn::bar_init(&bars.q_full, 1);
+        for (int i = 0; i < 2; i++) {
+            attn::bar_init(&bars.kv_full[i], 1);
+            attn::bar_init(&bars.kv_empty[i], 1);
+            attn::bar_init(&bars.s_full[i], 1);
+            attn::bar_init(&bars.p_full[i], 128);
+        }
+        attn::bar_init(&bars.o_final, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 9) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(attn::su32(&bars.tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    attn::fence_before();
+    __syncthreads();
+    attn::fence_after();
+    const uint32_t tmem = bars.tmem;
+
+    if (warp == 8) {
+        if (lane == 0) {                              // ---- TMA producer (as v3)
+            attn2::expect_tx(&bars.q_full, 2 * kOpTile);
+            for (int t = 0; t < 2; t++) {
+                attn2::tma_load_2d(sQ + t * kOpTile, &tmQ, h * kD, int(q0 + t * kTile), &bars.q_full);
+                attn2::tma_load_2d(sQ + t * kOpTile + kBox, &tmQ, h * kD + 64, int(q0 + t * kTile), &bars.q_full);
+            }
+            for (int64_t j = 0; j < nb; j++) {
+                const int st = int(j & 1);
+                if (j >= 2) attn::bar_wait(&bars.kv_empty[st], uint32_t(((j - 2) >> 1) & 1));
+                uint8_t *sK = sKV + st * 2 * kOpTile, *sV = sK + kOpTile;
+                attn2::expect_tx(&bars.kv_full[st], 2 * kOpTile);
+                if (j < cb) {
+                    const int yk = int(2 * h * a.n_cache + j * kTile), yv = int((2 * h + 1) * a.n_cache + j * kTile);
+                    attn2::tma_load_2d(sK, &tmKV, 0, yk, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sK + kBox, &tmKV, 64, yk, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sV, &tmKV, 0, yv, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sV + kBox, &tmKV, 64, yv, &bars.kv_full[st]);
+                } else {
+                    const int y = int((j - cb) * kTile);
+                    attn2::tma_load_2d(sK, &tmKc, h * kD, y, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sK + kBox, &tmKc, h * kD + 64, y, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sV, &tmVc, h * kD, y, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sV + kBox, &tmVc, h * kD + 64, y, &bars.kv_full[st]);
+                }
+            }
+        }
+    } else if (warp == 9) {
+        if (lane == 0) {                              // ---- MMA issuer
+            constexpr uint32_t idK = attn::umma_idesc(false), idV = attn::umma_idesc(true);
+            auto issue_s = [&](int t, int64_t j) {    // S_t = Q_t K_j^T
+                const int st = int(j & 1);
+                const uint32_t sk = attn::su32(sKV + st * 2 * kOpTile);
+                const uint32_t sq = attn::su32(sQ + t * kOpTile);
+#pragma unroll
+                for (int k = 0; k < kD / 16; k++) {
+                    const uint32_t off = (k >> 2) * kBox + (k & 3) * 32;
+                    attn::mma_f16(tmem + t * 128, attn2::desc_sw128(sq + off, 16, 1024),
+                                  attn2::desc_sw128(sk + off, 16, 1024), idK, k > 0);
+                }
+                attn::mma_commit(&bars.s_full[t]);
+            };
+            auto issue_pv = [&](int t, int64_t j) {   // O_t += P_t V_j  (P in TMEM over S_t)
+                const int st = int(j & 1);
+                const uint32_t sv = attn::su32(sKV + st * 2 * kOpTile) + kOpTile;
+#pragma unroll
+                for (int k = 0; k < kTile / 16; k++)
+                    attn3::mma_f16_tmem_a(tmem + 256 + t * 128, tmem + t * 128 + k * 8,
+                                          attn2::desc_sw128(sv + k * 2048, kBox, 1024), idV,
+                                          (j > 0 || k > 0) ? 1u : 0u);
+            };
+            attn::bar_wait(&bars.q_full, 0);
+            attn::bar_wait(&bars.kv_full[0], 0);
+            attn::fence_after();
+            issue_s(0, 0);
+            issue_s(1, 0);
+            for (int64_t j = 0; j < nb; j++) {
+                attn::bar_wait(&bars.p_full[0], uint32_t(j & 1));
+                attn::fence_after();
+                issue_pv(0, j);
+                if (j + 1 < nb) {
+                    attn::bar_wait(&bars.kv_full[(j + 1) & 1], uint32_t(((j + 1) >> 1) & 1));
+                    attn::fence_after();
+                    issue_s(0, j + 1);                // overwrites P_A(j): MMAs execute in order
+                }
+                attn::bar_wait(&bars.p_full[1], uint32_t(j & 1));
+                attn::fence_after();
+                issue_pv(1, j);
+                attn::mma_commit(&bars.kv_empty[j & 1]);
+                if (j + 1 < nb) issue_s(1, j + 1);
+            }
+            attn::mma_commit(&bars.o_final);
+        }
+    } else {
+        // ---- softmax (tile t = warp / 4), thread = query row = TMEM lane ----
+        const int t = warp >> 2;
+        const uint32_t t_lane = uint32_t((warp & 3) * 32) << 16;
+        const uint32_t tS = tmem + t * 128 + t_lane, tO = tmem + 256 + t * 128 + t_lane;
+        const float sl2 = a.scale_log2;
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int64_t j = 0; j < nb; j++) {
+            const int64_t cnt = j < cb ? a.n_cache - j * kTile : a.n_cur - (j - cb) * kTile;
+            const int nvalid = int(cnt < kTile ? cnt : kTile);
+            attn::bar_wait(&bars.s_full[t], uint32_t(j & 1));
+            attn::fence_after();
+            float s[128];
+            tmem_ld128(tS, s);
+            float m_new, alpha;
+            bool grow;
+            float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                              make_float2(0.f, 0.f)};     // independent partial row sums
+            auto phase = [&](auto mask_tag) {
+                constexpr bool MASK = decltype(mask_tag)::value;
+                if constexpr (MASK) {
+#pragma unroll
+                    for (int i = 0; i < 128; i++) s[i] = i < nvalid ? s[i] : -INFINITY;
+                }
+                float mv[32];
+#pragma unroll
+                for (int i = 0; i < 32; i++) mv[i] = fmaxf(fmaxf(s[4 * i], s[4 * i + 1]), fmaxf(s[4 * i + 2], s[4 * i + 3]));
+#pragma unroll
+                for (int span = 1; span < 32; span *= 2)
+#pragma unroll
+                    for (int i = 0; i < 32; i += 2 * span) mv[i] = fmaxf(mv[i], mv[i + span]);
+                const float mx = mv[0] * sl2;
+                grow = mx > m_run + 8.f;      // lazy rescale: only when the max grows by > 2^8
+                m_new = grow ? mx : m_run;
+                alpha = grow ? ex2_mufu(m_run - m_new) : 1.f;
+                const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_new, -m_new);
+                // P = exp2(S scale - m) in two halves of 64 columns, each packed to bf16
+                // pairs and written back over S columns already consumed
+#pragma unroll
+                for (int hf = 0; hf < 2; hf++) {
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int i2 = 0; i2 < 32; i2++) {
+                        const int i = hf * 32 + i2;
+                        const float2 x = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
+                        float2 e;
+                        if (2 * i < POLY_FROM) e = make_float2(ex2_mufu(x.x), ex2_mufu(x.y));
+                        else e = ex2_poly2(make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f)));
+                        if constexpr (MASK) {      // the poly path has no -inf
+                            e.x = 2 * i < nvalid ? e.x : 0.f;
+                            e.y = 2 * i + 1 < nvalid ? e.y : 0.f;
+                        }
+                        acc4[i2 & 3] = __fadd2_rn(acc4[i2 & 3], e);
+                        pk[i2] = attn::pack_bf16(e.x, e.y);
+                    }
+                    attn3::tmem_st32u(tS + hf * 32, pk);
+                }
+            };
+            if (nvalid == kTile) phase(std::false_type{});
+            else phase(std::true_type{});
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            // S_t(j) arrived => PV_t(j-1) has completed and PV_t(j) waits for this
+            // thread's p_full arrival: O_t is quiescent for the lazy rescale
+            if (j > 0 && __any_sync(0xffffffffu, grow)) {
+#pragma unroll
+                for (int ch = 0; ch < 4; ch++) {
+                    float ov[32];
+                    attn::tmem_ld32(tO + ch * 32, ov);
+#pragma unroll
+                    for (int i = 0; i < 32; i++) ov[i] *= alpha;
+                    attn::tmem_st32(tO + ch * 32, ov);
+                }
+            }
+            const float2 acc = __fadd2_rn(__fadd2_rn(acc4[0], acc4[1]), __fadd2_rn(acc4[2], acc4[3]));
+            l_run = l_run * alpha + (acc.x + acc.y);
+            m_run = m_new;
+            attn::fence_before();
+            attn2::arrive(&bars.p_full[t]);
+        }
+        // ---- epilogue ----
+        attn::bar_wait(&bars.o_final, 0);
+        attn::fence_after();
+        const float inv_l = 1.f / l_run;
+        const int64_t qi = q0 + t * kTile + (tid & 127);
+#pragma unroll
+        for (int ch = 0; ch < 4; ch++) {
+            float ov[32];
+            attn::tmem_ld32(tO + ch * 32, ov);
+            if (qi < a.nq) {
+                uint4 *dst = reinterpret_cast<uint4 *>(a.out + (qi * a.H + h) * kD + ch * 32);
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    dst[c] = make_uint4(attn::pack_bf16(ov[8 * c] * inv_l, ov[8 * c + 1] * inv_l),
+                                        attn::pack_bf16(ov[8 * c + 2] * inv_l, ov[8 * c + 3] * inv_l),
+                                        attn::pack_bf16(ov[8 * c + 4] * inv_l, ov[8 * c + 5] * inv_l),
+                                        attn::pack_bf16(ov[8 * c + 6] * inv_l, ov[8 * c + 7] * inv_l));
+            }
+        }
+    }
+    attn::fence_before();
+    __syncthreads();
+    if (warp == 9) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const uint16_t *vc, int64_t nq,
+               int64_t nc, int64_t ncur, int H, float scale_log2, uint16_t *out, cudaStream_t st) {
+    CUtensorMap mQ, mKV, mKc, mVc;
+    const bool okq = attn2::make_map(&mQ, q, uint64_t(nq), uint64_t(H) * kD, uint64_t(H) * kD);
+    const bool okkv = nc > 0 ? attn2::make_map(&mKV, kv, uint64_t(2 * H) * nc, kD, kD)
+                             : attn2::make_map(&mKV, q, 1, kD, kD);
+    const bool okk = ncur > 0 ? attn2::make_map(&mKc, kc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
+                              : attn2::make_map(&mKc, q, 1, kD, kD);
+    const bool okv = ncur > 0 ? attn2::make_map(&mVc, vc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
+                              : attn2::make_map(&mVc, q, 1, kD, kD);
+    if (!(okq && okkv && okk && okv)) return set_err(QVG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    const size_t smem = kSmem + 1024;
+    dim3 grid(unsigned((nq + 2 * kTile - 1) / (2 * kTile)), unsigned(H));
+    attn2::Args args{nq, nc, ncur, H, scale_log2, out};
+    static const int poly = [] { const char *e = getenv("QVG_ATTN_POLY"); return e ? atoi(e) : 96; }();
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        kern<<<grid, 320, smem, st>>>(mQ, mKV, mKc, mVc, args);
+    };
+    if (poly >= 128) go(k_attention_pp4<128>);
+    else if (poly >= 112) go(k_attention_pp4<112>);
+    else if (poly >= 96) go(k_attention_pp4<96>);
+    else go(k_attention_pp4<80>);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+}  // namespace attn4
+
 size_t attention_workspace_size(int64_t, int64_t n_cache, int64_t, int H, int d, const qvg_config *) {
     // bf16 reconstruction of the quantized cache (2H planes) for the TMA kernel
     return n_cache > 0 ? size_t(2) * H * n_cache * d * 2 + 256 : 0;
@@ -989,7 +1291,9 @@ int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scal
     } else if (n_cache > 0 && !kv) {
         return set_err(QVG_ERR_BAD_CONFIG, "cache is NULL");
     }
-    const int rc = attn3::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st);
+    static const int use_v3 = [] { const char *e = getenv("QVG_ATTN_KERNEL"); return e && !strcmp(e, "v3"); }();
+    const int rc = use_v3 ? attn3::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st)
+                          : attn4::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st);
     return rc ? set_err(rc, "attention launch failed: %s", cudaGetErrorString(cudaGetLastError())) : QVG_OK;
 }
 

@@ -1555,7 +1555,7 @@ static int codec_kernel_pref() {
     static int pref = -1;
     if (pref < 0) {
         const char *e = getenv("QVG_CODEC_KERNEL");
-        pref = !e ? 0 : !strcmp(e, "wring") ? 0 : !strcmp(e, "stream") ? 1 : !strcmp(e, "v6") ? 6 : !strcmp(e, "v5") ? 5 : !strcmp(e, "v4") ? 4 : 0;
+        pref = !e ? 0 : !strcmp(e, "wring") ? 2 : !strcmp(e, "stream") ? 1 : !strcmp(e, "v6") ? 6 : !strcmp(e, "v5") ? 5 : !strcmp(e, "v4") ? 4 : 0;
     }
     return pref;
 }
@@ -1592,11 +1592,15 @@ static bool v6_plan(int64_t P, int64_t N, int d, int S, int K, V6Launch &L) {
 template <int BITS, int S>
 static void launch_quant_fast(const QuantArgs &a, bool xbf16, cudaStream_t st) {
     const int g = tile_grid(a.ta);
+    // quantize: the v5 kernel (bf16 tables, L1-resident rows in flight over 24
+    // warps/SM) is still the fastest measured for many planes (2.22 vs 2.12
+    // TB/s on the Self-Forcing cache); the per-warp-ring kernel serves the rest
     const int pref = codec_kernel_pref();
-    if (S > 0 && a.v16 && pref == 0 && launch_quantize_wring(a, a.P, BITS, S, xbf16, st)) return;
-    if (S > 0 && a.v16 && pref <= 1 && launch_quantize_stream(a, a.P, BITS, S, xbf16, st)) return;
+    const bool v5_ok = a.v16 && a.v5 && (pref == 0 || pref == 5);
+    if (S > 0 && a.v16 && !v5_ok && (pref == 0 || pref == 2) && launch_quantize_wring(a, a.P, BITS, S, xbf16, st)) return;
+    if (S > 0 && a.v16 && !v5_ok && pref == 1 && launch_quantize_stream(a, a.P, BITS, S, xbf16, st)) return;
     V6Launch L;
-    if (S > 0 && a.v16 && (pref <= 1 || pref == 6) && v6_plan(a.P, a.N, a.d, S, a.K, L)) {
+    if (S > 0 && a.v16 && !v5_ok && pref == 6 && v6_plan(a.P, a.N, a.d, S, a.K, L)) {
         if (xbf16) {
             cudaFuncSetAttribute(k_quantize_v6<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
             k_quantize_v6<BITS, S, true><<<L.grid, 256, L.smem, st>>>(a, L.pl);
@@ -1685,9 +1689,9 @@ template <int BITS, int S>
 static void launch_deq_fast(const DequantArgs &a, bool obf16, cudaStream_t st) {
     const int g = tile_grid(a.ta);
     const int pref = codec_kernel_pref();
-    if (S > 0 && a.v16 && pref <= 1 && launch_dequantize_stream(a, a.P, BITS, S, obf16, st)) return;
+    if (S > 0 && a.v16 && pref <= 2 && launch_dequantize_stream(a, a.P, BITS, S, obf16, st)) return;
     V6Launch L;
-    if (S > 0 && a.v16 && (pref <= 1 || pref == 6) && v6_plan(a.P, a.N, a.d, S, a.K, L)) {
+    if (S > 0 && a.v16 && (pref <= 2 || pref == 6) && v6_plan(a.P, a.N, a.d, S, a.K, L)) {
         if (obf16) {
             cudaFuncSetAttribute(k_dequant_v6<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
             k_dequant_v6<BITS, S, true><<<L.grid, 256, L.smem, st>>>(a, L.pl);
