@@ -48,7 +48,7 @@ def gather_heads(local: torch.Tensor, n_heads: int, group: Optional[dist.Process
     pad = torch.zeros((nq, hmax, d), dtype=local.dtype, device=local.device)
     pad[:, :local.shape[1]] = local
     buf = torch.empty((world, nq, hmax, d), dtype=local.dtype, device=local.device)
-    if hasattr(dist, "all_gather_into_tensor") and local.is_cuda:
+    if hasattr(dist, "all_gather_into_tensor") and local.is_cuda and dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(buf, pad.contiguous(), group=group)
     else:
         dist.all_gather(list(buf.unbind(0)), pad.contiguous(), group=group)
