@@ -128,6 +128,13 @@ static void carve_kmeans(Carver &c, int64_t P, int64_t N, int d, int K, bool own
     b.nd_r = c.take<int32_t>(Lo);
     b.h_start = c.take<int32_t>(80);
     b.ob_leaves = int(Lo);
+    if (assign_tc_ok(d, K)) {
+        b.rsplit = c.take<uint16_t>(int64_t(assign_tc_split_elems(P, N)));
+        b.xnorm = c.take<float>(P * N);
+        b.c2 = c.take<double>(P * K);
+        b.recheck = c.take<int32_t>(P * N);
+        b.n_recheck = c.take<int32_t>(8);
+    }
 }
 
 static int upload_plans(KMeansBuffers &b, int64_t N, int d, cudaStream_t st) {

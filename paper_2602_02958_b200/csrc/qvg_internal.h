@@ -25,6 +25,11 @@ struct KMeansBuffers {
     int64_t *ob_off;
     int32_t *ob_len, *nd_l, *nd_r, *h_start;
     int ob_leaves, ob_heights;
+    // tensor-core assignment (qvg_assign_tc.cu); rsplit == nullptr: exact kernel only
+    uint16_t *rsplit;      // [P][T][3][128x128] bf16 row splits (UMMA layout)
+    float *xnorm;          // [P][N] row norms
+    double *c2;            // [P][K] exact centroid squared norms
+    int32_t *recheck, *n_recheck;
 };
 
 // qvg_codec.cu
@@ -56,6 +61,14 @@ int finalize_stage(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, i
                    cudaStream_t st);
 int run_add_back(const double *residual, const uint16_t *cent, const uint8_t *assign, int64_t P,
                  int64_t N, int d, int K, double *out, cudaStream_t st);
+
+// qvg_assign_tc.cu
+size_t assign_tc_split_elems(int64_t P, int64_t N);
+bool assign_tc_ok(int d, int K);
+int launch_split_rows(const double *rows, uint16_t *split, float *xnorm, int64_t P, int64_t N, cudaStream_t st);
+int launch_assign_tc(const uint16_t *split, const float *xnorm, const double *rows, const double *cent,
+                     const double *c2, int32_t *assign, int32_t *recheck, int32_t *n_recheck,
+                     const PlaneState *st_planes, int skip_done, int64_t P, int64_t N, int K, cudaStream_t st);
 
 // qvg_attn.cu
 size_t attention_workspace_size(int64_t nq, int64_t n_cache, int64_t n_cur, int H, int d,

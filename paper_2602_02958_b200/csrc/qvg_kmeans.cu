@@ -18,6 +18,9 @@
 // Every kernel reads a per-plane `done` flag, so one launch sequence of
 // max_iters Lloyd steps serves planes that converge at different iterations.
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
 #include "qvg_common.cuh"
 #include "qvg_internal.h"
 
@@ -320,6 +323,17 @@ __global__ void __launch_bounds__(256) k_assign(AssignArgs a) {
         int64_t row = r0 + ty + 16 * i;
         if (tx == 0 && row < N) a.assign[p * N + row] = j;
     }
+}
+
+// exact c2 = (centroids ** 2).sum(axis=1) (numpy pairwise, as k_assign) for the
+// tensor-core assignment path; 8 lanes per centroid
+__global__ void k_c2(const double *cent, double *c2, const PlaneState *st, int skip_done, int64_t P, int d, int K) {
+    const int64_t g = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 3;   // (plane, centroid)
+    const int64_t gc = g < P * K ? g : P * K - 1;
+    const int64_t p = gc / K;
+    const double *cc = cent + gc * d;
+    double s = row_pairwise8(d, threadIdx.x & 7, [&](int k) { return __dmul_rn(cc[k], cc[k]); });
+    if ((threadIdx.x & 7) == 0 && g < P * K && !(skip_done && st[p].done)) c2[g] = __dadd_rn(0.0, s);
 }
 
 // ------------------------------------------------------------------------
@@ -625,8 +639,26 @@ static void objective(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K
     k_obj_combine<<<(unsigned)P, 1024, 0, st>>>(o);
 }
 
+// QVG_ASSIGN=exact forces the float64 kernel (A/B measurements)
+static bool assign_tc_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("QVG_ASSIGN");
+        v = (e && !strcmp(e, "exact")) ? 0 : 1;
+    }
+    return v == 1;
+}
+
 static void assign_step(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int skip,
                         cudaStream_t st) {
+    if (b.rsplit && assign_tc_enabled()) {
+        // tensor-core filter with certified argmin + exact recheck (qvg_assign_tc.cu)
+        const int64_t n8 = P * K * 8;
+        k_c2<<<unsigned((n8 + 255) / 256), 256, 0, st>>>(b.cent, b.c2, b.st, skip, P, d, K);
+        launch_assign_tc(b.rsplit, b.xnorm, b.rows, b.cent, b.c2, b.assign, b.recheck, b.n_recheck, b.st, skip,
+                         P, N, K, st);
+        return;
+    }
     AssignArgs aa{b.rows, b.cent, b.assign, b.st, N, d, K, skip};
     k_assign<<<dim3((unsigned)((N + AR - 1) / AR), (unsigned)P), 256, 0, st>>>(aa);
 }
@@ -662,6 +694,9 @@ int run_kmeans_stage(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K,
                      double tol, const double *draws_stage, int64_t draws_stride, bool warm,
                      cudaStream_t st) {
     k_stage_reset<<<g1d(P, 256), 256, 0, st>>>(b.st, P);
+    // the rows are fixed for the whole stage: split them once for the tensor-core assignment
+    if (b.rsplit && assign_tc_enabled() && launch_split_rows(b.rows, b.rsplit, b.xnorm, P, N, st))
+        return QVG_ERR_CUDA;
     if (!warm && run_kmeanspp(b, P, N, d, K, draws_stage, draws_stride, st)) return QVG_ERR_CUDA;
     // objective of the starting centroids (Q/clustering.py:142-143)
     assign_step(b, P, N, d, K, 0, st);

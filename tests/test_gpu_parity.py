@@ -258,3 +258,37 @@ def test_planes_split_into_row_ranges(oracle_lib, P, N):
     ref = oracle_lib.prq_decompress_batch(rp, rs, cent.float().numpy(), asg, N, d, bits, B, 8)
     outb = D.dequantize(dc, torch.bfloat16).cpu()
     assert torch.equal(outb.view(torch.int16), torch.from_numpy(ref).to(torch.bfloat16).view(torch.int16))
+
+
+def test_compress_clustered_many_planes_vs_oracle(oracle_lib):
+    """Bench-like clustered K/V planes (outlier channels x10 / x100) through the
+    full compress: the tensor-core assignment filter with its exact recheck
+    must reproduce the reference's assignments, iterations and bytes."""
+    from paper_2602_02958_b200.synth import kv_cache_planes
+
+    cfg = QuantConfig(bits=2, group_size=64, stages=2, centroids=64)
+    x = kv_cache_planes(2, 6, 1024, 128, seed=5, device="cuda")        # 24 planes
+    P = x.shape[0]
+    dc = D.compress(x, cfg, chunk_index=3)
+    draws = np.stack([oracle_lib.pp_draws(0, 3, 2, 64)] * P)
+    pay, sc, cent, asg, iters = oracle_lib.prq_compress_batch(x.float().cpu().numpy(), 2, 64, 2, 64, 10, 1e-4,
+                                                              draws, 16)
+    assert np.array_equal(dc.assignments.cpu().numpy(), asg)
+    assert np.array_equal(dc.iters.cpu().numpy(), iters)
+    assert np.array_equal(dc.payload.cpu().numpy(), pay)
+    assert np.array_equal(dc.scales.cpu().numpy(), sc)
+
+
+def test_compress_longcat_k256_vs_oracle(oracle_lib):
+    """K = 256 centroids (two 128-centroid blocks in the tensor-core filter)."""
+    from paper_2602_02958_b200.synth import kv_cache_planes
+
+    cfg = QuantConfig(bits=2, group_size=64, stages=1, centroids=256)
+    x = kv_cache_planes(1, 2, 2048, 128, seed=9, device="cuda")        # 4 planes
+    P = x.shape[0]
+    dc = D.compress(x, cfg, chunk_index=0)
+    draws = np.stack([oracle_lib.pp_draws(0, 0, 1, 256)] * P)
+    pay, sc, cent, asg, iters = oracle_lib.prq_compress_batch(x.float().cpu().numpy(), 2, 64, 1, 256, 10, 1e-4,
+                                                              draws, 16)
+    assert np.array_equal(dc.assignments.cpu().numpy(), asg)
+    assert np.array_equal(dc.payload.cpu().numpy(), pay)
