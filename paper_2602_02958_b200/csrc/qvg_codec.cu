@@ -821,12 +821,26 @@ __global__ void __launch_bounds__(256) k_dequant_v5(DequantArgs a, PlaneLoop pl)
     if (all && (threadIdx.x & 31) == 0) atomicOr(a.status, int(all));
 }
 
+__device__ __forceinline__ float v5_max3_nan_abs(float m, float a, float b) {
+    float t, d;
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(t) : "f"(fabsf(a)), "f"(fabsf(b)));
+    asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(m), "f"(t));
+    return d;
+}
+template <int BITS>
+__host__ __device__ constexpr uint32_t v5_magic_sum() {
+    uint32_t acc = 0;
+    for (int k = 0; k < 32 / BITS; k++) acc += 0x4B400000u << (BITS * k);
+    return acc;
+}
+
 template <int BITS, int S, bool XBF16>
 __global__ void __launch_bounds__(256) k_quantize_v5(QuantArgs a, PlaneLoop pl) {
     constexpr int QMAX = (1 << (BITS - 1)) - 1;
     constexpr int SS = S > 0 ? S : 1;
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t bars[2];
+    __shared__ float rcp_tab[128];          // RN32(1 / e4m3(code))
     uint16_t *const tab0 = reinterpret_cast<uint16_t *>(smem);
     uint16_t *const tab1 = reinterpret_cast<uint16_t *>(smem + pl.tbytes);
     const uint32_t d = uint32_t(a.d), N = a.N;
@@ -835,6 +849,7 @@ __global__ void __launch_bounds__(256) k_quantize_v5(QuantArgs a, PlaneLoop pl) 
     const int glanes = 1 << a.gshift;
     const int lane = threadIdx.x & 31;
     bool nonfinite = false;
+    if (threadIdx.x < 128) rcp_tab[threadIdx.x] = __frcp_rn(e4m3_decode_fast(threadIdx.x));
     if (threadIdx.x == 0) {
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -867,9 +882,10 @@ __global__ void __launch_bounds__(256) k_quantize_v5(QuantArgs a, PlaneLoop pl) 
             float eb[kUnroll], am[kUnroll];
 #pragma unroll
             for (int u = 0; u < kUnroll; u++) {
-                // e = sum_t sum_k |r_t,k| bounds every element's sum_t |r_t,k| (the
-                // error-bound input) and, being a plain sum, turns any NaN/Inf in x
-                // or a centroid into a non-finite e: the finiteness check for free.
+                // e = sum_{t<S} max_k |r_t,k| + max_k |r_S,k| bounds every element's
+                // sum_t |r_t,k| (the error-bound input); the maxima propagate NaN, so a
+                // NaN/Inf in x or a centroid makes e non-finite: the finiteness check
+                float2 *r2 = reinterpret_cast<float2 *>(r[u]);
                 float e = 0.f;
 #pragma unroll
                 for (int t = 0; t < S; t++) {
@@ -877,22 +893,18 @@ __global__ void __launch_bounds__(256) k_quantize_v5(QuantArgs a, PlaneLoop pl) 
                     float c[16];
                     cvt16(c4[0], c4[1], c);
 #pragma unroll
-                    for (int k = 0; k < 16; k++) r[u][k] = __fsub_rn(r[u][k], c[k]);
+                    for (int q = 0; q < 8; q++) r2[q] = __fadd2_rn(r2[q], make_float2(-c[2 * q], -c[2 * q + 1]));
                     if (t < S - 1) {
                         float m = 0.f;
 #pragma unroll
-                        for (int k = 0; k < 16; k++) m = fmaxf(m, fabsf(r[u][k]));
+                        for (int q = 0; q < 8; q++) m = v5_max3_nan_abs(m, r2[q].x, r2[q].y);
                         e = __fadd_ru(e, m);
                     }
                 }
-                // NaN/Inf anywhere in x or a centroid reaches r_S; r*0 turns it into NaN
-                float nf = 0.f;
-#pragma unroll
-                for (int k = 0; k < 16; k++) nf = __fmaf_rn(r[u][k], 0.f, nf);
-                nonfinite |= nf != 0.f;
                 float mx = 0.f;
 #pragma unroll
-                for (int k = 0; k < 16; k++) mx = fmaxf(mx, fabsf(r[u][k]));
+                for (int q = 0; q < 8; q++) mx = v5_max3_nan_abs(mx, r2[q].x, r2[q].y);
+                nonfinite |= !(mx <= 3.402823466e38f) || !(e <= 3.402823466e38f);
                 eb[u] = S > 0 ? __fadd_ru(e, mx) : 0.f;
                 am[u] = mx;
             }
@@ -936,56 +948,83 @@ __global__ void __launch_bounds__(256) k_quantize_v5(QuantArgs a, PlaneLoop pl) 
                     if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
                 }
                 const float s = e4m3_decode_fast(code);
+                const float inv = rcp_tab[code & 0x7Fu];
+                const float2 inv2 = make_float2(inv, inv);
+                const float2 *r2 = reinterpret_cast<const float2 *>(r[u]);
+                // codes: the bits of fma(r, 1/s, 1.5*2^23 + 2^(b-1)) are 0x4B400000 + q + 2^(b-1);
+                // a multiply-add tree packs the fields (no carries: q + 2^(b-1) < 2^b)
+                constexpr float MAGIC = 12582912.f + float(1 << (BITS - 1));
+                constexpr int FPW = 32 / BITS;
+                constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
+                float2 yv[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) yv[q] = __ffma2_rn(r2[q], inv2, make_float2(MAGIC, MAGIC));
                 uint32_t b32[BITS / 2];
 #pragma unroll
-                for (int q = 0; q < BITS / 2; q++) b32[q] = 0;
-                bool amb = false;
+                for (int wd = 0; wd < BITS / 2; wd++) {
+                    uint32_t v[FPW];
+#pragma unroll
+                    for (int k2 = 0; k2 < FPW; k2++) {
+                        const int e = wd * FPW + k2;
+                        v[k2] = __float_as_uint((e & 1) ? yv[e >> 1].y : yv[e >> 1].x);
+                    }
+#pragma unroll
+                    for (int span = 1; span < FPW; span *= 2)
+#pragma unroll
+                        for (int k2 = 0; k2 < FPW; k2 += 2 * span) v[k2] += v[k2 + span] << (BITS * span);
+                    b32[wd] = (v[0] - v5_magic_sum<BITS>()) ^ SIGNS;
+                }
+                // ambiguity: per-element window predicate (E plus the 1/s rounding),
+                // reduced over the row, re-evaluated identically for the fix-up
+                const bool all = !(E < 0.125f * s) || code == 0x7Eu;
+                float thr;
+                float2 pa;
                 if constexpr (QMAX == 1) {
-                    const float half = 0.5f * s;
-                    amb = !(E < 0.125f * s);
-#pragma unroll
-                    uint32_t pw = a.one;   // runtime 1: keeps the packing multiplies on the FMA pipe
-#pragma unroll
-                    for (int k = 0; k < 16; k++) {
-                        const float av = fabsf(r[u][k]);
-                        amb |= fabsf(av - half) <= E;
-                        // code 1 (+) or 3 (-) = 2*sign + 1, sign by multiply-high
-                        const uint32_t v = __umulhi(__float_as_uint(r[u][k]), 2u) * (2u * a.one) + a.one;
-                        b32[0] += (av > half ? v : 0u) * pw;
-                        pw *= 4u * a.one;
-                    }
+                    const float h = 0.5f * s;
+                    const float W = __fmaf_ru(h, 2.38418579e-7f, E);
+                    thr = __fmul_ru(__fmul_ru(W, __fadd_ru(s, W)), 1.00000095367f);
+                    pa = make_float2(-h * h, -h * h);
                 } else {
-                    const float inv = __frcp_rn(s);
-#pragma unroll
-                    for (int k = 0; k < 16; k++) {
-                        const float av = fabsf(r[u][k]);
-                        const float t = av * inv;
-                        const float fl = floorf(t);
-                        const float hb = (fl + 0.5f) * s;
-                        const float w = __fmaf_ru(hb, 2.38418579e-7f, E);
-                        amb |= fl < float(QMAX) && av >= __fsub_rd(hb, w) && av <= __fadd_ru(hb, w);
-                        int q = min(int(rintf(t)), QMAX);
-                        if (r[u][k] < 0.f) q = -q;
-                        b32[(k * BITS) >> 5] |= (uint32_t(q) & ((1u << BITS) - 1u)) << ((k * BITS) & 31);
+                    const float delta = __fmaf_ru(__fmul_ru(E, inv), 1.0000002f, float(QMAX + 1) * 2.38418579e-7f);
+                    thr = __fsub_rd(0.5f, delta);
+                    pa = make_float2(-MAGIC, -MAGIC);
+                }
+                auto window = [&](int q) -> float2 {
+                    if constexpr (QMAX == 1) {
+                        const float2 gg = __ffma2_rn(r2[q], r2[q], pa);
+                        return make_float2(fabsf(gg.x), fabsf(gg.y));
+                    } else {
+                        const float2 qf = __fadd2_rn(yv[q], pa);
+                        const float2 dist = __ffma2_rn(r2[q], inv2, make_float2(-qf.x, -qf.y));
+                        return make_float2(fabsf(dist.x), fabsf(dist.y));
                     }
+                };
+                bool amb;
+                {
+                    float wv[8];
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        const float2 w = window(q);
+                        wv[q] = QMAX == 1 ? fminf(w.x, w.y) : fmaxf(w.x, w.y);
+                    }
+#pragma unroll
+                    for (int span = 1; span < 8; span *= 2)
+#pragma unroll
+                        for (int q = 0; q < 8; q += 2 * span) wv[q] = QMAX == 1 ? fminf(wv[q], wv[q + span]) : fmaxf(wv[q], wv[q + span]);
+                    amb = all || (QMAX == 1 ? wv[0] <= thr : wv[0] >= thr);
                 }
                 amb &= valid;
                 if (__any_sync(0xffffffffu, amb) && amb) {   // exact codes (rare)
                     uint32_t todo = 0;
-                    const bool all = !(E < 0.125f * s);
-                    const float inv = __frcp_rn(s);
 #pragma unroll
-                    for (int k = 0; k < 16; k++) {
-                        const float av = fabsf(r[u][k]);
-                        bool in;
-                        if constexpr (QMAX == 1) in = fabsf(av - 0.5f * s) <= E;
-                        else {
-                            const float fl = floorf(av * inv);
-                            const float hb = (fl + 0.5f) * s;
-                            const float w = __fmaf_ru(hb, 2.38418579e-7f, E);
-                            in = fl < float(QMAX) && av >= __fsub_rd(hb, w) && av <= __fadd_ru(hb, w);
-                        }
-                        todo |= (all || in) ? 1u << k : 0u;
+                    for (int q = 0; q < 8; q++) {
+                        const float2 w = window(q);
+                        bool in0, in1;
+                        if constexpr (QMAX == 1) { in0 = w.x <= thr; in1 = w.y <= thr; }
+                        else { in0 = w.x >= thr; in1 = w.y >= thr; }
+                        in0 |= all || !(fabsf(r2[q].x) <= 3.402823466e38f);
+                        in1 |= all || !(fabsf(r2[q].y) <= 3.402823466e38f);
+                        todo |= (in0 ? 1u << (2 * q) : 0u) | (in1 ? 2u << (2 * q) : 0u);
                     }
                     while (todo) {
                         const int k = __ffs(todo) - 1;
@@ -1689,7 +1728,7 @@ template <int BITS, int S>
 static void launch_deq_fast(const DequantArgs &a, bool obf16, cudaStream_t st) {
     const int g = tile_grid(a.ta);
     const int pref = codec_kernel_pref();
-    if (S > 0 && a.v16 && pref <= 2 && launch_dequantize_stream(a, a.P, BITS, S, obf16, st)) return;
+    if (S > 0 && a.v16 && (pref <= 3) && launch_dequantize_stream(a, a.P, BITS, S, obf16, st)) return;
     V6Launch L;
     if (S > 0 && a.v16 && (pref <= 2 || pref == 6) && v6_plan(a.P, a.N, a.d, S, a.K, L)) {
         if (obf16) {
