@@ -1013,7 +1013,7 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 }
 
 // columns [POLY_FROM, 128) of each S row use the polynomial exp2
-template <int POLY_FROM>
+template <int POLY_FROM, bool TR = false>
 __global__ void __launch_bounds__(320, 1)
 k_attention_pp4(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
                 const __grid_constant__ CUtensorMap tmKc, const __grid_constant__ CUtensorMap tmVc, attn2::Args a) {
@@ -1104,21 +1104,31 @@ k_attention_pp4(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             attn::fence_after();
             issue_s(0, 0);
             issue_s(1, 0);
+            long long tr[4][4];
+            const long long t0c = clock64();
             for (int64_t j = 0; j < nb; j++) {
                 attn::bar_wait(&bars.p_full[0], uint32_t(j & 1));
+                if (TR && j >= 8 && j < 12) tr[j - 8][0] = clock64() - t0c;
                 attn::fence_after();
                 issue_pv(0, j);
                 if (j + 1 < nb) {
                     attn::bar_wait(&bars.kv_full[(j + 1) & 1], uint32_t(((j + 1) >> 1) & 1));
+                    if (TR && j >= 8 && j < 12) tr[j - 8][1] = clock64() - t0c;
                     attn::fence_after();
                     issue_s(0, j + 1);                // overwrites P_A(j): MMAs execute in order
                 }
                 attn::bar_wait(&bars.p_full[1], uint32_t(j & 1));
+                if (TR && j >= 8 && j < 12) tr[j - 8][2] = clock64() - t0c;
                 attn::fence_after();
                 issue_pv(1, j);
                 attn::mma_commit(&bars.kv_empty[j & 1]);
                 if (j + 1 < nb) issue_s(1, j + 1);
+                if (TR && j >= 8 && j < 12) tr[j - 8][3] = clock64() - t0c;
             }
+            if (TR && blockIdx.x == 0 && blockIdx.y == 0)
+                for (int q = 0; q < 4; q++)
+                    printf("MMA j=%d pA_ready=%lld kv_ready=%lld pB_ready=%lld issued=%lld\n", q + 8, tr[q][0], tr[q][1],
+                           tr[q][2], tr[q][3]);
             attn::mma_commit(&bars.o_final);
         }
     } else {
@@ -1128,13 +1138,18 @@ k_attention_pp4(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         const uint32_t tS = tmem + t * 128 + t_lane, tO = tmem + 256 + t * 128 + t_lane;
         const float sl2 = a.scale_log2;
         float m_run = -INFINITY, l_run = 0.f;
+        long long tr[4][8];
+        const long long t0c = clock64();
         for (int64_t j = 0; j < nb; j++) {
             const int64_t cnt = j < cb ? a.n_cache - j * kTile : a.n_cur - (j - cb) * kTile;
             const int nvalid = int(cnt < kTile ? cnt : kTile);
+            if (TR && j >= 8 && j < 12) tr[j - 8][0] = clock64() - t0c;
             attn::bar_wait(&bars.s_full[t], uint32_t(j & 1));
+            if (TR && j >= 8 && j < 12) tr[j - 8][1] = clock64() - t0c;
             attn::fence_after();
             float s[128];
             tmem_ld128(tS, s);
+            if (TR && j >= 8 && j < 12) tr[j - 8][2] = clock64() - t0c;
             float m_new, alpha;
             bool grow;
             float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
@@ -1145,15 +1160,21 @@ k_attention_pp4(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 #pragma unroll
                     for (int i = 0; i < 128; i++) s[i] = i < nvalid ? s[i] : -INFINITY;
                 }
-                float mv[32];
+                // 3-input max tree: 128 -> 43 -> 15 -> 5 -> 2 -> 1
+                float m43[43];
 #pragma unroll
-                for (int i = 0; i < 32; i++) mv[i] = fmaxf(fmaxf(s[4 * i], s[4 * i + 1]), fmaxf(s[4 * i + 2], s[4 * i + 3]));
+                for (int i = 0; i < 42; i++) m43[i] = fmaxf(fmaxf(s[3 * i], s[3 * i + 1]), s[3 * i + 2]);
+                m43[42] = fmaxf(s[126], s[127]);
+                float m15[15];
 #pragma unroll
-                for (int span = 1; span < 32; span *= 2)
+                for (int i = 0; i < 14; i++) m15[i] = fmaxf(fmaxf(m43[3 * i], m43[3 * i + 1]), m43[3 * i + 2]);
+                m15[14] = m43[42];
+                float m5[5];
 #pragma unroll
-                    for (int i = 0; i < 32; i += 2 * span) mv[i] = fmaxf(mv[i], mv[i + span]);
-                const float mx = mv[0] * sl2;
-                grow = mx > m_run + 8.f;      // lazy rescale: only when the max grows by > 2^8
+                for (int i = 0; i < 5; i++) m5[i] = fmaxf(fmaxf(m15[3 * i], m15[3 * i + 1]), m15[3 * i + 2]);
+                const float mx = fmaxf(fmaxf(m5[0], m5[1]), fmaxf(fmaxf(m5[2], m5[3]), m5[4])) * sl2;
+                if (TR && j >= 8 && j < 12) tr[j - 8][4] = clock64() - t0c;
+                grow = mx > m_run + 16.f;     // lazy rescale: only when the max grows by > 2^16 (P <= 2^16: fp32/bf16-safe)
                 m_new = grow ? mx : m_run;
                 alpha = grow ? ex2_mufu(m_run - m_new) : 1.f;
                 const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_new, -m_new);
@@ -1177,11 +1198,13 @@ k_attention_pp4(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
                         pk[i2] = attn::pack_bf16(e.x, e.y);
                     }
                     attn3::tmem_st32u(tS + hf * 32, pk);
+                    if (TR && j >= 8 && j < 12) tr[j - 8][5 + hf] = clock64() - t0c;
                 }
             };
             if (nvalid == kTile) phase(std::false_type{});
             else phase(std::true_type{});
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if (TR && j >= 8 && j < 12) tr[j - 8][7] = clock64() - t0c;
             // S_t(j) arrived => PV_t(j-1) has completed and PV_t(j) waits for this
             // thread's p_full arrival: O_t is quiescent for the lazy rescale
             if (j > 0 && __any_sync(0xffffffffu, grow)) {
@@ -1199,7 +1222,12 @@ k_attention_pp4(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             m_run = m_new;
             attn::fence_before();
             attn2::arrive(&bars.p_full[t]);
+            if (TR && j >= 8 && j < 12) tr[j - 8][3] = clock64() - t0c;
         }
+        if (TR && blockIdx.x == 0 && blockIdx.y == 0 && (tid & 127) == 0)
+            for (int q = 0; q < 4; q++)
+                printf("SM%d j=%d start=%lld s_ready=%lld s_loaded=%lld max=%lld half0=%lld half1=%lld st_done=%lld p_arrived=%lld\n",
+                       t, q + 8, tr[q][0], tr[q][1], tr[q][2], tr[q][4], tr[q][5], tr[q][6], tr[q][7], tr[q][3]);
         // ---- epilogue ----
         attn::bar_wait(&bars.o_final, 0);
         attn::fence_after();
@@ -1244,10 +1272,19 @@ static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const 
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         kern<<<grid, 320, smem, st>>>(mQ, mKV, mKc, mVc, args);
     };
+    static const bool trace = getenv("QVG_ATTN_TRACE") != nullptr;
+    if (trace) {
+        if (poly >= 96) go(k_attention_pp4<96, true>);
+        else if (poly >= 80) go(k_attention_pp4<80, true>);
+        else if (poly >= 64) go(k_attention_pp4<64, true>);
+        else go(k_attention_pp4<48, true>);
+        return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+    }
     if (poly >= 128) go(k_attention_pp4<128>);
-    else if (poly >= 112) go(k_attention_pp4<112>);
     else if (poly >= 96) go(k_attention_pp4<96>);
-    else go(k_attention_pp4<80>);
+    else if (poly >= 80) go(k_attention_pp4<80>);
+    else if (poly >= 64) go(k_attention_pp4<64>);
+    else go(k_attention_pp4<48>);
     return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
 }
 }  // namespace attn4
