@@ -1542,6 +1542,255 @@ __global__ void __launch_bounds__(256, 2) k_quantize_v6(QuantArgs a, V6Plane pl)
 }
 
 // ------------------------------------------------------------------------
+// v5w: the v5 quantize with ONE 768-thread CTA per SM (24 warps, as v5's 3
+// CTAs) sharing double-buffered f32 centroid tables (padded, conflict-free
+// 16-channel blocks) widened once per plane from a TMA-staged bf16 copy: the
+// per-element bf16 -> f32 conversions of the centroids disappear.
+// ------------------------------------------------------------------------
+struct V5W {
+    uint32_t P, tbytes, off_tab, tab_floats, pitch, nchunk, lchunk;
+};
+__host__ __device__ __forceinline__ uint32_t v5w_blk(uint32_t c) { return 16u * c + 4u * (c >> 1); }
+__device__ __forceinline__ void v5w_widen(const uint16_t *stg, float *tab, uint32_t nchunk, uint32_t lchunk,
+                                          uint32_t pitch) {
+    const uint32_t cmask = (1u << lchunk) - 1u;
+    for (uint32_t q = threadIdx.x; q < nchunk; q += blockDim.x) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(stg + size_t(q) * 16);
+        float c[16];
+        cvt16(src[0], src[1], c);
+        float4 *dst = reinterpret_cast<float4 *>(tab + size_t(q >> lchunk) * pitch + v5w_blk(q & cmask));
+#pragma unroll
+        for (int jj = 0; jj < 4; jj++) dst[jj] = make_float4(c[4 * jj], c[4 * jj + 1], c[4 * jj + 2], c[4 * jj + 3]);
+    }
+}
+
+template <int BITS, int S, bool XBF16>
+__global__ void __launch_bounds__(768, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
+    constexpr int QMAX = (1 << (BITS - 1)) - 1;
+    constexpr int SS = S > 0 ? S : 1;
+    extern __shared__ __align__(128) uint8_t smem[];
+    __shared__ uint64_t bar;
+    __shared__ float rcp_tab[128];          // RN32(1 / e4m3(code))
+    uint16_t *const stg = reinterpret_cast<uint16_t *>(smem);
+    float *const tabs = reinterpret_cast<float *>(smem + pl.off_tab);
+    const uint32_t d = uint32_t(a.d), N = a.N;
+    const uint32_t cc = threadIdx.x & ((1u << a.lvpr) - 1u);
+    const int col = int(cc) << 4;
+    const uint32_t coff = v5w_blk(cc);
+    const uint32_t rslot = threadIdx.x >> a.lvpr, rpp = 768u >> a.lvpr;
+    const int glanes = 1 << a.gshift;
+    const int lane = threadIdx.x & 31;
+    bool nonfinite = false;
+    if (threadIdx.x < 128) rcp_tab[threadIdx.x] = __frcp_rn(e4m3_decode_fast(threadIdx.x));
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (S > 0 && threadIdx.x == 0 && blockIdx.x < pl.P) stage_table(a.cent, blockIdx.x, pl.tbytes, stg, &bar);
+    uint32_t j = 0;
+    for (uint32_t p = blockIdx.x; p < pl.P; p += gridDim.x, j++) {
+        // widen plane p's staged bf16 table into f32 buffer j&1 (the buffer was last
+        // read two planes ago, before the previous plane's barrier), then restage
+        float *const ct = tabs + (j & 1u) * pl.tab_floats;
+        if (S > 0) {
+            mbar_wait(&bar, j & 1u);
+            v5w_widen(stg, ct, pl.nchunk, pl.lchunk, pl.pitch);
+            __syncthreads();
+            if (threadIdx.x == 0 && p + gridDim.x < pl.P) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                stage_table(a.cent, p + gridDim.x, pl.tbytes, stg, &bar);
+            }
+        }
+        const uint64_t pN = uint64_t(p) * N;
+        const uint8_t *xb = static_cast<const uint8_t *>(a.x) + pN * d * (XBF16 ? 2 : 4);
+        const uint8_t *ap = a.asg + pN * S;
+        for (uint32_t i0 = 0; i0 < N; i0 += rpp * kUnroll) {
+            float r[kUnroll][16];
+            uint32_t ii[kUnroll];
+            int ai[kUnroll][SS];
+#pragma unroll
+            for (int u = 0; u < kUnroll; u++) {
+                const uint32_t i = i0 + u * rpp + rslot;
+                ii[u] = i < N ? i : N - 1;
+                load_x16<XBF16>(xb, ii[u] * d + col, r[u]);
+#pragma unroll
+                for (int t = 0; t < S; t++) ai[u][t] = __ldg(ap + t * N + ii[u]);
+            }
+            float eb[kUnroll], am[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; u++) {
+                // e = sum_{t<S} max_k |r_t,k| + max_k |r_S,k| bounds every element's
+                // sum_t |r_t,k| (the error-bound input); the maxima propagate NaN, so a
+                // NaN/Inf in x or a centroid makes e non-finite: the finiteness check
+                float2 *r2 = reinterpret_cast<float2 *>(r[u]);
+                float e = 0.f;
+#pragma unroll
+                for (int t = 0; t < S; t++) {
+                    const float4 *c4 = reinterpret_cast<const float4 *>(ct + uint32_t(t * a.K + ai[u][t]) * pl.pitch + coff);
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const float4 cv = c4[q];
+                        r2[2 * q] = __fadd2_rn(r2[2 * q], make_float2(-cv.x, -cv.y));
+                        r2[2 * q + 1] = __fadd2_rn(r2[2 * q + 1], make_float2(-cv.z, -cv.w));
+                    }
+                    if (t < S - 1) {
+                        float m = 0.f;
+#pragma unroll
+                        for (int q = 0; q < 8; q++) m = v5_max3_nan_abs(m, r2[q].x, r2[q].y);
+                        e = __fadd_ru(e, m);
+                    }
+                }
+                float mx = 0.f;
+#pragma unroll
+                for (int q = 0; q < 8; q++) mx = v5_max3_nan_abs(mx, r2[q].x, r2[q].y);
+                nonfinite |= !(mx <= 3.402823466e38f) || !(e <= 3.402823466e38f);
+                eb[u] = S > 0 ? __fadd_ru(e, mx) : 0.f;
+                am[u] = mx;
+            }
+            for (int m = 1; m < glanes; m <<= 1) {
+#pragma unroll
+                for (int u = 0; u < kUnroll; u++) {
+                    am[u] = fmaxf(am[u], __shfl_xor_sync(0xffffffffu, am[u], m));
+                    eb[u] = fmaxf(eb[u], __shfl_xor_sync(0xffffffffu, eb[u], m));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; u++) {
+                const bool valid = i0 + u * rpp + rslot < N;
+                const float E = __fmul_ru(eb[u], 2.38418579e-7f);
+                uint32_t code;
+                bool camb = false;
+                if (am[u] == 0.f && E == 0.f) code = 0x38u;
+                else {
+                    const float lo = __fsub_rd(am[u], E), hi = __fadd_ru(am[u], E);
+                    if (lo > 0.f) code = scale_code<QMAX>(lo, hi, camb);
+                    else { code = 0x38u; camb = true; }
+                }
+                camb &= valid;
+                auto exact_r = [&](int k) {
+                    return v6_exact_residual<XBF16, S>(xb, ct, ii[u] * d + col + k, coff + k, pl.pitch, a.K, ai[u][0],
+                                                    ai[u][SS > 1 ? 1 : 0], ai[u][SS > 2 ? 2 : 0],
+                                                    ai[u][SS > 3 ? 3 : 0]);
+                };
+                if (__any_sync(0xffffffffu, camb)) {          // exact scale (rare)
+                    const float thr = __fsub_rd(am[u], __fmul_ru(E, 2.f));
+                    uint32_t cand = 0;
+#pragma unroll
+                    for (int k = 0; k < 16; k++) cand |= (camb && fabsf(r[u][k]) >= thr) ? 1u << k : 0u;
+                    double a64 = 0.0;
+                    while (cand) {
+                        const int k = __ffs(cand) - 1;
+                        cand &= cand - 1;
+                        a64 = fmax(a64, fabs(exact_r(k)));
+                    }
+                    for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
+                    if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
+                }
+                const float s = e4m3_decode_fast(code);
+                const float inv = rcp_tab[code & 0x7Fu];
+                const float2 inv2 = make_float2(inv, inv);
+                const float2 *r2 = reinterpret_cast<const float2 *>(r[u]);
+                // codes: the bits of fma(r, 1/s, 1.5*2^23 + 2^(b-1)) are 0x4B400000 + q + 2^(b-1);
+                // a multiply-add tree packs the fields (no carries: q + 2^(b-1) < 2^b)
+                constexpr float MAGIC = 12582912.f + float(1 << (BITS - 1));
+                constexpr int FPW = 32 / BITS;
+                constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
+                float2 yv[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) yv[q] = __ffma2_rn(r2[q], inv2, make_float2(MAGIC, MAGIC));
+                uint32_t b32[BITS / 2];
+#pragma unroll
+                for (int wd = 0; wd < BITS / 2; wd++) {
+                    uint32_t v[FPW];
+#pragma unroll
+                    for (int k2 = 0; k2 < FPW; k2++) {
+                        const int e = wd * FPW + k2;
+                        v[k2] = __float_as_uint((e & 1) ? yv[e >> 1].y : yv[e >> 1].x);
+                    }
+#pragma unroll
+                    for (int span = 1; span < FPW; span *= 2)
+#pragma unroll
+                        for (int k2 = 0; k2 < FPW; k2 += 2 * span) v[k2] += v[k2 + span] << (BITS * span);
+                    b32[wd] = (v[0] - v5_magic_sum<BITS>()) ^ SIGNS;
+                }
+                // ambiguity: per-element window predicate (E plus the 1/s rounding),
+                // reduced over the row, re-evaluated identically for the fix-up
+                const bool all = !(E < 0.125f * s) || code == 0x7Eu;
+                float thr;
+                float2 pa;
+                if constexpr (QMAX == 1) {
+                    const float h = 0.5f * s;
+                    const float W = __fmaf_ru(h, 2.38418579e-7f, E);
+                    thr = __fmul_ru(__fmul_ru(W, __fadd_ru(s, W)), 1.00000095367f);
+                    pa = make_float2(-h * h, -h * h);
+                } else {
+                    const float delta = __fmaf_ru(__fmul_ru(E, inv), 1.0000002f, float(QMAX + 1) * 2.38418579e-7f);
+                    thr = __fsub_rd(0.5f, delta);
+                    pa = make_float2(-MAGIC, -MAGIC);
+                }
+                auto window = [&](int q) -> float2 {
+                    if constexpr (QMAX == 1) {
+                        const float2 gg = __ffma2_rn(r2[q], r2[q], pa);
+                        return make_float2(fabsf(gg.x), fabsf(gg.y));
+                    } else {
+                        const float2 qf = __fadd2_rn(yv[q], pa);
+                        const float2 dist = __ffma2_rn(r2[q], inv2, make_float2(-qf.x, -qf.y));
+                        return make_float2(fabsf(dist.x), fabsf(dist.y));
+                    }
+                };
+                bool amb;
+                {
+                    float wv[8];
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        const float2 w = window(q);
+                        wv[q] = QMAX == 1 ? fminf(w.x, w.y) : fmaxf(w.x, w.y);
+                    }
+#pragma unroll
+                    for (int span = 1; span < 8; span *= 2)
+#pragma unroll
+                        for (int q = 0; q < 8; q += 2 * span) wv[q] = QMAX == 1 ? fminf(wv[q], wv[q + span]) : fmaxf(wv[q], wv[q + span]);
+                    amb = all || (QMAX == 1 ? wv[0] <= thr : wv[0] >= thr);
+                }
+                amb &= valid;
+                if (__any_sync(0xffffffffu, amb) && amb) {   // exact codes (rare)
+                    uint32_t todo = 0;
+#pragma unroll
+                    for (int q = 0; q < 8; q++) {
+                        const float2 w = window(q);
+                        bool in0, in1;
+                        if constexpr (QMAX == 1) { in0 = w.x <= thr; in1 = w.y <= thr; }
+                        else { in0 = w.x >= thr; in1 = w.y >= thr; }
+                        in0 |= all || !(fabsf(r2[q].x) <= 3.402823466e38f);
+                        in1 |= all || !(fabsf(r2[q].y) <= 3.402823466e38f);
+                        todo |= (in0 ? 1u << (2 * q) : 0u) | (in1 ? 2u << (2 * q) : 0u);
+                    }
+                    while (todo) {
+                        const int k = __ffs(todo) - 1;
+                        todo &= todo - 1;
+                        const uint32_t q = exact_code<QMAX>(exact_r(k), s) & ((1u << BITS) - 1u);
+                        const int sh = (k * BITS) & 31, wi = (k * BITS) >> 5;
+#pragma unroll
+                        for (int q2 = 0; q2 < BITS / 2; q2++)
+                            if (q2 == wi) b32[q2] = (b32[q2] & ~(((1u << BITS) - 1u) << sh)) | (q << sh);
+                    }
+                }
+                if (!valid) continue;
+                const uint32_t e0 = ii[u] * d + col;
+                uint8_t *plp = a.payload + uint64_t(p) * a.pb + ((e0 * BITS) >> 3);
+                if constexpr (BITS == 2) *reinterpret_cast<uint32_t *>(plp) = b32[0];
+                else if constexpr (BITS == 4) *reinterpret_cast<uint2 *>(plp) = make_uint2(b32[0], b32[1]);
+                else *reinterpret_cast<uint4 *>(plp) = make_uint4(b32[0], b32[1], b32[2], b32[3]);
+                if ((lane & (glanes - 1)) == 0) a.scales[uint64_t(p) * a.ng + (e0 >> a.lgB)] = uint8_t(code);
+            }
+        }
+    }
+    const uint32_t all = __reduce_or_sync(0xffffffffu, nonfinite ? uint32_t(QVG_STATUS_NONFINITE) : 0u);
+    if (all && lane == 0) atomicOr(a.status, int(all));
+}
+
+// ------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------
 static int grid_for(int64_t work, int block) {
@@ -1594,7 +1843,7 @@ static int codec_kernel_pref() {
     static int pref = -1;
     if (pref < 0) {
         const char *e = getenv("QVG_CODEC_KERNEL");
-        pref = !e ? 0 : !strcmp(e, "wring") ? 2 : !strcmp(e, "stream") ? 1 : !strcmp(e, "v6") ? 6 : !strcmp(e, "v5") ? 5 : !strcmp(e, "v4") ? 4 : 0;
+        pref = !e ? 0 : !strcmp(e, "v5w") ? 7 : !strcmp(e, "wring") ? 2 : !strcmp(e, "stream") ? 1 : !strcmp(e, "v6") ? 6 : !strcmp(e, "v5") ? 5 : !strcmp(e, "v4") ? 4 : 0;
     }
     return pref;
 }
@@ -1629,12 +1878,36 @@ static bool v6_plan(int64_t P, int64_t N, int d, int S, int K, V6Launch &L) {
 }
 
 template <int BITS, int S>
+static bool launch_quant_v5w(const QuantArgs &a, bool xbf16, cudaStream_t st) {
+    const int n = a.d / 16;
+    if (n < 2 || (n & (n - 1)) || int64_t(a.P) < 148) return false;
+    const uint32_t pitch = uint32_t(16 * n + 4 * (n / 2));
+    const size_t tbytes = size_t(S) * a.K * a.d * 2;
+    const size_t off_tab = (tbytes + 127) & ~size_t(127);
+    const size_t tab_floats = size_t(S) * a.K * pitch;
+    const size_t smem = off_tab + 2 * tab_floats * 4;
+    if (smem > 220 * 1024) return false;
+    const V5W pl{a.P, uint32_t(tbytes), uint32_t(off_tab), uint32_t(tab_floats), pitch,
+                 uint32_t(size_t(S) * a.K * n), uint32_t(ilog2(n))};
+    const int grid = int(a.P < 148u ? a.P : 148u);
+    if (xbf16) {
+        cudaFuncSetAttribute(k_quantize_v5w<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_quantize_v5w<BITS, S, true><<<grid, 768, smem, st>>>(a, pl);
+    } else {
+        cudaFuncSetAttribute(k_quantize_v5w<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_quantize_v5w<BITS, S, false><<<grid, 768, smem, st>>>(a, pl);
+    }
+    return true;
+}
+
+template <int BITS, int S>
 static void launch_quant_fast(const QuantArgs &a, bool xbf16, cudaStream_t st) {
     const int g = tile_grid(a.ta);
     // quantize: the v5 kernel (bf16 tables, L1-resident rows in flight over 24
     // warps/SM) is still the fastest measured for many planes (2.22 vs 2.12
     // TB/s on the Self-Forcing cache); the per-warp-ring kernel serves the rest
     const int pref = codec_kernel_pref();
+    if (S > 0 && a.v16 && (pref == 0 || pref == 7) && launch_quant_v5w<BITS, S>(a, xbf16, st)) return;
     const bool v5_ok = a.v16 && a.v5 && (pref == 0 || pref == 5);
     if (S > 0 && a.v16 && !v5_ok && (pref == 0 || pref == 2) && launch_quantize_wring(a, a.P, BITS, S, xbf16, st)) return;
     if (S > 0 && a.v16 && !v5_ok && pref == 1 && launch_quantize_stream(a, a.P, BITS, S, xbf16, st)) return;
