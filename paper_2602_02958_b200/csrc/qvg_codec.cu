@@ -1549,6 +1549,7 @@ __global__ void __launch_bounds__(256, 2) k_quantize_v6(QuantArgs a, V6Plane pl)
 // ------------------------------------------------------------------------
 struct V5W {
     uint32_t P, tbytes, off_tab, tab_floats, pitch, nchunk, lchunk;
+    uint32_t nbuf;       // f32 table buffers (2, or 1 when two do not fit: one more barrier per plane)
 };
 __host__ __device__ __forceinline__ uint32_t v5w_blk(uint32_t c) { return 16u * c + 4u * (c >> 1); }
 __device__ __forceinline__ void v5w_widen(const uint16_t *stg, float *tab, uint32_t nchunk, uint32_t lchunk,
@@ -1592,8 +1593,9 @@ __global__ void __launch_bounds__(768, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
     for (uint32_t p = blockIdx.x; p < pl.P; p += gridDim.x, j++) {
         // widen plane p's staged bf16 table into f32 buffer j&1 (the buffer was last
         // read two planes ago, before the previous plane's barrier), then restage
-        float *const ct = tabs + (j & 1u) * pl.tab_floats;
+        float *const ct = tabs + (pl.nbuf == 2 ? (j & 1u) : 0u) * pl.tab_floats;
         if (S > 0) {
+            if (pl.nbuf == 1 && j > 0) __syncthreads();       // previous plane done with the only buffer
             mbar_wait(&bar, j & 1u);
             v5w_widen(stg, ct, pl.nchunk, pl.lchunk, pl.pitch);
             __syncthreads();
@@ -1885,10 +1887,15 @@ static bool launch_quant_v5w(const QuantArgs &a, bool xbf16, cudaStream_t st) {
     const size_t tbytes = size_t(S) * a.K * a.d * 2;
     const size_t off_tab = (tbytes + 127) & ~size_t(127);
     const size_t tab_floats = size_t(S) * a.K * pitch;
-    const size_t smem = off_tab + 2 * tab_floats * 4;
+    uint32_t nbuf = 2;
+    size_t smem = off_tab + 2 * tab_floats * 4;
+    if (smem > 220 * 1024) {
+        nbuf = 1;
+        smem = off_tab + tab_floats * 4;
+    }
     if (smem > 220 * 1024) return false;
     const V5W pl{a.P, uint32_t(tbytes), uint32_t(off_tab), uint32_t(tab_floats), pitch,
-                 uint32_t(size_t(S) * a.K * n), uint32_t(ilog2(n))};
+                 uint32_t(size_t(S) * a.K * n), uint32_t(ilog2(n)), nbuf};
     const int grid = int(a.P < 148u ? a.P : 148u);
     if (xbf16) {
         cudaFuncSetAttribute(k_quantize_v5w<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -93,15 +93,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_quantize_stream(QuantArgs a, Ge
     const int glanes = 1 << a.gshift;
     bool nonfinite = false;
     uint32_t cur = 0xFFFFFFFFu, jp = 0, k = 0, ph = 0;
-    if (S > 0 && threadIdx.x == 0 && sc.valid()) stage_table(a.cent, sc.p, g.tbytes, stg, &bars.tab);
+    if (S > 0 && !g.stg_global && threadIdx.x == 0 && sc.valid()) stage_table(a.cent, sc.p, g.tbytes, stg, &bars.tab);
     for (; sc.valid(); sc.next(g), k = k + 1 == g.nst ? (ph ^= 1u, 0u) : k + 1) {
         const uint32_t p = sc.p;
         if (S > 0 && p != cur) {
             named_sync_consumers();
-            mbar_wait(&bars.tab, jp & 1u);
-            widen(stg, tab, meta, g);
+            if (!g.stg_global) mbar_wait(&bars.tab, jp & 1u);
+            widen(g.stg_global ? a.cent + size_t(p) * (g.tbytes / 2) : stg, tab, meta, g);
             named_sync_consumers();
-            if (threadIdx.x == 0) {
+            if (!g.stg_global && threadIdx.x == 0) {
                 const int64_t nx = sc.next_plane(g);
                 if (nx >= 0) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -376,15 +376,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_stream(DequantArgs a, G
     const uint32_t mhi = ((1u << BITS) - 1u) << POS, one = 0x3F800000u;
     bool bad_scale = false, bad_asg = false;
     uint32_t cur = 0xFFFFFFFFu, jp = 0, k = 0, ph = 0;
-    if (S > 0 && threadIdx.x == 0 && sc.valid()) stage_table(a.cent, sc.p, g.tbytes, stg, &bars.tab);
+    if (S > 0 && !g.stg_global && threadIdx.x == 0 && sc.valid()) stage_table(a.cent, sc.p, g.tbytes, stg, &bars.tab);
     for (; sc.valid(); sc.next(g), k = k + 1 == g.nst ? (ph ^= 1u, 0u) : k + 1) {
         const uint32_t p = sc.p;
         if (S > 0 && p != cur) {
             named_sync_consumers();
-            mbar_wait(&bars.tab, jp & 1u);
-            widen(stg, tab, meta, g);
+            if (!g.stg_global) mbar_wait(&bars.tab, jp & 1u);
+            widen(g.stg_global ? a.cent + size_t(p) * (g.tbytes / 2) : stg, tab, meta, g);
             named_sync_consumers();
-            if (threadIdx.x == 0) {
+            if (!g.stg_global && threadIdx.x == 0) {
                 const int64_t nx = sc.next_plane(g);
                 if (nx >= 0) {
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -559,6 +559,7 @@ static bool plan(bool quant, int64_t P, int64_t N, int d, int S, int K, int bits
     size_t off_tab = (tbytes + 127) & ~size_t(127);
     size_t off_meta = off_tab + ((tabb + 127) & ~size_t(127));
     size_t off_ring = off_meta + ((nchunk * 8 + 1023) & ~size_t(1023));
+    uint32_t stg_global = 0;
     uint32_t big_row, small_row;
     if (quant) {
         big_row = uint32_t(d * xbytes);
@@ -573,7 +574,14 @@ static bool plan(bool quant, int64_t P, int64_t N, int d, int S, int K, int bits
     const size_t small = size_t(R) * small_row + size_t(S) * R;
     const size_t stage = (big + ((small + 15) & ~size_t(15)) + 127) & ~size_t(127);
     const size_t budget = 227 * 1024 - 1024;
-    if (off_ring + 2 * stage > budget) return false;
+    if (off_ring + 2 * stage > budget) {
+        // no room for the bf16 staging copy: widen straight from global memory
+        stg_global = 1;
+        off_tab = 0;
+        off_meta = (tabb + 127) & ~size_t(127);
+        off_ring = off_meta + ((nchunk * 8 + 1023) & ~size_t(1023));
+        if (off_ring + 2 * stage > budget) return false;
+    }
     uint32_t nst = uint32_t((budget - off_ring) / stage);
     if (nst > 8) nst = 8;
     // work items: planes split into row ranges (multiples of R) until every
@@ -587,7 +595,7 @@ static bool plan(bool quant, int64_t P, int64_t N, int d, int S, int K, int bits
     g = Geo{uint32_t(P), uint32_t(N), uint32_t(d), uint32_t(K), R, nst, pitch, uint32_t(tbytes),
             uint32_t(nchunk), uint32_t(ilog2i(n)), uint32_t(ipp), uint32_t(rpi), uint32_t(P * ipp),
             uint32_t(off_tab), uint32_t(off_meta), uint32_t(off_ring), uint32_t(stage), big_row, small_row,
-            uint32_t(big), 0u};
+            uint32_t(big), 0u, stg_global};
     if (const char *e = getenv("QVG_STREAM_DBG")) g.dbg = uint32_t(atoi(e));
     if (const char *e = getenv("QVG_STREAM_NST")) { const uint32_t v = uint32_t(atoi(e)); if (v >= 2 && v < nst) nst = v; g.nst = nst; }
     smem = off_ring + nst * stage;

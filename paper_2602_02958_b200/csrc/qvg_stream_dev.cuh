@@ -28,6 +28,7 @@ struct Geo {
     uint32_t small_row;    // scale bytes per row in the stage (K6), 0 for K5
     uint32_t off_small;    // offset of the small streams inside a stage
     uint32_t dbg;          // QVG_STREAM_DBG: 1 = consumers only drain the ring (measurement)
+    uint32_t stg_global;   // 1: tables widened from global memory (no smem staging copy)
 };
 
 // padded f32 table: 16-channel block c of a row at float 16c + 4(c>>1), which
