@@ -128,7 +128,8 @@ __device__ __forceinline__ void split3(double x, uint16_t &hi, uint16_t &mid, ui
 // ---------------------------------------------------------------------------
 // rows [P][N][128] f64 -> [P][T][3][128x128 UMMA tile] bf16 + row norms
 // ---------------------------------------------------------------------------
-__global__ void k_split_rows(const double *rows, uint16_t *split, float *xnorm, int64_t P, int64_t N, int T) {
+__global__ void k_split_rows(const double *rows, uint16_t *split, float *xnorm, float *rows32, int32_t *rows32_ok,
+                             int64_t P, int64_t N, int T) {
     // one thread = 8 channels (one 16-byte chunk of the tile) of one row
     const int64_t total = P * int64_t(T) * kM * (kD / 8);
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
@@ -143,12 +144,20 @@ __global__ void k_split_rows(const double *rows, uint16_t *split, float *xnorm, 
         double ss = 0.0;
         if (row < N) {
             const double *src = rows + (p * N + row) * kD + ch * 8;
+            float f[8];
+            bool exact = true;
 #pragma unroll
             for (int k = 0; k < 8; k++) {
                 const double x = src[k];
                 ss = fma(x, x, ss);
                 split3(x, v[0][k], v[1][k], v[2][k]);
+                f[k] = float(x);
+                exact &= double(f[k]) == x;
             }
+            float4 *dst32 = reinterpret_cast<float4 *>(rows32 + (p * N + row) * kD + ch * 8);
+            dst32[0] = make_float4(f[0], f[1], f[2], f[3]);
+            dst32[1] = make_float4(f[4], f[5], f[6], f[7]);
+            if (!exact) rows32_ok[p] = 0;
         } else {
 #pragma unroll
             for (int k = 0; k < 8; k++) v[0][k] = v[1][k] = v[2][k] = 0;
@@ -382,12 +391,14 @@ size_t assign_tc_split_elems(int64_t P, int64_t N) {
 
 bool assign_tc_ok(int d, int K) { return d == atc::kD && K >= 1 && K <= 256; }
 
-int launch_split_rows(const double *rows, uint16_t *split, float *xnorm, int64_t P, int64_t N, cudaStream_t st) {
+int launch_split_rows(const double *rows, uint16_t *split, float *xnorm, float *rows32, int32_t *rows32_ok,
+                      int64_t P, int64_t N, cudaStream_t st) {
     const int T = int((N + atc::kM - 1) / atc::kM);
+    cudaMemsetAsync(rows32_ok, 1, size_t(P) * sizeof(int32_t), st);      // nonzero = exact until shown otherwise
     const int64_t total = P * T * atc::kM * (atc::kD / 8);
     int64_t g = (total + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
-    atc::k_split_rows<<<unsigned(g), 256, 0, st>>>(rows, split, xnorm, P, N, T);
+    atc::k_split_rows<<<unsigned(g), 256, 0, st>>>(rows, split, xnorm, rows32, rows32_ok, P, N, T);
     return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
 }
 

@@ -134,6 +134,8 @@ static void carve_kmeans(Carver &c, int64_t P, int64_t N, int d, int K, bool own
         b.c2 = c.take<double>(P * K);
         b.recheck = c.take<int32_t>(P * N);
         b.n_recheck = c.take<int32_t>(8);
+        b.rows32 = c.take<float>(P * N * d);
+        b.rows32_ok = c.take<int32_t>(P);
     }
 }
 

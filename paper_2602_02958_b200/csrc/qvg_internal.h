@@ -30,6 +30,9 @@ struct KMeansBuffers {
     float *xnorm;          // [P][N] row norms
     double *c2;            // [P][K] exact centroid squared norms
     int32_t *recheck, *n_recheck;
+    float *rows32;         // [P][N][d] float32 copy of the stage rows (k_split_rows)
+    int32_t *rows32_ok;    // [P] nonzero: the copy is exact for the whole plane
+    int rows32_valid;      // set once k_split_rows has filled rows32 for the current rows
 };
 
 // qvg_codec.cu
@@ -47,7 +50,7 @@ int launch_unpack(const uint8_t *in, int64_t n, int bits, int8_t *out, cudaStrea
 int launch_widen(const void *x, int xbf16, double *rows, int64_t n, int32_t *status, cudaStream_t st);
 int run_kmeanspp(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, const double *draws,
                  int64_t draws_stride, cudaStream_t st);
-int run_kmeans_stage(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int max_iters,
+int run_kmeans_stage(KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int max_iters,
                      double tol, const double *draws_stage, int64_t draws_stride, bool warm,
                      cudaStream_t st);
 int kmeans_outputs(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, uint8_t *assign,
@@ -65,7 +68,8 @@ int run_add_back(const double *residual, const uint16_t *cent, const uint8_t *as
 // qvg_assign_tc.cu
 size_t assign_tc_split_elems(int64_t P, int64_t N);
 bool assign_tc_ok(int d, int K);
-int launch_split_rows(const double *rows, uint16_t *split, float *xnorm, int64_t P, int64_t N, cudaStream_t st);
+int launch_split_rows(const double *rows, uint16_t *split, float *xnorm, float *rows32, int32_t *rows32_ok,
+                      int64_t P, int64_t N, cudaStream_t st);
 int launch_assign_tc(const uint16_t *split, const float *xnorm, const double *rows, const double *cent,
                      const double *c2, int32_t *assign, int32_t *recheck, int32_t *n_recheck,
                      const PlaneState *st_planes, int skip_done, int64_t P, int64_t N, int K, cudaStream_t st);

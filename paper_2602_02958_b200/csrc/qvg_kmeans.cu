@@ -85,6 +85,8 @@ __global__ void k_widen(const void *x, int xbf16, double *rows, int64_t n, int32
 // ------------------------------------------------------------------------
 struct PPArgs {
     const double *rows;      // [P][N][d]
+    const float *rows32;     // [P][N][d] float32 copy (nullable)
+    const int32_t *rows32_ok;   // [P] 1: the copy is exact
     const double *draws;     // this stage's draws of plane 0; plane p at + p*draws_stride
     int64_t draws_stride;
     double *cent;            // [P][K][d]
@@ -96,8 +98,10 @@ struct PPArgs {
     int d, K;
 };
 
-__global__ void __launch_bounds__(1024) k_kmeanspp(PPArgs a) {
-    extern __shared__ double sm[];
+// rows read as T (double, or float when the plane's float64 rows are all exactly
+// representable in float32, see k_split_rows): identical values, half the bytes
+template <typename T>
+__device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const T *rows_all, double *sm) {
     double *xc = sm;                       // [d]
     double *leaf = sm + 128;               // [n_leaves]
     __shared__ double s_total;
@@ -107,7 +111,7 @@ __global__ void __launch_bounds__(1024) k_kmeanspp(PPArgs a) {
     const int64_t p = blockIdx.x;
     const int64_t N = a.N;
     const int d = a.d, K = a.K;
-    const double *rows = a.rows + p * N * d;
+    const T *rows = rows_all + p * N * d;
     double *d2 = a.d2 + p * N;
     double *cent = a.cent + p * int64_t(K) * d;
     const double *draws = a.draws + p * a.draws_stride;
@@ -122,23 +126,58 @@ __global__ void __launch_bounds__(1024) k_kmeanspp(PPArgs a) {
     for (int pk = 0; pk < K; pk++) {
         const int64_t c = s_pick;
         for (int k = tid; k < d; k += blockDim.x) {
-            double v = rows[c * d + k];
+            double v = double(rows[c * d + k]);
             xc[k] = v;
             cent[int64_t(pk) * d + k] = v;
         }
         __syncthreads();
         if (pk == K - 1) break;
         // d2 = min(d2, ((rows - rows[c])**2).sum(axis=1))
-        for (int64_t i0 = int64_t(warp) * 4; i0 < N; i0 += blockDim.x >> 3) {  // warp-uniform
-            const int64_t i = i0 + (lane >> 3);
-            const int64_t ii = i < N ? i : N - 1;
-            const double *ri = rows + ii * d;
-            double dist = row_pairwise8(d, j8, [&](int k) {
-                double t = __dsub_rn(ri[k], xc[k]);
-                return __dmul_rn(t, t);
-            });
-            dist = __dadd_rn(0.0, dist);
-            if (j8 == 0 && i < N) d2[i] = (pk == 0 || dist < d2[i]) ? dist : d2[i];
+        if (d == 128) {
+            // head_dim 128: all 16 loads of a lane issued before the (ordered) sums,
+            // two rows per 8-lane group in flight
+            double xcl[16];
+#pragma unroll
+            for (int q = 0; q < 16; q++) xcl[q] = xc[q * 8 + j8];
+            const int64_t step = blockDim.x >> 3;                      // rows per CTA pass
+            for (int64_t i0 = int64_t(warp) * 4; i0 < N; i0 += 2 * step) {   // warp-uniform
+                const int64_t ia = i0 + (lane >> 3), ib = ia + step;
+                const T *ra = rows + (ia < N ? ia : N - 1) * 128 + j8;
+                const T *rb = rows + (ib < N ? ib : N - 1) * 128 + j8;
+                double va[16], vb[16];
+#pragma unroll
+                for (int q = 0; q < 16; q++) { va[q] = double(ra[q * 8]); vb[q] = double(rb[q * 8]); }
+                double sa, sb;
+                {
+                    double t = __dsub_rn(va[0], xcl[0]);
+                    sa = __dmul_rn(t, t);
+                    t = __dsub_rn(vb[0], xcl[0]);
+                    sb = __dmul_rn(t, t);
+                }
+#pragma unroll
+                for (int q = 1; q < 16; q++) {
+                    double t = __dsub_rn(va[q], xcl[q]);
+                    sa = __dadd_rn(sa, __dmul_rn(t, t));
+                    t = __dsub_rn(vb[q], xcl[q]);
+                    sb = __dadd_rn(sb, __dmul_rn(t, t));
+                }
+                sa = __dadd_rn(0.0, pairwise8_tree(sa));
+                sb = __dadd_rn(0.0, pairwise8_tree(sb));
+                if (j8 == 0 && ia < N) d2[ia] = (pk == 0 || sa < d2[ia]) ? sa : d2[ia];
+                if (j8 == 0 && ib < N) d2[ib] = (pk == 0 || sb < d2[ib]) ? sb : d2[ib];
+            }
+        } else {
+            for (int64_t i0 = int64_t(warp) * 4; i0 < N; i0 += blockDim.x >> 3) {  // warp-uniform
+                const int64_t i = i0 + (lane >> 3);
+                const int64_t ii = i < N ? i : N - 1;
+                const T *ri = rows + ii * d;
+                double dist = row_pairwise8(d, j8, [&](int k) {
+                    double t = __dsub_rn(double(ri[k]), xc[k]);
+                    return __dmul_rn(t, t);
+                });
+                dist = __dadd_rn(0.0, dist);
+                if (j8 == 0 && i < N) d2[i] = (pk == 0 || dist < d2[i]) ? dist : d2[i];
+            }
         }
         __syncthreads();
         // total = weights.sum() : leaves then numpy recursion
@@ -186,7 +225,7 @@ __global__ void __launch_bounds__(1024) k_kmeanspp(PPArgs a) {
             if (lane == 31) s_wsum[warp] = incl;
             __syncthreads();
             if (warp == 0) {
-                double w = s_wsum[lane];
+                double w = lane < int(blockDim.x >> 5) ? s_wsum[lane] : 0.0;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
                     double t = __shfl_up_sync(0xffffffffu, w, o);
@@ -205,7 +244,7 @@ __global__ void __launch_bounds__(1024) k_kmeanspp(PPArgs a) {
             }
             cnt += __syncthreads_count(le);
             amb |= __syncthreads_or(am) != 0;
-            if (tid == 0) s_base = s_base + s_wsum[31];
+            if (tid == 0) s_base = s_base + s_wsum[(blockDim.x >> 5) - 1];
             __syncthreads();
         }
         if (tid == 0) {
@@ -224,6 +263,13 @@ __global__ void __launch_bounds__(1024) k_kmeanspp(PPArgs a) {
         }
         __syncthreads();
     }
+}
+
+
+__global__ void __launch_bounds__(1024) k_kmeanspp(PPArgs a) {
+    extern __shared__ double sm[];
+    if (a.rows32 && a.rows32_ok[blockIdx.x]) kmeanspp_body<float>(a, a.rows32, sm);
+    else kmeanspp_body<double>(a, a.rows, sm);
 }
 
 // ------------------------------------------------------------------------
@@ -665,7 +711,7 @@ static void assign_step(const KMeansBuffers &b, int64_t P, int64_t N, int d, int
 
 int run_kmeanspp(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, const double *draws,
                  int64_t draws_stride, cudaStream_t st) {
-    PPArgs pa{b.rows, draws, draws_stride, b.cent, b.d2, b.pk_off, b.pk_len, b.pk_leaves, N, d, K};
+    PPArgs pa{b.rows, b.rows32_valid ? b.rows32 : nullptr, b.rows32_ok, draws, draws_stride, b.cent, b.d2, b.pk_off, b.pk_len, b.pk_leaves, N, d, K};
     size_t smem = sizeof(double) * (128 + b.pk_leaves);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_kmeanspp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -690,13 +736,16 @@ static void lloyd_body(const KMeansBuffers &b, int64_t P, int64_t N, int d, int 
 
 // One SAS stage's k-means for all planes (Q/clustering.py:110-160); leaves
 // the final assignment in b.assign and the iteration count in b.st.
-int run_kmeans_stage(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int max_iters,
+int run_kmeans_stage(KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int max_iters,
                      double tol, const double *draws_stage, int64_t draws_stride, bool warm,
                      cudaStream_t st) {
     k_stage_reset<<<g1d(P, 256), 256, 0, st>>>(b.st, P);
     // the rows are fixed for the whole stage: split them once for the tensor-core assignment
-    if (b.rsplit && assign_tc_enabled() && launch_split_rows(b.rows, b.rsplit, b.xnorm, P, N, st))
-        return QVG_ERR_CUDA;
+    b.rows32_valid = 0;
+    if (b.rsplit && assign_tc_enabled()) {
+        if (launch_split_rows(b.rows, b.rsplit, b.xnorm, b.rows32, b.rows32_ok, P, N, st)) return QVG_ERR_CUDA;
+        b.rows32_valid = 1;
+    }
     if (!warm && run_kmeanspp(b, P, N, d, K, draws_stage, draws_stride, st)) return QVG_ERR_CUDA;
     // objective of the starting centroids (Q/clustering.py:142-143)
     assign_step(b, P, N, d, K, 0, st);
