@@ -203,6 +203,22 @@ QVG_API int qvg_attention(const uint16_t *q, const uint8_t *payload, const uint8
                   const qvg_config *cfg /* host */, float softmax_scale, uint16_t *out,
                   void *workspace, size_t workspace_bytes, void *stream);
 
+/* Baseline competitors (Q/baselines.py), composed with qvg_quantize /
+ * qvg_dequantize at S = 0 (= RTN, Q/baselines.py:20-42):
+ *  - qvg_hadamard replaces hadamard_transform / inverse_hadamard
+ *    (Q/baselines.py:148-164) for n_rows rows of d (power of two, 32..1024):
+ *    out = fwht(x * signs) / sqrt_d (inverse = 0) or fwht(x) / sqrt_d * signs
+ *    (inverse = 1), float64 butterflies in numpy's order, stored as f64
+ *    (the reference's return value) or rounded to f32 (out_dtype); signs [d]
+ *    f32 +-1 (random_signs, host), sqrt_d = np.sqrt(d).
+ *  - qvg_token_transpose builds the KIVI key path's transposed plane
+ *    (Q/baselines.py:60-73): [P][N][d] -> [P][d][n_padded] f32 with zero
+ *    pad rows (inverse = 1: [P][d][n_padded] f32 -> [P][N][d] f32). */
+QVG_API int qvg_hadamard(const void *x, int32_t x_dtype, int64_t n_rows, int32_t d, const float *signs,
+                         double sqrt_d, int32_t inverse, void *out, int32_t out_dtype, void *stream);
+QVG_API int qvg_token_transpose(const void *x, int32_t x_dtype, int64_t n_planes, int64_t n_tokens,
+                                int64_t n_padded, int32_t d, int32_t inverse, float *out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

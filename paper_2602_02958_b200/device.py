@@ -385,3 +385,103 @@ def attention(q: torch.Tensor, cache: Optional[DeviceChunks], k_cur: torch.Tenso
         _ptr(k_cur), _ptr(v_cur), nq, nc, ncur, H, d, cp, scale, _ptr(out), _ptr(ws), nbytes,
         _stream(q.device)))
     return out
+
+
+# ---------------------------------------------------------------------------
+# baseline competitors (Q/baselines.py) on the device
+# ---------------------------------------------------------------------------
+
+def random_signs(d: int, seed: int) -> np.ndarray:
+    """Seeded +-1 diagonal of the QuaRot rotation (Q/baselines.py:126-129):
+    host Philox draws, data-independent, as the reference."""
+    rng = np.random.Generator(np.random.Philox(seed))
+    return np.where(rng.random(d) < 0.5, -1.0, 1.0).astype(np.float32)
+
+
+def hadamard(x: torch.Tensor, signs: Union[np.ndarray, torch.Tensor], inverse: bool = False,
+             out_dtype=torch.float32) -> torch.Tensor:
+    """Rows of x [..., d] (f32/bf16) through the seeded Hadamard rotation:
+    fwht(x * signs) / sqrt(d) (hadamard_transform, Q/baselines.py:148) or its
+    inverse fwht(x) / sqrt(d) * signs (Q/baselines.py:159), float64
+    butterflies in numpy's order, returned as float64 (the reference's value)
+    or rounded to float32."""
+    _require_cuda(x)
+    d = x.shape[-1]
+    s = torch.as_tensor(np.asarray(signs, dtype=np.float32) if not torch.is_tensor(signs) else signs,
+                        dtype=torch.float32).to(x.device).contiguous()
+    if s.numel() != d:
+        from .qvgcodec.errors import DimensionMismatch
+        raise DimensionMismatch("signs length != row length")
+    out = torch.empty(x.shape, dtype=out_dtype, device=x.device)
+    odt = _lib.DTYPE_F64 if out_dtype == torch.float64 else _lib.DTYPE_F32
+    _lib.check(_lib.load().qvg_hadamard(_ptr(x), _x_dtype(x), x.numel() // d, d, _ptr(s),
+                                        float(np.sqrt(d)), int(bool(inverse)), _ptr(out), odt,
+                                        _stream(x.device)))
+    return out
+
+
+def token_transpose(x: torch.Tensor, group_size: int):
+    """[P, N, d] -> ([P, d, N + pad] float32, pad): the KIVI key path's
+    transposed plane with the final partial token group zero-padded
+    (Q/baselines.py:60-73)."""
+    _require_cuda(x)
+    P, N, d = x.shape
+    pad = (-N) % group_size
+    out = torch.empty((P, d, N + pad), dtype=torch.float32, device=x.device)
+    _lib.check(_lib.load().qvg_token_transpose(_ptr(x), _x_dtype(x), P, N, N + pad, d, 0, _ptr(out),
+                                               _stream(x.device)))
+    return out, pad
+
+
+def token_untranspose(y: torch.Tensor, n_tokens: int) -> torch.Tensor:
+    """[P, d, Np] float32 -> [P, n_tokens, d] float32 (Q/baselines.py:84-88)."""
+    _require_cuda(y)
+    P, d, Np = y.shape
+    out = torch.empty((P, n_tokens, d), dtype=torch.float32, device=y.device)
+    _lib.check(_lib.load().qvg_token_transpose(_ptr(y), _lib.DTYPE_F32, P, n_tokens, Np, d, 1, _ptr(out),
+                                               _stream(y.device)))
+    return out
+
+
+def _rtn(bits: int, group_size: int) -> QuantConfig:
+    return QuantConfig(bits=bits, group_size=group_size, stages=0, centroids=1)
+
+
+def rtn_quantize(x: torch.Tensor, bits: int, group_size: int):
+    """RTN (Q/baselines.py:24-27): the group quantizer with no smoothing."""
+    return quantize(x, _rtn(bits, group_size))
+
+
+def rtn_dequantize(payload: torch.Tensor, scales: torch.Tensor, n_tokens: int, head_dim: int, bits: int,
+                   group_size: int, out_dtype=torch.float32) -> torch.Tensor:
+    return dequantize(DeviceChunks(_rtn(bits, group_size), n_tokens, head_dim, payload, scales, None, None),
+                      out_dtype)
+
+
+def quarot_quantize(x: torch.Tensor, bits: int, group_size: int, seed: int):
+    """QuaRot (Q/baselines.py:177-194): rotate every row, round to float32,
+    then RTN.  Returns (payload, scales)."""
+    rot = hadamard(x, random_signs(x.shape[-1], seed))
+    return quantize(rot, _rtn(bits, group_size))
+
+
+def quarot_dequantize(payload: torch.Tensor, scales: torch.Tensor, n_tokens: int, head_dim: int, bits: int,
+                      group_size: int, seed: int) -> torch.Tensor:
+    """Q/baselines.py:197-202: RTN decode, inverse rotation, float32."""
+    rot = rtn_dequantize(payload, scales, n_tokens, head_dim, bits, group_size)
+    return hadamard(rot, random_signs(head_dim, seed), inverse=True)
+
+
+def token_axis_quantize(x: torch.Tensor, bits: int, group_size: int):
+    """KIVI key path (Q/baselines.py:60-73): groups of consecutive tokens per
+    channel.  Returns (payload, scales, pad)."""
+    t, pad = token_transpose(x, group_size)
+    pay, sc = quantize(t, _rtn(bits, group_size))
+    return pay, sc, pad
+
+
+def token_axis_dequantize(payload: torch.Tensor, scales: torch.Tensor, n_tokens: int, head_dim: int, bits: int,
+                          group_size: int) -> torch.Tensor:
+    pad = (-n_tokens) % group_size
+    t = rtn_dequantize(payload, scales, head_dim, n_tokens + pad, bits, group_size)
+    return token_untranspose(t, n_tokens)
