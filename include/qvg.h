@@ -203,6 +203,21 @@ QVG_API int qvg_attention(const uint16_t *q, const uint8_t *payload, const uint8
                   const qvg_config *cfg /* host */, float softmax_scale, uint16_t *out,
                   void *workspace, size_t workspace_bytes, void *stream);
 
+/* qvg_attention with PRE-RoPE cached keys: the
+ * cache holds keys before the rotary embedding; after the reconstruction
+ * each cached key row t is rotated with rope_cos / rope_sin [n_cache][d/2]
+ * (f32, the caller's positions / frequencies — any 1-D or 3-D RoPE layout):
+ * rope_mode 1 = rotate-half pairs (i, i + d/2), 2 = interleaved (2i, 2i+1);
+ * 0 = none (== qvg_attention).  q and k_cur are expected post-RoPE.  Needs
+ * the reconstruction workspace (also for the bf16 comparator, kv_bf16). */
+QVG_API int qvg_attention_rope(const uint16_t *q, const uint8_t *payload, const uint8_t *scales,
+                               const uint16_t *centroids, const uint8_t *assign, const uint16_t *kv_bf16,
+                               const uint16_t *k_cur, const uint16_t *v_cur, int64_t nq, int64_t n_cache,
+                               int64_t n_cur, int32_t n_heads, int32_t head_dim, const qvg_config *cfg,
+                               float softmax_scale, const float *rope_cos, const float *rope_sin,
+                               int32_t rope_mode, uint16_t *out, void *workspace, size_t workspace_bytes,
+                               void *stream);
+
 /* Baseline competitors (Q/baselines.py), composed with qvg_quantize /
  * qvg_dequantize at S = 0 (= RTN, Q/baselines.py:20-42):
  *  - qvg_hadamard replaces hadamard_transform / inverse_hadamard

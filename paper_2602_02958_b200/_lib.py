@@ -77,6 +77,8 @@ _SIGS = {
     "qvg_attention_workspace_size": (_SZ, [_I64, _I64, _I64, _I32, _I32, _CFG]),
     "qvg_attention": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _CFG,
                              ctypes.c_float, _P, _P, _SZ, _P]),
+    "qvg_attention_rope": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _CFG,
+                                  ctypes.c_float, _P, _P, _I32, _P, _P, _SZ, _P]),
     "qvg_hadamard": (_I32, [_P, _I32, _I64, _I32, _P, _D, _I32, _P, _I32, _P]),
     "qvg_token_transpose": (_I32, [_P, _I32, _I64, _I64, _I64, _I32, _I32, _P, _P]),
 }

@@ -1289,6 +1289,53 @@ static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const 
 }
 }  // namespace attn4
 
+// ============================================================================
+// pre-RoPE key caching: the cache stores keys BEFORE the
+// rotary embedding; after the K6 reconstruction the K planes are rotated in
+// place with the caller's per-position tables (any 1-D / 3-D RoPE layout
+// reduces to cos/sin [n_cache][d/2]): mode 1 = rotate-half pairs (i, i+d/2),
+// mode 2 = interleaved pairs (2i, 2i+1).  fp32 math, bf16 RNE store.
+// ============================================================================
+__global__ void k_rope_kplanes(uint16_t *kv, int64_t H, int64_t n, int d, const float *cosv, const float *sinv,
+                               int mode, const uint16_t *src) {
+    const int half = d / 2;
+    const int64_t total = H * n * half;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int i = int(e % half);
+        const int64_t hn = e / half;
+        const int64_t h = hn / n, t = hn - h * n;
+        const int64_t base = ((2 * h) * n + t) * d;           // K plane of head h, token t
+        const int i0 = mode == 1 ? i : 2 * i, i1 = mode == 1 ? i + half : 2 * i + 1;
+        const uint16_t *in = src ? src : kv;
+        const float a = bf16_to_f32(in[base + i0]), b = bf16_to_f32(in[base + i1]);
+        const float c = cosv[t * half + i], sn = sinv[t * half + i];
+        kv[base + i0] = f32_to_bf16_bits_rne(__fsub_rn(__fmul_rn(a, c), __fmul_rn(b, sn)));
+        kv[base + i1] = f32_to_bf16_bits_rne(__fadd_rn(__fmul_rn(a, sn), __fmul_rn(b, c)));
+    }
+}
+
+// copy of the V planes of a bf16 cache into the workspace (the comparator
+// path with RoPE: K is rotated out of place, V copied beside it)
+__global__ void k_copy_vplanes(const uint16_t *src, uint16_t *dst, int64_t H, int64_t n, int d) {
+    const int64_t per = n * d, total = H * per;
+    for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t h = e / per, r = e - h * per;
+        dst[(2 * h + 1) * per + r] = src[(2 * h + 1) * per + r];
+    }
+}
+
+int run_rope_cache(uint16_t *ws_kv, const uint16_t *src_kv, int64_t H, int64_t n, int d, const float *cosv,
+                   const float *sinv, int mode, cudaStream_t st) {
+    const int64_t total = H * n * (d / 2);
+    int64_t g = (total + 255) / 256;
+    if (g > 148 * 16) g = 148 * 16;
+    if (src_kv) {
+        k_copy_vplanes<<<unsigned(g), 256, 0, st>>>(src_kv, ws_kv, H, n, d);
+    }
+    k_rope_kplanes<<<unsigned(g), 256, 0, st>>>(ws_kv, H, n, d, cosv, sinv, mode, src_kv);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+
 size_t attention_workspace_size(int64_t, int64_t n_cache, int64_t, int H, int d, const qvg_config *) {
     // bf16 reconstruction of the quantized cache (2H planes) for the TMA kernel
     return n_cache > 0 ? size_t(2) * H * n_cache * d * 2 + 256 : 0;
@@ -1298,12 +1345,17 @@ int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scal
                   const uint16_t *cent, const uint8_t *assign, const uint16_t *kv_bf16,
                   const uint16_t *k_cur, const uint16_t *v_cur, int64_t nq, int64_t n_cache,
                   int64_t n_cur, int H, int d, const qvg_config *cfg, float scale, uint16_t *out,
-                  void *workspace, size_t wbytes, cudaStream_t st) {
+                  void *workspace, size_t wbytes, cudaStream_t st, const float *rope_cos,
+                  const float *rope_sin, int rope_mode) {
     using namespace attn;
     if (d != kD) return set_err(QVG_ERR_UNSUPPORTED, "attention kernel supports head_dim 128, got %d", d);
     if (n_cur > 0 && (!k_cur || !v_cur)) return set_err(QVG_ERR_BAD_CONFIG, "k_cur/v_cur are NULL");
     const float sl2 = scale * 1.4426950408889634f;
     const uint16_t *kv = kv_bf16;
+    if (rope_mode && (!rope_cos || !rope_sin || d % 2 || rope_mode > 2))
+        return set_err(QVG_ERR_BAD_CONFIG, "rope needs cos/sin tables [n_cache][d/2] and mode 1 or 2");
+    if (rope_mode && n_cache > 0 && payload && !workspace)
+        return set_err(QVG_ERR_WORKSPACE, "pre-RoPE keys need the reconstruction workspace");
     if (n_cache > 0 && payload && !workspace) {
         // no workspace: the fused kernel dequantizes codes/scales/centroids in-tile
         if (cfg->group_size % 8 != 0 || kD % cfg->group_size != 0)
@@ -1324,6 +1376,16 @@ int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scal
                                    cfg->group_size, cfg->stages, cfg->centroids, rec, QVG_DTYPE_BF16,
                                    status, st);
         if (rc) return set_err(rc, "cache reconstruction failed");
+        kv = rec;
+        if (rope_mode && run_rope_cache(rec, nullptr, H, n_cache, d, rope_cos, rope_sin, rope_mode, st))
+            return set_err(QVG_ERR_CUDA, "rope launch failed");
+    } else if (n_cache > 0 && kv && rope_mode) {
+        // bf16 comparator with pre-RoPE keys: rotated copy in the workspace
+        const size_t need = attention_workspace_size(nq, n_cache, n_cur, H, d, cfg);
+        if (!workspace || wbytes < need) return set_err(QVG_ERR_WORKSPACE, "rope needs %zu workspace bytes", need);
+        uint16_t *rec = static_cast<uint16_t *>(workspace);
+        if (run_rope_cache(rec, kv, H, n_cache, d, rope_cos, rope_sin, rope_mode, st))
+            return set_err(QVG_ERR_CUDA, "rope launch failed");
         kv = rec;
     } else if (n_cache > 0 && !kv) {
         return set_err(QVG_ERR_BAD_CONFIG, "cache is NULL");

@@ -346,7 +346,7 @@ def attention(q: torch.Tensor, cache: Optional[DeviceChunks], k_cur: torch.Tenso
               v_cur: torch.Tensor, softmax_scale: Optional[float] = None,
               kv_bf16: Optional[torch.Tensor] = None,
               out: Optional[torch.Tensor] = None, fused: bool = False,
-              workspace: Optional[torch.Tensor] = None) -> torch.Tensor:
+              workspace: Optional[torch.Tensor] = None, rope=None) -> torch.Tensor:
     """O = softmax(q [Khat; k_cur]^T * scale) [Vhat; v_cur] per head.
 
     q [Nq, H, d] bf16; cache: 2H planes (plane 2h = K of head h, 2h+1 = V)
@@ -354,6 +354,9 @@ def attention(q: torch.Tensor, cache: Optional[DeviceChunks], k_cur: torch.Tenso
     fused=True dequantizes the cache inside the attention kernel (no bf16
     staging buffer); the default reconstructs it to bf16 in a workspace with the
     HBM-bound decoder and runs the pipelined TMA/tcgen05 kernel.
+    rope=(cos, sin, "rotate_half"|"interleaved") marks the cached keys as
+    pre-RoPE: the reconstructed keys are rotated with cos/sin [n_cache, d/2]
+    (float32, CUDA) before the attention; q and k_cur are post-RoPE.
     """
     _require_cuda(q, k_cur, v_cur, kv_bf16, out)
     nq, H, d = q.shape
@@ -379,11 +382,23 @@ def attention(q: torch.Tensor, cache: Optional[DeviceChunks], k_cur: torch.Tenso
             torch.empty(max(n, 1), dtype=torch.uint8, device=q.device)
         nbytes = ws.numel()
     c = cache
-    _lib.check(lib.qvg_attention(
+    if rope is None:
+        _lib.check(lib.qvg_attention(
+            _ptr(q), _ptr(c.payload if c else None), _ptr(c.scales if c else None),
+            _ptr(c.centroids if c else None), _ptr(c.assignments if c else None), _ptr(kv_bf16),
+            _ptr(k_cur), _ptr(v_cur), nq, nc, ncur, H, d, cp, scale, _ptr(out), _ptr(ws), nbytes,
+            _stream(q.device)))
+        return out
+    cos_t, sin_t, mode = rope
+    _require_cuda(cos_t, sin_t)
+    if ws is None:
+        ws = torch.empty(max(n, 1), dtype=torch.uint8, device=q.device)
+        nbytes = ws.numel()
+    _lib.check(lib.qvg_attention_rope(
         _ptr(q), _ptr(c.payload if c else None), _ptr(c.scales if c else None),
         _ptr(c.centroids if c else None), _ptr(c.assignments if c else None), _ptr(kv_bf16),
-        _ptr(k_cur), _ptr(v_cur), nq, nc, ncur, H, d, cp, scale, _ptr(out), _ptr(ws), nbytes,
-        _stream(q.device)))
+        _ptr(k_cur), _ptr(v_cur), nq, nc, ncur, H, d, cp, scale, _ptr(cos_t), _ptr(sin_t),
+        {"rotate_half": 1, "interleaved": 2}[mode], _ptr(out), _ptr(ws), nbytes, _stream(q.device)))
     return out
 
 

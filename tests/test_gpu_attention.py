@@ -120,3 +120,57 @@ def test_head_sharding_is_bit_identical():
             assert torch.equal(local_cache.payload, chunks.payload[2 * h0:2 * h1])
             local = D.attention(sl(q), local_cache, sl(kc), sl(vc))
             assert torch.equal(local, full[:, h0:h1])
+
+
+def _rope_np(k, cos, sin, mode):
+    """k [H, n, d] float64 rotated per position (the kernel's rule, bf16 store)."""
+    import torch as _t
+    half = k.shape[-1] // 2
+    if mode == "rotate_half":
+        a, b = k[..., :half], k[..., half:]
+    else:
+        a, b = k[..., 0::2], k[..., 1::2]
+    ra = a * cos - b * sin
+    rb = a * sin + b * cos
+    out = np.empty_like(k)
+    if mode == "rotate_half":
+        out[..., :half], out[..., half:] = ra, rb
+    else:
+        out[..., 0::2], out[..., 1::2] = ra, rb
+    return _t.from_numpy(out.astype(np.float32)).to(_t.bfloat16).float().numpy()
+
+
+@pytest.mark.parametrize("mode", ["rotate_half", "interleaved"])
+@pytest.mark.parametrize("quant", [True, False])
+def test_pre_rope_cached_keys_vs_oracle(oracle_lib, mode, quant):
+    """keys cached before RoPE, rotated after the decode."""
+    torch.manual_seed(3)
+    H, nq, nc, ncur, d = 2, 160, 320, 96, 128
+    cfg = QuantConfig(bits=2, group_size=64, stages=2, centroids=16)
+    pos = np.arange(nc, dtype=np.float64)[:, None]
+    freq = 10000.0 ** (-np.arange(d // 2, dtype=np.float64) / (d // 2))
+    cos = np.cos(pos * freq).astype(np.float32)
+    sin = np.sin(pos * freq).astype(np.float32)
+    q = (torch.randn(nq, H, d, device="cuda") * 0.5).to(torch.bfloat16)
+    kc = torch.randn(ncur, H, d, device="cuda").to(torch.bfloat16)
+    vc = torch.randn(ncur, H, d, device="cuda").to(torch.bfloat16)
+    planes = clustered_planes(2 * H, nc, d, n_clusters=16, outlier_scale=4.0, seed=2)
+    rope = (torch.from_numpy(cos).cuda(), torch.from_numpy(sin).cuda(), mode)
+    if quant:
+        chunks = D.compress(planes, cfg)
+        out = D.attention(q, chunks, kc, vc, d ** -0.5, rope=rope)
+        deq = oracle_lib.prq_decompress_batch(chunks.payload.cpu().numpy(), chunks.scales.cpu().numpy(),
+                                              chunks.centroids.float().cpu().numpy(),
+                                              chunks.assignments.cpu().numpy(), nc, d, cfg.bits,
+                                              cfg.group_size, 8)
+        kcache = torch.from_numpy(deq[0::2]).to(torch.bfloat16).double().numpy()
+        vcache = deq[1::2]
+    else:
+        out = D.attention(q, None, kc, vc, d ** -0.5, kv_bf16=planes, rope=rope)
+        pf = planes.float().cpu().numpy()
+        kcache, vcache = pf[0::2].astype(np.float64), pf[1::2]
+    torch.cuda.synchronize()
+    kr = _rope_np(kcache, cos.astype(np.float64), sin.astype(np.float64), mode)
+    ref = oracle_lib.attention(q.float().cpu().numpy(), kr, vcache, kc.float().cpu().numpy(),
+                               vc.float().cpu().numpy(), d ** -0.5, 8)
+    _check(out, ref)
