@@ -1542,18 +1542,23 @@ __global__ void __launch_bounds__(256, 2) k_quantize_v6(QuantArgs a, V6Plane pl)
 }
 
 // ------------------------------------------------------------------------
-// v5w: the v5 quantize with ONE 768-thread CTA per SM (24 warps, as v5's 3
-// CTAs) sharing double-buffered f32 centroid tables (padded, conflict-free
-// 16-channel blocks) widened once per plane from a TMA-staged bf16 copy: the
-// per-element bf16 -> f32 conversions of the centroids disappear.
+// v5w: the v5 quantize with ONE CTA per SM (32 warps by default) sharing
+// double-buffered f32 centroid tables (padded, conflict-free 16-channel
+// blocks) widened once per plane from a TMA-staged bf16 copy: the per-element
+// bf16 -> f32 conversions of the centroids disappear.  For bf16 inputs a
+// per-row exactness certificate (block {unit, max} metadata from the widen)
+// proves the f32 residual equals the reference's float64 one, which zeroes the
+// error bound: scale straddles at exact E4M3 grid hits vanish and exact ties
+// are resolved from registers instead of reloading x.
 // ------------------------------------------------------------------------
 struct V5W {
     uint32_t P, tbytes, off_tab, tab_floats, pitch, nchunk, lchunk;
     uint32_t nbuf;       // f32 table buffers (2, or 1 when two do not fit: one more barrier per plane)
+    uint32_t off_meta;   // per buffer: nchunk float2 {unit, max |c|} of each 16-channel block
 };
 __host__ __device__ __forceinline__ uint32_t v5w_blk(uint32_t c) { return 16u * c + 4u * (c >> 1); }
-__device__ __forceinline__ void v5w_widen(const uint16_t *stg, float *tab, uint32_t nchunk, uint32_t lchunk,
-                                          uint32_t pitch) {
+__device__ __forceinline__ void v5w_widen(const uint16_t *stg, float *tab, float2 *meta, uint32_t nchunk,
+                                          uint32_t lchunk, uint32_t pitch) {
     const uint32_t cmask = (1u << lchunk) - 1u;
     for (uint32_t q = threadIdx.x; q < nchunk; q += blockDim.x) {
         const uint4 *src = reinterpret_cast<const uint4 *>(stg + size_t(q) * 16);
@@ -1562,11 +1567,33 @@ __device__ __forceinline__ void v5w_widen(const uint16_t *stg, float *tab, uint3
         float4 *dst = reinterpret_cast<float4 *>(tab + size_t(q >> lchunk) * pitch + v5w_blk(q & cmask));
 #pragma unroll
         for (int jj = 0; jj < 4; jj++) dst[jj] = make_float4(c[4 * jj], c[4 * jj + 1], c[4 * jj + 2], c[4 * jj + 3]);
+        // {unit, max |c|}: unit = 2^(e-7), the ulp of a bf16 with the smallest
+        // non-zero magnitude's exponent (0 when that is not a normal float, +inf
+        // for an all-zero block); NaN/Inf make max non-finite
+        float mx = 0.f, mn = __int_as_float(0x7F800000);
+#pragma unroll
+        for (int k = 0; k < 16; k++) {
+            const float av = fabsf(c[k]);
+            mx = fmaxf(mx, av);
+            mn = av > 0.f ? fminf(mn, av) : mn;
+        }
+        float unit = mn;
+        if (mn != __int_as_float(0x7F800000)) {
+            const uint32_t eb = __float_as_uint(mn) & 0x7F800000u;
+            unit = eb > (7u << 23) ? __uint_as_float(eb - (7u << 23)) : 0.f;
+        }
+        meta[q] = make_float2(unit, mx);
     }
 }
+__device__ __forceinline__ float v5_min3_abs(float m, float a, float b) {
+    float t, d;
+    asm("min.f32 %0, %1, %2;" : "=f"(t) : "f"(fabsf(a)), "f"(fabsf(b)));
+    asm("min.f32 %0, %1, %2;" : "=f"(d) : "f"(m), "f"(t));
+    return d;
+}
 
-template <int BITS, int S, bool XBF16>
-__global__ void __launch_bounds__(768, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
+template <int BITS, int S, bool XBF16, int NT, int U, int C>
+__global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
     constexpr int QMAX = (1 << (BITS - 1)) - 1;
     constexpr int SS = S > 0 ? S : 1;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -1575,11 +1602,17 @@ __global__ void __launch_bounds__(768, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
     uint16_t *const stg = reinterpret_cast<uint16_t *>(smem);
     float *const tabs = reinterpret_cast<float *>(smem + pl.off_tab);
     const uint32_t d = uint32_t(a.d), N = a.N;
-    const uint32_t cc = threadIdx.x & ((1u << a.lvpr) - 1u);
-    const int col = int(cc) << 4;
-    const uint32_t coff = v5w_blk(cc);
-    const uint32_t rslot = threadIdx.x >> a.lvpr, rpp = 768u >> a.lvpr;
-    const int glanes = 1 << a.gshift;
+    // C = 16 or 32 channels per thread (one or two padded 16-channel blocks,
+    // contiguous in the table: v5w_blk(2c + 1) = v5w_blk(2c) + 16)
+    static_assert(C == 16 || C == 32, "channels per thread");
+    constexpr int NQ = C / 2, NW = BITS * C / 32;
+    constexpr uint32_t LC = C == 32 ? 1u : 0u;
+    const uint32_t lv = a.lvpr - LC;
+    const uint32_t cc = threadIdx.x & ((1u << lv) - 1u);
+    const int col = int(cc) * C;
+    const uint32_t coff = v5w_blk(cc << LC);
+    const uint32_t rslot = threadIdx.x >> lv, rpp = uint32_t(NT) >> lv;
+    const int glanes = 1 << (a.gshift - int(LC));
     const int lane = threadIdx.x & 31;
     bool nonfinite = false;
     if (threadIdx.x < 128) rcp_tab[threadIdx.x] = __frcp_rn(e4m3_decode_fast(threadIdx.x));
@@ -1594,10 +1627,11 @@ __global__ void __launch_bounds__(768, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
         // widen plane p's staged bf16 table into f32 buffer j&1 (the buffer was last
         // read two planes ago, before the previous plane's barrier), then restage
         float *const ct = tabs + (pl.nbuf == 2 ? (j & 1u) : 0u) * pl.tab_floats;
+        float2 *const mt = reinterpret_cast<float2 *>(smem + pl.off_meta) + (pl.nbuf == 2 ? (j & 1u) : 0u) * pl.nchunk;
         if (S > 0) {
             if (pl.nbuf == 1 && j > 0) __syncthreads();       // previous plane done with the only buffer
             mbar_wait(&bar, j & 1u);
-            v5w_widen(stg, ct, pl.nchunk, pl.lchunk, pl.pitch);
+            v5w_widen(stg, ct, mt, pl.nchunk, pl.lchunk, pl.pitch);
             __syncthreads();
             if (threadIdx.x == 0 && p + gridDim.x < pl.P) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1607,58 +1641,92 @@ __global__ void __launch_bounds__(768, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
         const uint64_t pN = uint64_t(p) * N;
         const uint8_t *xb = static_cast<const uint8_t *>(a.x) + pN * d * (XBF16 ? 2 : 4);
         const uint8_t *ap = a.asg + pN * S;
-        for (uint32_t i0 = 0; i0 < N; i0 += rpp * kUnroll) {
-            float r[kUnroll][16];
-            uint32_t ii[kUnroll];
-            int ai[kUnroll][SS];
+        for (uint32_t i0 = 0; i0 < N; i0 += rpp * U) {
+            float r[U][C];
+            uint32_t ii[U];
+            int ai[U][SS];
 #pragma unroll
-            for (int u = 0; u < kUnroll; u++) {
+            for (int u = 0; u < U; u++) {
                 const uint32_t i = i0 + u * rpp + rslot;
                 ii[u] = i < N ? i : N - 1;
                 load_x16<XBF16>(xb, ii[u] * d + col, r[u]);
+                if constexpr (C == 32) load_x16<XBF16>(xb, ii[u] * d + col + 16, r[u] + 16);
 #pragma unroll
                 for (int t = 0; t < S; t++) ai[u][t] = __ldg(ap + t * N + ii[u]);
             }
-            float eb[kUnroll], am[kUnroll];
+            float eb[U], am[U];
+            bool cert[U];
+            constexpr bool kCert = XBF16 && S > 0;
 #pragma unroll
-            for (int u = 0; u < kUnroll; u++) {
-                // e = sum_{t<S} max_k |r_t,k| + max_k |r_S,k| bounds every element's
-                // sum_t |r_t,k| (the error-bound input); the maxima propagate NaN, so a
-                // NaN/Inf in x or a centroid makes e non-finite: the finiteness check
+            for (int u = 0; u < U; u++) {
                 float2 *r2 = reinterpret_cast<float2 *>(r[u]);
-                float e = 0.f;
+                // bf16 x: certificate that every partial sum x - c_1 - ... is exact in
+                // f32 (all operands multiples of a power of two `unit`, every partial
+                // magnitude < 2^24 unit; the bound uses |x| <= |r_S| + sum |c_t| with a
+                // 2x margin) -- then r IS the reference's float64 residual: E = 0
+                float xmn = __int_as_float(0x7F800000);
+                if constexpr (kCert) {
+#pragma unroll
+                    for (int q = 0; q < NQ; q++) xmn = v5_min3_abs(xmn, r2[q].x, r2[q].y);
+                }
+                float e = 0.f, csum = 0.f, cun = __int_as_float(0x7F800000);
 #pragma unroll
                 for (int t = 0; t < S; t++) {
-                    const float4 *c4 = reinterpret_cast<const float4 *>(ct + uint32_t(t * a.K + ai[u][t]) * pl.pitch + coff);
+                    const uint32_t row = uint32_t(t * a.K + ai[u][t]);
+                    const float4 *c4 = reinterpret_cast<const float4 *>(ct + row * pl.pitch + coff);
 #pragma unroll
-                    for (int q = 0; q < 4; q++) {
+                    for (int q = 0; q < C / 4; q++) {
                         const float4 cv = c4[q];
                         r2[2 * q] = __fadd2_rn(r2[2 * q], make_float2(-cv.x, -cv.y));
                         r2[2 * q + 1] = __fadd2_rn(r2[2 * q + 1], make_float2(-cv.z, -cv.w));
                     }
-                    if (t < S - 1) {
+                    if constexpr (kCert) {
+                        if constexpr (C == 32) {
+                            const float4 m = reinterpret_cast<const float4 *>(mt)[(row << (pl.lchunk - 1)) + cc];
+                            cun = fminf(cun, fminf(m.x, m.z));
+                            csum = __fadd_ru(csum, fmaxf(m.y, m.w));
+                        } else {
+                            const float2 m = mt[(row << pl.lchunk) + cc];
+                            cun = fminf(cun, m.x);
+                            csum = __fadd_ru(csum, m.y);
+                        }
+                    } else if (t < S - 1) {
+                        // e = sum_{t<S} max_k |r_t,k| (+ max |r_S| below) bounds every
+                        // element's sum_t |r_t,k|, the error-bound input
                         float m = 0.f;
 #pragma unroll
-                        for (int q = 0; q < 8; q++) m = v5_max3_nan_abs(m, r2[q].x, r2[q].y);
+                        for (int q = 0; q < NQ; q++) m = v5_max3_nan_abs(m, r2[q].x, r2[q].y);
                         e = __fadd_ru(e, m);
                     }
                 }
+                // the maxima propagate NaN: a NaN/Inf in x or a centroid is caught here
                 float mx = 0.f;
 #pragma unroll
-                for (int q = 0; q < 8; q++) mx = v5_max3_nan_abs(mx, r2[q].x, r2[q].y);
+                for (int q = 0; q < NQ; q++) mx = v5_max3_nan_abs(mx, r2[q].x, r2[q].y);
+                if constexpr (kCert) {
+                    const uint32_t xe = __float_as_uint(xmn) & 0x7F800000u;
+                    const float unit = fminf(xe > (7u << 23) ? __uint_as_float(xe - (7u << 23)) : 0.f, cun);
+                    const float bnd = __fadd_ru(mx, __fmul_ru(csum, 2.f));
+                    cert[u] = bnd < unit * 8388608.f;
+                    // otherwise max |r_t| <= max |r_S| + sum_t' max |c_t'| for every t
+                    e = cert[u] ? 0.f : __fmul_ru(float(S), __fadd_ru(mx, csum));
+                    eb[u] = e;
+                } else {
+                    cert[u] = false;
+                    eb[u] = S > 0 ? __fadd_ru(e, mx) : 0.f;
+                }
                 nonfinite |= !(mx <= 3.402823466e38f) || !(e <= 3.402823466e38f);
-                eb[u] = S > 0 ? __fadd_ru(e, mx) : 0.f;
                 am[u] = mx;
             }
             for (int m = 1; m < glanes; m <<= 1) {
 #pragma unroll
-                for (int u = 0; u < kUnroll; u++) {
+                for (int u = 0; u < U; u++) {
                     am[u] = fmaxf(am[u], __shfl_xor_sync(0xffffffffu, am[u], m));
                     eb[u] = fmaxf(eb[u], __shfl_xor_sync(0xffffffffu, eb[u], m));
                 }
             }
 #pragma unroll
-            for (int u = 0; u < kUnroll; u++) {
+            for (int u = 0; u < U; u++) {
                 const bool valid = i0 + u * rpp + rslot < N;
                 const float E = __fmul_ru(eb[u], 2.38418579e-7f);
                 uint32_t code;
@@ -1677,14 +1745,24 @@ __global__ void __launch_bounds__(768, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
                 };
                 if (__any_sync(0xffffffffu, camb)) {          // exact scale (rare)
                     const float thr = __fsub_rd(am[u], __fmul_ru(E, 2.f));
-                    uint32_t cand = 0;
-#pragma unroll
-                    for (int k = 0; k < 16; k++) cand |= (camb && fabsf(r[u][k]) >= thr) ? 1u << k : 0u;
                     double a64 = 0.0;
-                    while (cand) {
-                        const int k = __ffs(cand) - 1;
-                        cand &= cand - 1;
-                        a64 = fmax(a64, fabs(exact_r(k)));
+                    if (camb) {
+                        if (cert[u]) {                          // the row's own exact maximum
+                            float m = 0.f;
+#pragma unroll
+                            for (int k = 0; k < C; k++) m = fmaxf(m, fabsf(r[u][k]));
+                            a64 = double(m);
+                        }
+                        else {
+                            uint32_t cand = 0;
+#pragma unroll
+                            for (int k = 0; k < C; k++) cand |= fabsf(r[u][k]) >= thr ? 1u << k : 0u;
+                            while (cand) {
+                                const int k = __ffs(cand) - 1;
+                                cand &= cand - 1;
+                                a64 = fmax(a64, fabs(exact_r(k)));
+                            }
+                        }
                     }
                     for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
                     if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
@@ -1698,12 +1776,12 @@ __global__ void __launch_bounds__(768, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
                 constexpr float MAGIC = 12582912.f + float(1 << (BITS - 1));
                 constexpr int FPW = 32 / BITS;
                 constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
-                float2 yv[8];
+                float2 yv[NQ];
 #pragma unroll
-                for (int q = 0; q < 8; q++) yv[q] = __ffma2_rn(r2[q], inv2, make_float2(MAGIC, MAGIC));
-                uint32_t b32[BITS / 2];
+                for (int q = 0; q < NQ; q++) yv[q] = __ffma2_rn(r2[q], inv2, make_float2(MAGIC, MAGIC));
+                uint32_t b32[NW];
 #pragma unroll
-                for (int wd = 0; wd < BITS / 2; wd++) {
+                for (int wd = 0; wd < NW; wd++) {
                     uint32_t v[FPW];
 #pragma unroll
                     for (int k2 = 0; k2 < FPW; k2++) {
@@ -1743,23 +1821,23 @@ __global__ void __launch_bounds__(768, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
                 };
                 bool amb;
                 {
-                    float wv[8];
+                    float wv[NQ];
 #pragma unroll
-                    for (int q = 0; q < 8; q++) {
+                    for (int q = 0; q < NQ; q++) {
                         const float2 w = window(q);
                         wv[q] = QMAX == 1 ? fminf(w.x, w.y) : fmaxf(w.x, w.y);
                     }
 #pragma unroll
-                    for (int span = 1; span < 8; span *= 2)
+                    for (int span = 1; span < NQ; span *= 2)
 #pragma unroll
-                        for (int q = 0; q < 8; q += 2 * span) wv[q] = QMAX == 1 ? fminf(wv[q], wv[q + span]) : fmaxf(wv[q], wv[q + span]);
+                        for (int q = 0; q < NQ; q += 2 * span) wv[q] = QMAX == 1 ? fminf(wv[q], wv[q + span]) : fmaxf(wv[q], wv[q + span]);
                     amb = all || (QMAX == 1 ? wv[0] <= thr : wv[0] >= thr);
                 }
                 amb &= valid;
                 if (__any_sync(0xffffffffu, amb) && amb) {   // exact codes (rare)
                     uint32_t todo = 0;
 #pragma unroll
-                    for (int q = 0; q < 8; q++) {
+                    for (int q = 0; q < NQ; q++) {
                         const float2 w = window(q);
                         bool in0, in1;
                         if constexpr (QMAX == 1) { in0 = w.x <= thr; in1 = w.y <= thr; }
@@ -1768,22 +1846,36 @@ __global__ void __launch_bounds__(768, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
                         in1 |= all || !(fabsf(r2[q].y) <= 3.402823466e38f);
                         todo |= (in0 ? 1u << (2 * q) : 0u) | (in1 ? 2u << (2 * q) : 0u);
                     }
-                    while (todo) {
-                        const int k = __ffs(todo) - 1;
-                        todo &= todo - 1;
-                        const uint32_t q = exact_code<QMAX>(exact_r(k), s) & ((1u << BITS) - 1u);
-                        const int sh = (k * BITS) & 31, wi = (k * BITS) >> 5;
+                    if (cert[u]) {                             // r is exact: no reloads
 #pragma unroll
-                        for (int q2 = 0; q2 < BITS / 2; q2++)
-                            if (q2 == wi) b32[q2] = (b32[q2] & ~(((1u << BITS) - 1u) << sh)) | (q << sh);
+                        for (int k = 0; k < C; k++) {
+                            if (!((todo >> k) & 1u)) continue;
+                            const uint32_t q = exact_code<QMAX>(double(r[u][k]), s) & ((1u << BITS) - 1u);
+                            const int sh = (k * BITS) & 31, wi = (k * BITS) >> 5;
+                            b32[wi] = (b32[wi] & ~(((1u << BITS) - 1u) << sh)) | (q << sh);
+                        }
+                    } else {
+                        while (todo) {
+                            const int k = __ffs(todo) - 1;
+                            todo &= todo - 1;
+                            const uint32_t q = exact_code<QMAX>(exact_r(k), s) & ((1u << BITS) - 1u);
+                            const int sh = (k * BITS) & 31, wi = (k * BITS) >> 5;
+#pragma unroll
+                            for (int q2 = 0; q2 < NW; q2++)
+                                if (q2 == wi) b32[q2] = (b32[q2] & ~(((1u << BITS) - 1u) << sh)) | (q << sh);
+                        }
                     }
                 }
                 if (!valid) continue;
                 const uint32_t e0 = ii[u] * d + col;
                 uint8_t *plp = a.payload + uint64_t(p) * a.pb + ((e0 * BITS) >> 3);
-                if constexpr (BITS == 2) *reinterpret_cast<uint32_t *>(plp) = b32[0];
-                else if constexpr (BITS == 4) *reinterpret_cast<uint2 *>(plp) = make_uint2(b32[0], b32[1]);
-                else *reinterpret_cast<uint4 *>(plp) = make_uint4(b32[0], b32[1], b32[2], b32[3]);
+                if constexpr (NW == 1) *reinterpret_cast<uint32_t *>(plp) = b32[0];
+                else if constexpr (NW == 2) *reinterpret_cast<uint2 *>(plp) = make_uint2(b32[0], b32[1]);
+                else {
+#pragma unroll
+                    for (int w4 = 0; w4 < NW / 4; w4++)
+                        reinterpret_cast<uint4 *>(plp)[w4] = make_uint4(b32[4 * w4], b32[4 * w4 + 1], b32[4 * w4 + 2], b32[4 * w4 + 3]);
+                }
                 if ((lane & (glanes - 1)) == 0) a.scales[uint64_t(p) * a.ng + (e0 >> a.lgB)] = uint8_t(code);
             }
         }
@@ -1887,23 +1979,39 @@ static bool launch_quant_v5w(const QuantArgs &a, bool xbf16, cudaStream_t st) {
     const size_t tbytes = size_t(S) * a.K * a.d * 2;
     const size_t off_tab = (tbytes + 127) & ~size_t(127);
     const size_t tab_floats = size_t(S) * a.K * pitch;
+    const size_t nchunk = size_t(S) * a.K * n;
     uint32_t nbuf = 2;
-    size_t smem = off_tab + 2 * tab_floats * 4;
+    size_t smem = off_tab + 2 * (tab_floats * 4 + nchunk * 8);
     if (smem > 220 * 1024) {
         nbuf = 1;
-        smem = off_tab + tab_floats * 4;
+        smem = off_tab + tab_floats * 4 + nchunk * 8;
     }
     if (smem > 220 * 1024) return false;
     const V5W pl{a.P, uint32_t(tbytes), uint32_t(off_tab), uint32_t(tab_floats), pitch,
-                 uint32_t(size_t(S) * a.K * n), uint32_t(ilog2(n)), nbuf};
+                 uint32_t(nchunk), uint32_t(ilog2(n)), nbuf, uint32_t(off_tab + nbuf * tab_floats * 4)};
     const int grid = int(a.P < 148u ? a.P : 148u);
+    static const int cfg = [] {
+        const char *e = getenv("QVG_V5W_CFG");
+        return e ? atoi(e) : 0;
+    }();
+#define V5W_GO(XB, NT, UU, CC)                                                                                   \
+    do {                                                                                                     \
+        cudaFuncSetAttribute(k_quantize_v5w<BITS, S, XB, NT, UU, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             int(smem));                                                                     \
+        k_quantize_v5w<BITS, S, XB, NT, UU, CC><<<grid, NT, smem, st>>>(a, pl);                                  \
+    } while (0)
+    const bool c32 = a.lvpr >= 1 && a.gshift >= 1;      // d >= 32 and groups of >= 32 channels
+    // 32 warps of one row each issue best (the loop is a long dependent chain:
+    // more warps, not more rows per warp); QVG_V5W_CFG=1: 24 warps x 2 rows,
+    // 2: 24 warps x 32 channels (measurement knobs)
     if (xbf16) {
-        cudaFuncSetAttribute(k_quantize_v5w<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k_quantize_v5w<BITS, S, true><<<grid, 768, smem, st>>>(a, pl);
+        if (cfg == 1) V5W_GO(true, 768, 2, 16);
+        else if (cfg == 2 && c32) V5W_GO(true, 768, 1, 32);
+        else V5W_GO(true, 1024, 1, 16);
     } else {
-        cudaFuncSetAttribute(k_quantize_v5w<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k_quantize_v5w<BITS, S, false><<<grid, 768, smem, st>>>(a, pl);
+        V5W_GO(false, 768, 2, 16);
     }
+#undef V5W_GO
     return true;
 }
 

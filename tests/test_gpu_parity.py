@@ -292,3 +292,32 @@ def test_compress_longcat_k256_vs_oracle(oracle_lib):
                                                               draws, 16)
     assert np.array_equal(dc.assignments.cpu().numpy(), asg)
     assert np.array_equal(dc.payload.cpu().numpy(), pay)
+
+
+@pytest.mark.parametrize("bits,B,S", [(2, 64, 2), (2, 16, 1), (4, 32, 3), (8, 64, 2), (2, 128, 4)])
+def test_many_planes_bf16_certificate_stress(oracle_lib, bits, B, S):
+    """>= 148 bf16 planes select the certified persistent quantize (v5w):
+    coarse dyadic inputs and centroids put residuals exactly on code
+    boundaries and group maxima exactly on the E4M3 grid (exact ties resolved
+    from registers), while zeros, subnormals and 1e-30 .. 1e4 magnitude mixes
+    make the exactness certificate fail for many rows (the float64 path)."""
+    rng = np.random.default_rng(bits * 13 + B + S)
+    P, N, d, K = 160, 70, 128, 6
+    coarse = rng.integers(-24, 25, size=(P, N, d)).astype(np.float32) / 16
+    x = np.where(rng.random((P, N, d)) < 0.5, coarse, rng.normal(0, 1.5, size=(P, N, d)).astype(np.float32))
+    x[:8] = coarse[:8]                                          # whole planes on the grid
+    x[8, :, ::5] = 0.0
+    x[9, :, ::7] = 1e-39                                        # subnormal (bf16 keeps some)
+    x[10] *= np.float32(1e-30)
+    x[11, :, ::3] *= np.float32(1e4)
+    mags = np.array([0.0, 1e-30, 1e-8, 0.125, 0.5, 1.0, 0.75, 3.0], np.float32)
+    cent = (rng.choice(mags, size=(P, S, K, d)) * rng.choice([-1, 1], size=(P, S, K, d))).astype(np.float32)
+    cent[:P // 2] = np.round(cent[:P // 2] * 8) / 8                # half the planes: dyadic centroids only
+    xt = torch.from_numpy(x).to(torch.bfloat16)
+    ct = torch.from_numpy(cent).to(torch.bfloat16)
+    asg = rng.integers(0, K, size=(P, S, N)).astype(np.uint8)
+    cfg = QuantConfig(bits=bits, group_size=B, stages=S, centroids=K)
+    pay, sc = D.quantize(xt.cuda(), cfg, ct.cuda(), torch.from_numpy(asg).cuda())
+    rp, rs = oracle_lib.quantize_given_metas_batch(xt.float().numpy(), ct.float().numpy(), asg, bits, B, 8)
+    assert np.array_equal(sc.cpu().numpy(), rs)
+    assert np.array_equal(pay.cpu().numpy(), rp)
