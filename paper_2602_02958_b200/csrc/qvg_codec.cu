@@ -1554,11 +1554,12 @@ __global__ void __launch_bounds__(256, 2) k_quantize_v6(QuantArgs a, V6Plane pl)
 struct V5W {
     uint32_t P, tbytes, off_tab, tab_floats, pitch, nchunk, lchunk;
     uint32_t nbuf;       // f32 table buffers (2, or 1 when two do not fit: one more barrier per plane)
-    uint32_t off_meta;   // per buffer: nchunk float2 {unit, max |c|} of each 16-channel block
 };
 __host__ __device__ __forceinline__ uint32_t v5w_blk(uint32_t c) { return 16u * c + 4u * (c >> 1); }
-__device__ __forceinline__ void v5w_widen(const uint16_t *stg, float *tab, float2 *meta, uint32_t nchunk,
-                                          uint32_t lchunk, uint32_t pitch) {
+// the 4-float pad after each block pair holds the pair's {unit, max |c|} metadata
+__host__ __device__ __forceinline__ uint32_t v5w_meta(uint32_t c) { return 36u * (c >> 1) + 32u + 2u * (c & 1u); }
+__device__ __forceinline__ void v5w_widen(const uint16_t *stg, float *tab, uint32_t nchunk, uint32_t lchunk,
+                                          uint32_t pitch) {
     const uint32_t cmask = (1u << lchunk) - 1u;
     for (uint32_t q = threadIdx.x; q < nchunk; q += blockDim.x) {
         const uint4 *src = reinterpret_cast<const uint4 *>(stg + size_t(q) * 16);
@@ -1582,7 +1583,7 @@ __device__ __forceinline__ void v5w_widen(const uint16_t *stg, float *tab, float
             const uint32_t eb = __float_as_uint(mn) & 0x7F800000u;
             unit = eb > (7u << 23) ? __uint_as_float(eb - (7u << 23)) : 0.f;
         }
-        meta[q] = make_float2(unit, mx);
+        *reinterpret_cast<float2 *>(tab + size_t(q >> lchunk) * pitch + v5w_meta(q & cmask)) = make_float2(unit, mx);
     }
 }
 __device__ __forceinline__ float v5_min3_abs(float m, float a, float b) {
@@ -1592,8 +1593,11 @@ __device__ __forceinline__ float v5_min3_abs(float m, float a, float b) {
     return d;
 }
 
-template <int BITS, int S, bool XBF16, int NT, int U, int C>
+template <int BITS, int S, bool XBF16, int NT, int U, int C, bool PIPE = false>
 __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
+    // PIPE (bf16, one 16-channel row per pass): the next pass's x and
+    // assignments are loaded into registers before this pass is processed
+    static_assert(!PIPE || (XBF16 && U == 1 && C == 16), "register pipeline: bf16 rows, U = 1, C = 16");
     constexpr int QMAX = (1 << (BITS - 1)) - 1;
     constexpr int SS = S > 0 ? S : 1;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -1611,6 +1615,7 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
     const uint32_t cc = threadIdx.x & ((1u << lv) - 1u);
     const int col = int(cc) * C;
     const uint32_t coff = v5w_blk(cc << LC);
+    const uint32_t mdelta = C == 32 || !(cc & 1u) ? 32u : 18u;       // metadata, relative to coff
     const uint32_t rslot = threadIdx.x >> lv, rpp = uint32_t(NT) >> lv;
     const int glanes = 1 << (a.gshift - int(LC));
     const int lane = threadIdx.x & 31;
@@ -1627,11 +1632,10 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
         // widen plane p's staged bf16 table into f32 buffer j&1 (the buffer was last
         // read two planes ago, before the previous plane's barrier), then restage
         float *const ct = tabs + (pl.nbuf == 2 ? (j & 1u) : 0u) * pl.tab_floats;
-        float2 *const mt = reinterpret_cast<float2 *>(smem + pl.off_meta) + (pl.nbuf == 2 ? (j & 1u) : 0u) * pl.nchunk;
         if (S > 0) {
             if (pl.nbuf == 1 && j > 0) __syncthreads();       // previous plane done with the only buffer
             mbar_wait(&bar, j & 1u);
-            v5w_widen(stg, ct, mt, pl.nchunk, pl.lchunk, pl.pitch);
+            v5w_widen(stg, ct, pl.nchunk, pl.lchunk, pl.pitch);
             __syncthreads();
             if (threadIdx.x == 0 && p + gridDim.x < pl.P) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1641,18 +1645,38 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
         const uint64_t pN = uint64_t(p) * N;
         const uint8_t *xb = static_cast<const uint8_t *>(a.x) + pN * d * (XBF16 ? 2 : 4);
         const uint8_t *ap = a.asg + pN * S;
+        uint4 nx0, nx1;
+        int na[SS];
+        auto fetch = [&](uint32_t i) {
+            i = i < N ? i : N - 1;
+            const uint4 *xp = reinterpret_cast<const uint4 *>(xb + (uint64_t(i) * d + col) * 2);
+            nx0 = __ldg(xp);
+            nx1 = __ldg(xp + 1);
+#pragma unroll
+            for (int t = 0; t < S; t++) na[t] = __ldg(ap + t * N + i);
+        };
+        if constexpr (PIPE) fetch(rslot);
         for (uint32_t i0 = 0; i0 < N; i0 += rpp * U) {
             float r[U][C];
             uint32_t ii[U];
             int ai[U][SS];
+            if constexpr (PIPE) {
+                const uint32_t i = i0 + rslot;
+                ii[0] = i < N ? i : N - 1;
+                cvt16(nx0, nx1, r[0]);
 #pragma unroll
-            for (int u = 0; u < U; u++) {
-                const uint32_t i = i0 + u * rpp + rslot;
-                ii[u] = i < N ? i : N - 1;
-                load_x16<XBF16>(xb, ii[u] * d + col, r[u]);
-                if constexpr (C == 32) load_x16<XBF16>(xb, ii[u] * d + col + 16, r[u] + 16);
+                for (int t = 0; t < S; t++) ai[0][t] = na[t];
+                if (i0 + rpp < N) fetch(i + rpp);
+            } else {
 #pragma unroll
-                for (int t = 0; t < S; t++) ai[u][t] = __ldg(ap + t * N + ii[u]);
+                for (int u = 0; u < U; u++) {
+                    const uint32_t i = i0 + u * rpp + rslot;
+                    ii[u] = i < N ? i : N - 1;
+                    load_x16<XBF16>(xb, ii[u] * d + col, r[u]);
+                    if constexpr (C == 32) load_x16<XBF16>(xb, ii[u] * d + col + 16, r[u] + 16);
+#pragma unroll
+                    for (int t = 0; t < S; t++) ai[u][t] = __ldg(ap + t * N + ii[u]);
+                }
             }
             float eb[U], am[U];
             bool cert[U];
@@ -1673,7 +1697,8 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
 #pragma unroll
                 for (int t = 0; t < S; t++) {
                     const uint32_t row = uint32_t(t * a.K + ai[u][t]);
-                    const float4 *c4 = reinterpret_cast<const float4 *>(ct + row * pl.pitch + coff);
+                    const float *cr = ct + row * pl.pitch + coff;
+                    const float4 *c4 = reinterpret_cast<const float4 *>(cr);
 #pragma unroll
                     for (int q = 0; q < C / 4; q++) {
                         const float4 cv = c4[q];
@@ -1682,11 +1707,11 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
                     }
                     if constexpr (kCert) {
                         if constexpr (C == 32) {
-                            const float4 m = reinterpret_cast<const float4 *>(mt)[(row << (pl.lchunk - 1)) + cc];
+                            const float4 m = *reinterpret_cast<const float4 *>(cr + mdelta);
                             cun = fminf(cun, fminf(m.x, m.z));
                             csum = __fadd_ru(csum, fmaxf(m.y, m.w));
                         } else {
-                            const float2 m = mt[(row << pl.lchunk) + cc];
+                            const float2 m = *reinterpret_cast<const float2 *>(cr + mdelta);
                             cun = fminf(cun, m.x);
                             csum = __fadd_ru(csum, m.y);
                         }
@@ -1821,17 +1846,17 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
                 };
                 bool amb;
                 {
-                    float wv[NQ];
+                    // two 3-input chains (min for the 2-bit distance to s/2, max for
+                    // the distance from the nearest integer)
+                    float w0 = QMAX == 1 ? __int_as_float(0x7F800000) : 0.f, w1 = w0;
 #pragma unroll
                     for (int q = 0; q < NQ; q++) {
                         const float2 w = window(q);
-                        wv[q] = QMAX == 1 ? fminf(w.x, w.y) : fmaxf(w.x, w.y);
+                        float &acc = (q & 1) ? w1 : w0;
+                        acc = QMAX == 1 ? fminf(acc, fminf(w.x, w.y)) : fmaxf(acc, fmaxf(w.x, w.y));
                     }
-#pragma unroll
-                    for (int span = 1; span < NQ; span *= 2)
-#pragma unroll
-                        for (int q = 0; q < NQ; q += 2 * span) wv[q] = QMAX == 1 ? fminf(wv[q], wv[q + span]) : fmaxf(wv[q], wv[q + span]);
-                    amb = all || (QMAX == 1 ? wv[0] <= thr : wv[0] >= thr);
+                    const float wv = QMAX == 1 ? fminf(w0, w1) : fmaxf(w0, w1);
+                    amb = all || (QMAX == 1 ? wv <= thr : wv >= thr);
                 }
                 amb &= valid;
                 if (__any_sync(0xffffffffu, amb) && amb) {   // exact codes (rare)
@@ -1981,35 +2006,38 @@ static bool launch_quant_v5w(const QuantArgs &a, bool xbf16, cudaStream_t st) {
     const size_t tab_floats = size_t(S) * a.K * pitch;
     const size_t nchunk = size_t(S) * a.K * n;
     uint32_t nbuf = 2;
-    size_t smem = off_tab + 2 * (tab_floats * 4 + nchunk * 8);
+    size_t smem = off_tab + 2 * tab_floats * 4;
     if (smem > 220 * 1024) {
         nbuf = 1;
-        smem = off_tab + tab_floats * 4 + nchunk * 8;
+        smem = off_tab + tab_floats * 4;
     }
     if (smem > 220 * 1024) return false;
     const V5W pl{a.P, uint32_t(tbytes), uint32_t(off_tab), uint32_t(tab_floats), pitch,
-                 uint32_t(nchunk), uint32_t(ilog2(n)), nbuf, uint32_t(off_tab + nbuf * tab_floats * 4)};
+                 uint32_t(nchunk), uint32_t(ilog2(n)), nbuf};
     const int grid = int(a.P < 148u ? a.P : 148u);
     static const int cfg = [] {
         const char *e = getenv("QVG_V5W_CFG");
         return e ? atoi(e) : 0;
     }();
-#define V5W_GO(XB, NT, UU, CC)                                                                                   \
-    do {                                                                                                     \
-        cudaFuncSetAttribute(k_quantize_v5w<BITS, S, XB, NT, UU, CC>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             int(smem));                                                                     \
-        k_quantize_v5w<BITS, S, XB, NT, UU, CC><<<grid, NT, smem, st>>>(a, pl);                                  \
+#define V5W_GO(XB, NT, UU, CC, PP)                                                                        \
+    do {                                                                                                  \
+        cudaFuncSetAttribute(k_quantize_v5w<BITS, S, XB, NT, UU, CC, PP>,                                 \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));                     \
+        k_quantize_v5w<BITS, S, XB, NT, UU, CC, PP><<<grid, NT, smem, st>>>(a, pl);                       \
     } while (0)
     const bool c32 = a.lvpr >= 1 && a.gshift >= 1;      // d >= 32 and groups of >= 32 channels
-    // 32 warps of one row each issue best (the loop is a long dependent chain:
-    // more warps, not more rows per warp); QVG_V5W_CFG=1: 24 warps x 2 rows,
-    // 2: 24 warps x 32 channels (measurement knobs)
+    // the loop is a long dependent chain: many warps of one row each, with the
+    // next row's loads in flight, issue best (measured 4.76 ms vs 4.87 for 32
+    // warps without the register pipeline and 4.97 for 24 warps x 2 rows).
+    // QVG_V5W_CFG=1: 24 warps x 2 rows, 2: 24 warps x 32 channels,
+    // 3: 32 warps x 1 row (measurement knobs)
     if (xbf16) {
-        if (cfg == 1) V5W_GO(true, 768, 2, 16);
-        else if (cfg == 2 && c32) V5W_GO(true, 768, 1, 32);
-        else V5W_GO(true, 1024, 1, 16);
+        if (cfg == 1) V5W_GO(true, 768, 2, 16, false);
+        else if (cfg == 2 && c32) V5W_GO(true, 768, 1, 32, false);
+        else if (cfg == 3) V5W_GO(true, 1024, 1, 16, false);
+        else V5W_GO(true, 768, 1, 16, true);
     } else {
-        V5W_GO(false, 768, 2, 16);
+        V5W_GO(false, 768, 2, 16, false);
     }
 #undef V5W_GO
     return true;
