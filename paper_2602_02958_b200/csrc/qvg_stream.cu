@@ -445,14 +445,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_stream(DequantArgs a, G
             // every non-final partial sum exact in f32 <= all terms multiples of
             // `unit` and sum of magnitudes < 2^24 unit
             // (a row whose codes are all zero has q*s == 0: only the centroid terms count)
-            bool cert = true;
+            bool cert = true, swap01 = false;
             if constexpr (S >= 2) {
                 uint32_t anyq = 0;
 #pragma unroll
                 for (int q = 0; q < Codes16<BITS>::NW; q++) anyq |= w[u].w[q];
-                float unit = anyq ? fmaxf(__uint_as_float((__float_as_uint(sv) & 0x7F800000u) - (3u << 23)), 0.001953125f)
-                                  : __int_as_float(0x7F800000);
-                float bound = anyq ? sv * float(1 << (BITS - 1)) : 0.f;
+                const float unit_s = anyq ? fmaxf(__uint_as_float((__float_as_uint(sv) & 0x7F800000u) - (3u << 23)), 0.001953125f)
+                                          : __int_as_float(0x7F800000);
+                const float bound_s = anyq ? sv * float(1 << (BITS - 1)) : 0.f;
+                float unit = unit_s, bound = bound_s;
 #pragma unroll
                 for (int t = 1; t < S; t++) {
                     const float2 m = meta[(uint32_t(t * int(g.K) + ai[u][t]) << lvpr) + c];
@@ -460,15 +461,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_stream(DequantArgs a, G
                     bound = __fadd_ru(bound, m.y);
                 }
                 cert = S == 2 && !anyq ? true : bound < unit * 16777216.f;
+                if constexpr (S == 2) {
+                    // the other order: q*s + C_1 exact in f32, C_2 added last = ONE
+                    // rounding of the exact three-term sum.  That is the reference's
+                    // RN32 of its float64 chain when that chain is exact too (all terms
+                    // multiples of the common unit, magnitudes < 2^53 units); it
+                    // certifies rows whose stage-2 centroid block has tiny entries
+                    if (!cert) {
+                        const float2 m0 = meta[(uint32_t(ai[u][0]) << lvpr) + c];
+                        swap01 = __fadd_ru(bound_s, m0.y) < fminf(unit_s, m0.x) * 16777216.f &&
+                                 __fadd_ru(bound, m0.y) < fminf(unit, m0.x) * 9007199254740992.f;
+                        cert = swap01;
+                    }
+                }
             }
-#pragma unroll
-            for (int t = S - 1; t >= 0; t--) {                 // reversed(stages)
-                const float *row = tab + uint32_t(t * int(g.K) + ai[u][t]) * g.pitch + coff;
+            if constexpr (S == 2) {
+                const float *ra = tab + uint32_t(int(g.K) + ai[u][1]) * g.pitch + coff;
+                const float *rb = tab + uint32_t(ai[u][0]) * g.pitch + coff;
+                const float *first = swap01 ? rb : ra, *last = swap01 ? ra : rb;
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
-                    const float4 cv = *reinterpret_cast<const float4 *>(row + 4 * j);
+                    const float4 cv = *reinterpret_cast<const float4 *>(first + 4 * j);
                     y[2 * j] = __fadd2_rn(y[2 * j], make_float2(cv.x, cv.y));
                     y[2 * j + 1] = __fadd2_rn(y[2 * j + 1], make_float2(cv.z, cv.w));
+                }
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const float4 cv = *reinterpret_cast<const float4 *>(last + 4 * j);
+                    y[2 * j] = __fadd2_rn(y[2 * j], make_float2(cv.x, cv.y));
+                    y[2 * j + 1] = __fadd2_rn(y[2 * j + 1], make_float2(cv.z, cv.w));
+                }
+            } else {
+#pragma unroll
+                for (int t = S - 1; t >= 0; t--) {             // reversed(stages)
+                    const float *row = tab + uint32_t(t * int(g.K) + ai[u][t]) * g.pitch + coff;
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        const float4 cv = *reinterpret_cast<const float4 *>(row + 4 * j);
+                        y[2 * j] = __fadd2_rn(y[2 * j], make_float2(cv.x, cv.y));
+                        y[2 * j + 1] = __fadd2_rn(y[2 * j + 1], make_float2(cv.z, cv.w));
+                    }
                 }
             }
             if constexpr (S >= 2) {

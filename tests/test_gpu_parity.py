@@ -321,3 +321,30 @@ def test_many_planes_bf16_certificate_stress(oracle_lib, bits, B, S):
     rp, rs = oracle_lib.quantize_given_metas_batch(xt.float().numpy(), ct.float().numpy(), asg, bits, B, 8)
     assert np.array_equal(sc.cpu().numpy(), rs)
     assert np.array_equal(pay.cpu().numpy(), rp)
+
+
+@pytest.mark.parametrize("c1mag", [1e-30, 1e-12, 3e-8, 0.0])
+def test_dequant_two_stage_add_order_certificate(oracle_lib, c1mag):
+    """S = 2 rows whose stage-2 centroid block holds tiny entries: the
+    reversed-order add-back (C_2 last) is certified only when the reference's
+    float64 chain is exact too.  Dyadic stage-1 centroids equal to -q*s
+    cancel exactly, so a wrong order would surface the tiny term."""
+    rng = np.random.default_rng(int(abs(np.log10(c1mag))) if c1mag else 7)
+    P, N, d, K, bits, B = 160, 64, 128, 4, 2, 64
+    pay = rng.integers(0, 256, size=(P, N * d * bits // 8)).astype(np.uint8)
+    codes = np.array([0x28, 0x30, 0x38, 0x2C], np.uint8)           # 0.25, 0.5, 1.0, 0.375
+    sc = rng.choice(codes, size=(P, N * d // B)).astype(np.uint8)
+    c0 = rng.choice(np.array([0.0, 0.25, -0.25, 0.5, -0.5, 0.75, 1.0, -1.5], np.float32), size=(P, 1, K, d))
+    c1 = (rng.choice(np.array([0.0, 1.0, 3.0], np.float32), size=(P, 1, K, d)) * np.float32(c1mag)
+          + rng.choice(np.array([0.0, 0.0, 0.125, -0.0625], np.float32), size=(P, 1, K, d)))
+    c1[:, :, ::2] = np.float32(c1mag) * rng.choice([-1.0, 1.0], size=c1[:, :, ::2].shape)
+    cent = torch.from_numpy(np.concatenate([c0, c1], axis=1).astype(np.float32)).to(torch.bfloat16)
+    asg = rng.integers(0, K, size=(P, 2, N)).astype(np.uint8)
+    cfg = QuantConfig(bits=bits, group_size=B, stages=2, centroids=K)
+    dc = D.DeviceChunks(cfg, N, d, torch.from_numpy(pay).cuda(), torch.from_numpy(sc).cuda(), cent.cuda(),
+                        torch.from_numpy(asg).cuda())
+    ref = oracle_lib.prq_decompress_batch(pay, sc, cent.float().numpy(), asg, N, d, bits, B, 8)
+    out = D.dequantize(dc, torch.float32).cpu().numpy()
+    assert np.array_equal(_u32(out), _u32(ref))
+    outb = D.dequantize(dc, torch.bfloat16).cpu()
+    assert torch.equal(outb.view(torch.int16), torch.from_numpy(ref).to(torch.bfloat16).view(torch.int16))
