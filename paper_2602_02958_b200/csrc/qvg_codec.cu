@@ -1586,6 +1586,9 @@ __device__ __forceinline__ void v5w_widen(const uint16_t *stg, float *tab, uint3
         *reinterpret_cast<float2 *>(tab + size_t(q >> lchunk) * pitch + v5w_meta(q & cmask)) = make_float2(unit, mx);
     }
 }
+__device__ __forceinline__ void v5w_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ float v5_min3_abs(float m, float a, float b) {
     float t, d;
     asm("min.f32 %0, %1, %2;" : "=f"(t) : "f"(fabsf(a)), "f"(fabsf(b)));
@@ -1602,10 +1605,15 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
     constexpr int SS = S > 0 ? S : 1;
     extern __shared__ __align__(128) uint8_t smem[];
     __shared__ uint64_t bar;
+    __shared__ uint64_t full[2], empty[2];  // f32 table buffer b: widened / released by every warp
     __shared__ float rcp_tab[128];          // RN32(1 / e4m3(code))
     uint16_t *const stg = reinterpret_cast<uint16_t *>(smem);
     float *const tabs = reinterpret_cast<float *>(smem + pl.off_tab);
     const uint32_t d = uint32_t(a.d), N = a.N;
+    // Two table buffers and no CTA-wide barrier per plane: plane j+1's table is
+    // widened half-way through plane j (after every warp released buffer
+    // (j+1)&1 at the end of plane j-1), so warps flow across plane boundaries.
+    const bool flow = S > 0 && pl.nbuf == 2;
     // C = 16 or 32 channels per thread (one or two padded 16-channel blocks,
     // contiguous in the table: v5w_blk(2c + 1) = v5w_blk(2c) + 16)
     static_assert(C == 16 || C == 32, "channels per thread");
@@ -1623,16 +1631,32 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
     if (threadIdx.x < 128) rcp_tab[threadIdx.x] = __frcp_rn(e4m3_decode_fast(threadIdx.x));
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&full[b], NT);
+            mbar_init(&empty[b], NT / 32);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (S > 0 && threadIdx.x == 0 && blockIdx.x < pl.P) stage_table(a.cent, blockIdx.x, pl.tbytes, stg, &bar);
+    if (flow && blockIdx.x < pl.P) {
+        mbar_wait(&bar, 0);
+        v5w_widen(stg, tabs, pl.nchunk, pl.lchunk, pl.pitch);
+        v5w_arrive(&full[0]);
+    }
+    const uint32_t mid = ((N + rpp * U - 1) / (rpp * U)) / 2;    // the pass that widens the next table
     uint32_t j = 0;
     for (uint32_t p = blockIdx.x; p < pl.P; p += gridDim.x, j++) {
-        // widen plane p's staged bf16 table into f32 buffer j&1 (the buffer was last
-        // read two planes ago, before the previous plane's barrier), then restage
         float *const ct = tabs + (pl.nbuf == 2 ? (j & 1u) : 0u) * pl.tab_floats;
-        if (S > 0) {
+        if (flow) {
+            mbar_wait(&full[j & 1u], (j >> 1) & 1u);             // every thread widened its share,
+            if (threadIdx.x == 0 && p + gridDim.x < pl.P) {      // so the staging copy is free
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                stage_table(a.cent, p + gridDim.x, pl.tbytes, stg, &bar);
+            }
+        } else if (S > 0) {
+            // widen plane p's staged bf16 table into f32 buffer j&1 (the buffer was last
+            // read two planes ago, before the previous plane's barrier), then restage
             if (pl.nbuf == 1 && j > 0) __syncthreads();       // previous plane done with the only buffer
             mbar_wait(&bar, j & 1u);
             v5w_widen(stg, ct, pl.nchunk, pl.lchunk, pl.pitch);
@@ -1656,7 +1680,15 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
             for (int t = 0; t < S; t++) na[t] = __ldg(ap + t * N + i);
         };
         if constexpr (PIPE) fetch(rslot);
-        for (uint32_t i0 = 0; i0 < N; i0 += rpp * U) {
+        uint32_t pass = 0;
+        for (uint32_t i0 = 0; i0 < N; i0 += rpp * U, pass++) {
+            if (flow && pass == mid && p + gridDim.x < pl.P) {
+                const uint32_t jn = j + 1;
+                if (jn >= 2) mbar_wait(&empty[jn & 1u], ((jn - 2) >> 1) & 1u);   // plane j-1 released
+                mbar_wait(&bar, jn & 1u);                                     // staged
+                v5w_widen(stg, tabs + (jn & 1u) * pl.tab_floats, pl.nchunk, pl.lchunk, pl.pitch);
+                v5w_arrive(&full[jn & 1u]);
+            }
             float r[U][C];
             uint32_t ii[U];
             int ai[U][SS];
@@ -1903,6 +1935,10 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
                 }
                 if ((lane & (glanes - 1)) == 0) a.scales[uint64_t(p) * a.ng + (e0 >> a.lgB)] = uint8_t(code);
             }
+        }
+        if (flow) {                                               // done reading buffer j&1
+            __syncwarp();
+            if (lane == 0) v5w_arrive(&empty[j & 1u]);
         }
     }
     const uint32_t all = __reduce_or_sync(0xffffffffu, nonfinite ? uint32_t(QVG_STATUS_NONFINITE) : 0u);
