@@ -89,6 +89,23 @@ __device__ __forceinline__ void bar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+// wait with nanosleep back-off: a warp that finds the phase incomplete sleeps
+// instead of re-issuing try_wait, leaving the issue slots of its SMSP to the
+// working softmax warps (ns = 0: plain spin)
+__device__ __forceinline__ bool bar_try(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred P1;\nmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\nselp.u32 %0, 1, 0, P1;\n}"
+        : "=r"(ok)
+        : "r"(su32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void bar_wait_nap(uint64_t *bar, uint32_t parity, uint32_t ns) {
+    while (!bar_try(bar, parity))
+        if (ns) __nanosleep(ns);
+}
+
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -451,6 +468,7 @@ struct Args {
     int H;
     float scale_log2;
     uint16_t *out;
+    uint32_t nap_sm = 0, nap_mma = 0, nap_tma = 0;   // nanosleep back-off of the softmax / MMA / TMA waits
 };
 
 struct Bars {
@@ -961,6 +979,30 @@ static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const 
 // the FMA pipe (degree-3 polynomial on the rounded-off fraction, exponent
 // added in the integer domain) to relieve the 16/clk/SM MUFU.
 // ============================================================================
+// QVG_ATTN_NAP="sm,mma,tma": nanosleep back-off (ns) of the softmax, MMA-issuer
+// and TMA-producer waits.  Default 0 (plain spin): on the LongCat layer no
+// setting changed pp4 (5.46 ms); pp5 needs sm >= 16 (6.05 -> 5.54 ms)
+static void nap_args(attn2::Args &a) {
+    static const uint32_t v[3] = {[] {
+                                      const char *e = getenv("QVG_ATTN_NAP");
+                                      return e ? uint32_t(atoi(e)) : 0u;
+                                  }(),
+                                  [] {
+                                      const char *e = getenv("QVG_ATTN_NAP");
+                                      const char *c = e ? strchr(e, ',') : nullptr;
+                                      return c ? uint32_t(atoi(c + 1)) : 0u;
+                                  }(),
+                                  [] {
+                                      const char *e = getenv("QVG_ATTN_NAP");
+                                      const char *c = e ? strchr(e, ',') : nullptr;
+                                      c = c ? strchr(c + 1, ',') : nullptr;
+                                      return c ? uint32_t(atoi(c + 1)) : 0u;
+                                  }()};
+    a.nap_sm = v[0];
+    a.nap_mma = v[1];
+    a.nap_tma = v[2];
+}
+
 namespace attn4 {
 using attn::kTile;
 using attn::kD;
@@ -1057,7 +1099,7 @@ k_attention_pp4(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             }
             for (int64_t j = 0; j < nb; j++) {
                 const int st = int(j & 1);
-                if (j >= 2) attn::bar_wait(&bars.kv_empty[st], uint32_t(((j - 2) >> 1) & 1));
+                if (j >= 2) attn::bar_wait_nap(&bars.kv_empty[st], uint32_t(((j - 2) >> 1) & 1), a.nap_tma);
                 uint8_t *sK = sKV + st * 2 * kOpTile, *sV = sK + kOpTile;
                 attn2::expect_tx(&bars.kv_full[st], 2 * kOpTile);
                 if (j < cb) {
@@ -1107,17 +1149,17 @@ k_attention_pp4(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             long long tr[4][4];
             const long long t0c = clock64();
             for (int64_t j = 0; j < nb; j++) {
-                attn::bar_wait(&bars.p_full[0], uint32_t(j & 1));
+                attn::bar_wait_nap(&bars.p_full[0], uint32_t(j & 1), a.nap_mma);
                 if (TR && j >= 8 && j < 12) tr[j - 8][0] = clock64() - t0c;
                 attn::fence_after();
                 issue_pv(0, j);
                 if (j + 1 < nb) {
-                    attn::bar_wait(&bars.kv_full[(j + 1) & 1], uint32_t(((j + 1) >> 1) & 1));
+                    attn::bar_wait_nap(&bars.kv_full[(j + 1) & 1], uint32_t(((j + 1) >> 1) & 1), a.nap_mma);
                     if (TR && j >= 8 && j < 12) tr[j - 8][1] = clock64() - t0c;
                     attn::fence_after();
                     issue_s(0, j + 1);                // overwrites P_A(j): MMAs execute in order
                 }
-                attn::bar_wait(&bars.p_full[1], uint32_t(j & 1));
+                attn::bar_wait_nap(&bars.p_full[1], uint32_t(j & 1), a.nap_mma);
                 if (TR && j >= 8 && j < 12) tr[j - 8][2] = clock64() - t0c;
                 attn::fence_after();
                 issue_pv(1, j);
@@ -1144,7 +1186,7 @@ k_attention_pp4(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             const int64_t cnt = j < cb ? a.n_cache - j * kTile : a.n_cur - (j - cb) * kTile;
             const int nvalid = int(cnt < kTile ? cnt : kTile);
             if (TR && j >= 8 && j < 12) tr[j - 8][0] = clock64() - t0c;
-            attn::bar_wait(&bars.s_full[t], uint32_t(j & 1));
+            attn::bar_wait_nap(&bars.s_full[t], uint32_t(j & 1), a.nap_sm);
             if (TR && j >= 8 && j < 12) tr[j - 8][1] = clock64() - t0c;
             attn::fence_after();
             float s[128];
@@ -1267,6 +1309,7 @@ static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const 
     const size_t smem = kSmem + 1024;
     dim3 grid(unsigned((nq + 2 * kTile - 1) / (2 * kTile)), unsigned(H));
     attn2::Args args{nq, nc, ncur, H, scale_log2, out};
+    nap_args(args);
     static const int poly = [] { const char *e = getenv("QVG_ATTN_POLY"); return e ? atoi(e) : 96; }();
     auto go = [&](auto kern) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -1288,6 +1331,311 @@ static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const 
     return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
 }
 }  // namespace attn4
+
+// ============================================================================
+// attn5: the attn4 schedule with every S row split over TWO softmax warps
+// (columns 0-63 / 64-127 of the same TMEM lanes), so each SMSP runs two
+// softmax warps of the active tile and hides the MUFU / TMEM / FMA latencies
+// of a single warp.  18 warps: 16 softmax (tile t = warp >> 3, column half
+// hf = (warp >> 2) & 1, lane quarter = warp & 3), TMA producer, MMA issuer.
+// The halves exchange row maxima through shared memory (one 64-thread named
+// barrier per phase), keep separate running sums (same max frame), and write
+// P into their OWN S columns (half hf at TMEM columns 64 hf .. 64 hf + 31); the
+// PV MMA takes its A operand for k-steps 4..7 from the second half.  Each half
+// rescales and stores its 64 output columns.
+// ============================================================================
+namespace attn5 {
+using attn::kTile;
+using attn::kD;
+using attn2::kBox;
+using attn2::kOpTile;
+constexpr uint32_t kSmem = attn3::kSmem;
+constexpr int kThreads = 18 * 32;
+
+struct Bars {
+    uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], p_full[2], o_final;
+    uint32_t tmem;
+    float xmax[2][2][128];      // [tile][half][row] partial row maxima
+    float lsum[2][2][128];      // final partial row sums
+};
+
+__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float v[64]) {
+    uint32_t *r = reinterpret_cast<uint32_t *>(v);
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[32 * c + 0]), "=r"(r[32 * c + 1]), "=r"(r[32 * c + 2]), "=r"(r[32 * c + 3]),
+              "=r"(r[32 * c + 4]), "=r"(r[32 * c + 5]), "=r"(r[32 * c + 6]), "=r"(r[32 * c + 7]),
+              "=r"(r[32 * c + 8]), "=r"(r[32 * c + 9]), "=r"(r[32 * c + 10]), "=r"(r[32 * c + 11]),
+              "=r"(r[32 * c + 12]), "=r"(r[32 * c + 13]), "=r"(r[32 * c + 14]), "=r"(r[32 * c + 15]),
+              "=r"(r[32 * c + 16]), "=r"(r[32 * c + 17]), "=r"(r[32 * c + 18]), "=r"(r[32 * c + 19]),
+              "=r"(r[32 * c + 20]), "=r"(r[32 * c + 21]), "=r"(r[32 * c + 22]), "=r"(r[32 * c + 23]),
+              "=r"(r[32 * c + 24]), "=r"(r[32 * c + 25]), "=r"(r[32 * c + 26]), "=r"(r[32 * c + 27]),
+              "=r"(r[32 * c + 28]), "=r"(r[32 * c + 29]), "=r"(r[32 * c + 30]), "=r"(r[32 * c + 31])
+            : "r"(taddr + 32 * c));
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t v[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
+__device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+
+// columns [POLY_FROM, 64) of each half row use the polynomial exp2
+template <int POLY_FROM>
+__global__ void __launch_bounds__(kThreads, 1)
+k_attention_pp5(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
+                const __grid_constant__ CUtensorMap tmKc, const __grid_constant__ CUtensorMap tmVc, attn2::Args a) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sQ = smem;
+    uint8_t *sKV = smem + 2 * kOpTile;
+    __shared__ Bars bars;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int h = blockIdx.y;
+    const int64_t q0 = int64_t(blockIdx.x) * 2 * kTile;
+    const int64_t cb = (a.n_cache + kTile - 1) / kTile;
+    const int64_t nb = cb + (a.n_cur + kTile - 1) / kTile;
+
+    if (tid == 0) {
+        attn::bar_init(&bars.q_full, 1);
+        for (int i = 0; i < 2; i++) {
+            attn::bar_init(&bars.kv_full[i], 1);
+            attn::bar_init(&bars.kv_empty[i], 1);
+            attn::bar_init(&bars.s_full[i], 1);
+            attn::bar_init(&bars.p_full[i], 256);
+        }
+        attn::bar_init(&bars.o_final, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 17) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(attn::su32(&bars.tmem)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    attn::fence_before();
+    __syncthreads();
+    attn::fence_after();
+    const uint32_t tmem = bars.tmem;
+
+    if (warp == 16) {
+        if (lane == 0) {                              // ---- TMA producer
+            attn2::expect_tx(&bars.q_full, 2 * kOpTile);
+            for (int t = 0; t < 2; t++) {
+                attn2::tma_load_2d(sQ + t * kOpTile, &tmQ, h * kD, int(q0 + t * kTile), &bars.q_full);
+                attn2::tma_load_2d(sQ + t * kOpTile + kBox, &tmQ, h * kD + 64, int(q0 + t * kTile), &bars.q_full);
+            }
+            for (int64_t j = 0; j < nb; j++) {
+                const int st = int(j & 1);
+                if (j >= 2) attn::bar_wait_nap(&bars.kv_empty[st], uint32_t(((j - 2) >> 1) & 1), a.nap_tma);
+                uint8_t *sK = sKV + st * 2 * kOpTile, *sV = sK + kOpTile;
+                attn2::expect_tx(&bars.kv_full[st], 2 * kOpTile);
+                if (j < cb) {
+                    const int yk = int(2 * h * a.n_cache + j * kTile), yv = int((2 * h + 1) * a.n_cache + j * kTile);
+                    attn2::tma_load_2d(sK, &tmKV, 0, yk, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sK + kBox, &tmKV, 64, yk, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sV, &tmKV, 0, yv, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sV + kBox, &tmKV, 64, yv, &bars.kv_full[st]);
+                } else {
+                    const int y = int((j - cb) * kTile);
+                    attn2::tma_load_2d(sK, &tmKc, h * kD, y, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sK + kBox, &tmKc, h * kD + 64, y, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sV, &tmVc, h * kD, y, &bars.kv_full[st]);
+                    attn2::tma_load_2d(sV + kBox, &tmVc, h * kD + 64, y, &bars.kv_full[st]);
+                }
+            }
+        }
+    } else if (warp == 17) {
+        if (lane == 0) {                              // ---- MMA issuer
+            constexpr uint32_t idK = attn::umma_idesc(false), idV = attn::umma_idesc(true);
+            auto issue_s = [&](int t, int64_t j) {    // S_t = Q_t K_j^T
+                const int st = int(j & 1);
+                const uint32_t sk = attn::su32(sKV + st * 2 * kOpTile);
+                const uint32_t sq = attn::su32(sQ + t * kOpTile);
+#pragma unroll
+                for (int k = 0; k < kD / 16; k++) {
+                    const uint32_t off = (k >> 2) * kBox + (k & 3) * 32;
+                    attn::mma_f16(tmem + t * 128, attn2::desc_sw128(sq + off, 16, 1024),
+                                  attn2::desc_sw128(sk + off, 16, 1024), idK, k > 0);
+                }
+                attn::mma_commit(&bars.s_full[t]);
+            };
+            auto issue_pv = [&](int t, int64_t j) {   // O_t += P_t V_j; P of keys 64.. at S columns 64..
+                const int st = int(j & 1);
+                const uint32_t sv = attn::su32(sKV + st * 2 * kOpTile) + kOpTile;
+#pragma unroll
+                for (int k = 0; k < kTile / 16; k++)
+                    attn3::mma_f16_tmem_a(tmem + 256 + t * 128, tmem + t * 128 + (k >> 2) * 64 + (k & 3) * 8,
+                                          attn2::desc_sw128(sv + k * 2048, kBox, 1024), idV,
+                                          (j > 0 || k > 0) ? 1u : 0u);
+            };
+            attn::bar_wait(&bars.q_full, 0);
+            attn::bar_wait(&bars.kv_full[0], 0);
+            attn::fence_after();
+            issue_s(0, 0);
+            issue_s(1, 0);
+            for (int64_t j = 0; j < nb; j++) {
+                attn::bar_wait_nap(&bars.p_full[0], uint32_t(j & 1), a.nap_mma);
+                attn::fence_after();
+                issue_pv(0, j);
+                if (j + 1 < nb) {
+                    attn::bar_wait_nap(&bars.kv_full[(j + 1) & 1], uint32_t(((j + 1) >> 1) & 1), a.nap_mma);
+                    attn::fence_after();
+                    issue_s(0, j + 1);
+                }
+                attn::bar_wait_nap(&bars.p_full[1], uint32_t(j & 1), a.nap_mma);
+                attn::fence_after();
+                issue_pv(1, j);
+                attn::mma_commit(&bars.kv_empty[j & 1]);
+                if (j + 1 < nb) issue_s(1, j + 1);
+            }
+            attn::mma_commit(&bars.o_final);
+        }
+    } else {
+        // ---- softmax: tile t, column half hf, rows = TMEM lanes of quarter qd ----
+        const int t = warp >> 3, hf = (warp >> 2) & 1, qd = warp & 3;
+        const int row = qd * 32 + lane;
+        const uint32_t t_lane = uint32_t(qd * 32) << 16;
+        const uint32_t tS = tmem + t * 128 + hf * 64 + t_lane, tO = tmem + 256 + t * 128 + hf * 64 + t_lane;
+        const int bar_id = 1 + t * 4 + qd;            // the two halves of these 32 rows
+        const float sl2 = a.scale_log2;
+        float m_run = -INFINITY, l_run = 0.f;
+        for (int64_t j = 0; j < nb; j++) {
+            const int64_t cnt = j < cb ? a.n_cache - j * kTile : a.n_cur - (j - cb) * kTile;
+            const int nvalid = int(cnt < kTile ? cnt : kTile) - hf * 64;     // valid columns of this half
+            attn::bar_wait_nap(&bars.s_full[t], uint32_t(j & 1), a.nap_sm);
+            attn::fence_after();
+            float s[64];
+            tmem_ld64(tS, s);
+            float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                              make_float2(0.f, 0.f)};
+            float m_new, alpha;
+            bool grow;
+            auto phase = [&](auto mask_tag) {
+                constexpr bool MASK = decltype(mask_tag)::value;
+                if constexpr (MASK) {
+#pragma unroll
+                    for (int i = 0; i < 64; i++) s[i] = i < nvalid ? s[i] : -INFINITY;
+                }
+                // 3-input max tree: 64 -> 22 -> 8 -> 3 -> 1, then the other half's
+                float m22[22];
+#pragma unroll
+                for (int i = 0; i < 21; i++) m22[i] = fmaxf(fmaxf(s[3 * i], s[3 * i + 1]), s[3 * i + 2]);
+                m22[21] = s[63];
+                float m8[8];
+#pragma unroll
+                for (int i = 0; i < 7; i++) m8[i] = fmaxf(fmaxf(m22[3 * i], m22[3 * i + 1]), m22[3 * i + 2]);
+                m8[7] = m22[21];
+                const float mh = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                                       fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+                bars.xmax[t][hf][row] = mh;
+                pair_sync(bar_id);
+                const float mx = fmaxf(mh, bars.xmax[t][hf ^ 1][row]) * sl2;
+                grow = mx > m_run + 16.f;     // lazy rescale (identical decision in both halves)
+                m_new = grow ? mx : m_run;
+                alpha = grow ? attn4::ex2_mufu(m_run - m_new) : 1.f;
+                const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_new, -m_new);
+#pragma unroll
+                for (int hq = 0; hq < 2; hq++) {
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int i2 = 0; i2 < 16; i2++) {
+                        const int i = hq * 16 + i2;
+                        const float2 x = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
+                        float2 e;
+                        if (2 * i < POLY_FROM) e = make_float2(attn4::ex2_mufu(x.x), attn4::ex2_mufu(x.y));
+                        else e = attn4::ex2_poly2(make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f)));
+                        if constexpr (MASK) {
+                            e.x = 2 * i < nvalid ? e.x : 0.f;
+                            e.y = 2 * i + 1 < nvalid ? e.y : 0.f;
+                        }
+                        acc4[i2 & 3] = __fadd2_rn(acc4[i2 & 3], e);
+                        pk[i2] = attn::pack_bf16(e.x, e.y);
+                    }
+                    tmem_st16u(tS + hq * 16, pk);
+                }
+            };
+            if (nvalid >= 64) phase(std::false_type{});
+            else phase(std::true_type{});
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            if (j > 0 && __any_sync(0xffffffffu, grow)) {
+#pragma unroll
+                for (int ch = 0; ch < 2; ch++) {
+                    float ov[32];
+                    attn::tmem_ld32(tO + ch * 32, ov);
+#pragma unroll
+                    for (int i = 0; i < 32; i++) ov[i] *= alpha;
+                    attn::tmem_st32(tO + ch * 32, ov);
+                }
+            }
+            const float2 acc = __fadd2_rn(__fadd2_rn(acc4[0], acc4[1]), __fadd2_rn(acc4[2], acc4[3]));
+            l_run = l_run * alpha + (acc.x + acc.y);
+            m_run = m_new;
+            attn::fence_before();
+            attn2::arrive(&bars.p_full[t]);
+        }
+        // ---- epilogue: combine the halves' sums, each half stores 64 columns ----
+        bars.lsum[t][hf][row] = l_run;
+        attn::bar_wait(&bars.o_final, 0);
+        attn::fence_after();
+        pair_sync(bar_id);
+        const float inv_l = 1.f / (bars.lsum[t][0][row] + bars.lsum[t][1][row]);
+        const int64_t qi = q0 + t * kTile + row;
+#pragma unroll
+        for (int ch = 0; ch < 2; ch++) {
+            float ov[32];
+            attn::tmem_ld32(tO + ch * 32, ov);
+            if (qi < a.nq) {
+                uint4 *dst = reinterpret_cast<uint4 *>(a.out + (qi * a.H + h) * kD + hf * 64 + ch * 32);
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    dst[c] = make_uint4(attn::pack_bf16(ov[8 * c] * inv_l, ov[8 * c + 1] * inv_l),
+                                        attn::pack_bf16(ov[8 * c + 2] * inv_l, ov[8 * c + 3] * inv_l),
+                                        attn::pack_bf16(ov[8 * c + 4] * inv_l, ov[8 * c + 5] * inv_l),
+                                        attn::pack_bf16(ov[8 * c + 6] * inv_l, ov[8 * c + 7] * inv_l));
+            }
+        }
+    }
+    attn::fence_before();
+    __syncthreads();
+    if (warp == 17) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const uint16_t *vc, int64_t nq,
+               int64_t nc, int64_t ncur, int H, float scale_log2, uint16_t *out, cudaStream_t st) {
+    CUtensorMap mQ, mKV, mKc, mVc;
+    const bool okq = attn2::make_map(&mQ, q, uint64_t(nq), uint64_t(H) * kD, uint64_t(H) * kD);
+    const bool okkv = nc > 0 ? attn2::make_map(&mKV, kv, uint64_t(2 * H * nc), kD, kD)
+                             : attn2::make_map(&mKV, kc, 1, uint64_t(H) * kD, uint64_t(H) * kD);
+    const bool okk = ncur > 0 ? attn2::make_map(&mKc, kc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
+                              : attn2::make_map(&mKc, q, 1, kD, kD);
+    const bool okv = ncur > 0 ? attn2::make_map(&mVc, vc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
+                              : attn2::make_map(&mVc, q, 1, kD, kD);
+    if (!(okq && okkv && okk && okv)) return set_err(QVG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+    const size_t smem = kSmem + 1024;
+    dim3 grid(unsigned((nq + 2 * kTile - 1) / (2 * kTile)), unsigned(H));
+    attn2::Args args{nq, nc, ncur, H, scale_log2, out};
+    static const int poly = [] { const char *e = getenv("QVG_ATTN_POLY5"); return e ? atoi(e) : 48; }();
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        kern<<<grid, kThreads, smem, st>>>(mQ, mKV, mKc, mVc, args);
+    };
+    nap_args(args);
+    if (poly >= 64) go(k_attention_pp5<64>);
+    else if (poly >= 48) go(k_attention_pp5<48>);
+    else if (poly >= 40) go(k_attention_pp5<40>);
+    else go(k_attention_pp5<32>);
+    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
+}
+}  // namespace attn5
 
 // ============================================================================
 // pre-RoPE key caching: the cache stores keys BEFORE the
@@ -1390,9 +1738,13 @@ int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scal
     } else if (n_cache > 0 && !kv) {
         return set_err(QVG_ERR_BAD_CONFIG, "cache is NULL");
     }
-    static const int use_v3 = [] { const char *e = getenv("QVG_ATTN_KERNEL"); return e && !strcmp(e, "v3"); }();
-    const int rc = use_v3 ? attn3::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st)
-                          : attn4::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st);
+    static const int kern = [] {
+        const char *e = getenv("QVG_ATTN_KERNEL");
+        return !e ? 0 : !strcmp(e, "v3") ? 3 : !strcmp(e, "pp5") ? 5 : 0;
+    }();
+    const int rc = kern == 3 ? attn3::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st)
+                 : kern == 5 ? attn5::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st)
+                             : attn4::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st);
     return rc ? set_err(rc, "attention launch failed: %s", cudaGetErrorString(cudaGetLastError())) : QVG_OK;
 }
 

@@ -348,3 +348,24 @@ def test_dequant_two_stage_add_order_certificate(oracle_lib, c1mag):
     assert np.array_equal(_u32(out), _u32(ref))
     outb = D.dequantize(dc, torch.bfloat16).cpu()
     assert torch.equal(outb.view(torch.int16), torch.from_numpy(ref).to(torch.bfloat16).view(torch.int16))
+
+
+@pytest.mark.parametrize("d,K,S,bits,B", [(64, 64, 2, 2, 64), (256, 32, 2, 4, 64), (128, 256, 1, 2, 64),
+                                          (128, 256, 2, 2, 32), (128, 16, 3, 8, 16)])
+def test_many_planes_shapes_vs_oracle(oracle_lib, d, K, S, bits, B):
+    """>= 148 planes at other head dims / table sizes: d 64 and 256, K 256
+    (one f32 table buffer: the per-plane barrier path), 16-channel groups."""
+    rng = np.random.default_rng(d + K + S)
+    P, N = 150, 40
+    x = _rand_planes(rng, P, N, d, 10.0)
+    cent = torch.from_numpy(rng.normal(0, 1.5, size=(P, S, K, d)).astype(np.float32)).to(torch.bfloat16)
+    asg = torch.from_numpy(rng.integers(0, K, size=(P, S, N)).astype(np.uint8))
+    cfg = QuantConfig(bits=bits, group_size=B, stages=S, centroids=K)
+    pay, sc = D.quantize(x.cuda(), cfg, cent.cuda(), asg.cuda())
+    rp, rs = oracle_lib.quantize_given_metas_batch(x.float().numpy(), cent.float().numpy(), asg.numpy(), bits, B, 8)
+    assert np.array_equal(sc.cpu().numpy(), rs)
+    assert np.array_equal(pay.cpu().numpy(), rp)
+    dc = D.DeviceChunks(cfg, N, d, pay, sc, cent.cuda(), asg.cuda())
+    out = D.dequantize(dc, torch.float32).cpu().numpy()
+    ref = oracle_lib.prq_decompress_batch(rp, rs, cent.float().numpy(), asg.numpy(), N, d, bits, B, 8)
+    assert np.array_equal(_u32(out), _u32(ref))
