@@ -334,6 +334,22 @@ def main():
                 "peak_kind": peak_kind,
                 "per_kernel_frac": {k: round(v["GBps"] / hbm_peak, 4) for k, v in kernels.items()}}
 
+    # streaming warm start (SURVEY 8(f) row 1, Q/prq.py:61-71): chunk 1 encoded
+    # from chunk 0's float64 centroids of the same planes -- k-means++ skipped
+    warm = None
+    if P >= 2 * P_chunk:
+        c0 = D.compress(x[:P_chunk], cfg, chunk_index=0, keep_f64=True, check=False)
+        wms = []
+        for _ in range(3):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            cw = D.compress(x[P_chunk:2 * P_chunk], cfg, chunk_index=1, warm_init=c0.centroids_f64, check=False)
+            torch.cuda.synchronize()
+            wms.append((time.perf_counter() - t0) * 1e3)
+            del cw
+        del c0
+        warm = float(np.median(wms))
+
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_step, 4),
@@ -349,7 +365,10 @@ def main():
         "encode": {"tokens_per_s": round(P_chunk * N / (np.median(enc_ms[1:] or enc_ms) / 1e3), 1),
                    "ms_per_chunk": round(float(np.median(enc_ms[1:] or enc_ms)), 2),
                    "planes_per_chunk": P_chunk,
-                   "note": "full prq_compress (k-means++ / Lloyd / smoothing / quantize), one chunk"},
+                   "note": "full prq_compress (k-means++ / Lloyd / smoothing / quantize), one chunk",
+                   "warm_ms_per_chunk": None if warm is None else round(warm, 2),
+                   "warm_tokens_per_s": None if warm is None else round(P_chunk * N / (warm / 1e3), 1),
+                   "warm_note": "streaming warm start: the previous chunk's float64 centroids as init"},
         "gpu_launches": 2 * args.steps,
         "clocks": clk.summary(),
     }

@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "qvg_common.cuh"
 #include "qvg_internal.h"
@@ -451,6 +452,8 @@ __global__ void __launch_bounds__(1024) k_members(MemberArgs a) {
 // K3b: per (cluster, channel) ordered sums = np.add.at, then / count.
 struct SumArgs {
     const double *rows;
+    const float *rows32;        // exact float32 copy when rows32_ok[p] (half the bytes)
+    const int32_t *rows32_ok;
     double *cent;
     const int32_t *counts, *offsets, *members;
     const PlaneState *st;
@@ -466,20 +469,23 @@ __global__ void __launch_bounds__(128) k_sums(SumArgs a) {
     const int cnt = a.counts[p * K + j];
     if (cnt == 0) return;                         // keep the old centroid
     const int32_t *mem = a.members + p * a.N + a.offsets[p * (K + 1) + j];
-    const double *rows = a.rows + p * a.N * d;
-    for (int k = threadIdx.x; k < d; k += blockDim.x) {
-        double acc = 0.0;
-        int t = 0;
-        for (; t + 8 <= cnt; t += 8) {
-            double v[8];
+    auto body = [&](auto rows) {
+        for (int k = threadIdx.x; k < d; k += blockDim.x) {
+            double acc = 0.0;
+            int t = 0;
+            for (; t + 8 <= cnt; t += 8) {
+                double v[8];
 #pragma unroll
-            for (int u = 0; u < 8; u++) v[u] = rows[int64_t(mem[t + u]) * d + k];
+                for (int u = 0; u < 8; u++) v[u] = double(rows[int64_t(mem[t + u]) * d + k]);
 #pragma unroll
-            for (int u = 0; u < 8; u++) acc = __dadd_rn(acc, v[u]);
+                for (int u = 0; u < 8; u++) acc = __dadd_rn(acc, v[u]);
+            }
+            for (; t < cnt; t++) acc = __dadd_rn(acc, double(rows[int64_t(mem[t]) * d + k]));
+            a.cent[(p * K + j) * int64_t(d) + k] = __ddiv_rn(acc, double(cnt));
         }
-        for (; t < cnt; t++) acc = __dadd_rn(acc, rows[int64_t(mem[t]) * d + k]);
-        a.cent[(p * K + j) * int64_t(d) + k] = __ddiv_rn(acc, double(cnt));
-    }
+    };
+    if (a.rows32 && a.rows32_ok[p]) body(a.rows32 + p * a.N * d);
+    else body(a.rows + p * a.N * d);
 }
 
 // K3c: empty-cluster repair (one CTA of 1024 per plane; returns at once when
@@ -560,6 +566,8 @@ __global__ void __launch_bounds__(1024) k_repair(RepairArgs a) {
 // ------------------------------------------------------------------------
 struct ObjArgs {
     const double *rows;
+    const float *rows32;        // exact float32 copy when rows32_ok[p]
+    const int32_t *rows32_ok;
     const double *cent;
     const int32_t *assign;
     double *nodes;            // [P][n_nodes]
@@ -572,6 +580,7 @@ struct ObjArgs {
     int d, K;
     int mode;                 // 0: initial objective -> prev; 1: Lloyd step + tol test; 2: objective only
     double tol;
+    int lgd;                  // log2(d) when d is a power of two, else -1
 };
 
 __global__ void __launch_bounds__(256) k_obj_leaves(ObjArgs a) {
@@ -585,16 +594,27 @@ __global__ void __launch_bounds__(256) k_obj_leaves(ObjArgs a) {
     const int j8 = threadIdx.x & 7;
     const int64_t wg = (blockIdx.x * int64_t(blockDim.x) + threadIdx.x) >> 5;   // global warp
     const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t L0 = wg * 4; L0 < a.n_leaves; L0 += nw * 4) {                // warp-uniform
-        const int64_t L = L0 + ((threadIdx.x & 31) >> 3);
-        const int64_t LL = L < a.n_leaves ? L : a.n_leaves - 1;
-        double s = leaf_sum8(a.lf_off[LL], a.lf_len[LL], j8, [&](int64_t e) {
-            int64_t row = e / d;
-            int col = int(e - row * d);
-            double t = __dsub_rn(rows[e], cent[int64_t(asg[row]) * d + col]);
-            return __dmul_rn(t, t);
-        });
-        if (j8 == 0 && L < a.n_leaves) a.nodes[p * n_nodes + L] = s;
+    auto run = [&](auto rw, auto pow2) {
+        constexpr bool P2 = decltype(pow2)::value;
+        for (int64_t L0 = wg * 4; L0 < a.n_leaves; L0 += nw * 4) {            // warp-uniform
+            const int64_t L = L0 + ((threadIdx.x & 31) >> 3);
+            const int64_t LL = L < a.n_leaves ? L : a.n_leaves - 1;
+            double s = leaf_sum8(a.lf_off[LL], a.lf_len[LL], j8, [&](int64_t e) {
+                const int64_t row = P2 ? e >> a.lgd : e / d;
+                const int col = P2 ? int(e & (d - 1)) : int(e - row * d);
+                double t = __dsub_rn(double(rw[e]), cent[int64_t(asg[row]) * d + col]);
+                return __dmul_rn(t, t);
+            });
+            if (j8 == 0 && L < a.n_leaves) a.nodes[p * n_nodes + L] = s;
+        }
+    };
+    const bool r32 = a.rows32 && a.rows32_ok[p];
+    if (a.lgd >= 0) {
+        if (r32) run(a.rows32 + p * a.N * d, std::true_type{});
+        else run(rows, std::true_type{});
+    } else {
+        if (r32) run(a.rows32 + p * a.N * d, std::false_type{});
+        else run(rows, std::false_type{});
     }
 }
 
@@ -677,8 +697,10 @@ int launch_widen(const void *x, int xbf16, double *rows, int64_t n, int32_t *sta
 
 static void objective(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int mode,
                       double tol, cudaStream_t st) {
-    ObjArgs o{b.rows, b.cent, b.assign, b.nodes, b.st, b.ob_off, b.ob_len, b.nd_l, b.nd_r,
-              b.h_start, b.ob_leaves, b.ob_heights, N, d, K, mode, tol};
+    const int lgd = (d & (d - 1)) == 0 ? __builtin_ctz(unsigned(d)) : -1;
+    ObjArgs o{b.rows, b.rows32_valid ? b.rows32 : nullptr, b.rows32_ok, b.cent, b.assign, b.nodes, b.st,
+              b.ob_off, b.ob_len, b.nd_l, b.nd_r, b.h_start, b.ob_leaves, b.ob_heights, N, d, K, mode, tol,
+              lgd};
     dim3 g((unsigned)((int64_t(b.ob_leaves) * 8 + 255) / 256 < 4096 ? (int64_t(b.ob_leaves) * 8 + 255) / 256 : 4096),
            (unsigned)P);
     k_obj_leaves<<<g, 256, 0, st>>>(o);
@@ -727,7 +749,7 @@ static void lloyd_body(const KMeansBuffers &b, int64_t P, int64_t N, int d, int 
     assign_step(b, P, N, d, K, 1, st);
     MemberArgs ma{b.assign, b.counts, b.offsets, b.members, b.st, N, K};
     k_members<<<(unsigned)P, 1024, msmem, st>>>(ma);
-    SumArgs sa{b.rows, b.cent, b.counts, b.offsets, b.members, b.st, N, d, K};
+    SumArgs sa{b.rows, b.rows32_valid ? b.rows32 : nullptr, b.rows32_ok, b.cent, b.counts, b.offsets, b.members, b.st, N, d, K};
     k_sums<<<dim3((unsigned)K, (unsigned)P), 128, 0, st>>>(sa);
     RepairArgs ra{b.rows, b.cent, b.assign, b.counts, b.d2, b.st, N, d, K};
     k_repair<<<(unsigned)P, 1024, 0, st>>>(ra);
