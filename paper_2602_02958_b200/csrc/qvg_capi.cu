@@ -122,6 +122,9 @@ static void carve_kmeans(Carver &c, int64_t P, int64_t N, int d, int K, bool own
     b.pk_off = c.take<int64_t>(Lp);
     b.pk_len = c.take<int32_t>(Lp);
     b.pk_leaves = int(Lp);
+    b.pk_l = c.take<int32_t>(Lp);
+    b.pk_r = c.take<int32_t>(Lp);
+    b.pk_hstart = c.take<int32_t>(80);
     b.ob_off = c.take<int64_t>(Lo);
     b.ob_len = c.take<int32_t>(Lo);
     b.nd_l = c.take<int32_t>(Lo);
@@ -145,6 +148,13 @@ static int upload_plans(KMeansBuffers &b, int64_t N, int d, cudaStream_t st) {
     build_plan(N, pp);
     if (po.heights > 78) return set_err(QVG_ERR_UNSUPPORTED, "pairwise tree too deep");
     b.ob_heights = po.heights;
+    if (pp.heights > 78) return set_err(QVG_ERR_UNSUPPORTED, "pairwise tree too deep");
+    b.pk_heights = pp.heights;
+    if (!pp.l.empty()) {
+        cudaMemcpyAsync(b.pk_l, pp.l.data(), pp.l.size() * 4, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(b.pk_r, pp.r.data(), pp.r.size() * 4, cudaMemcpyHostToDevice, st);
+    }
+    cudaMemcpyAsync(b.pk_hstart, pp.hstart.data(), pp.hstart.size() * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(b.pk_off, pp.off.data(), pp.off.size() * 8, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(b.pk_len, pp.len.data(), pp.len.size() * 4, cudaMemcpyHostToDevice, st);
     cudaMemcpyAsync(b.ob_off, po.off.data(), po.off.size() * 8, cudaMemcpyHostToDevice, st);

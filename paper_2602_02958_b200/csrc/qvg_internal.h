@@ -22,6 +22,8 @@ struct KMeansBuffers {
     int64_t *pk_off;
     int32_t *pk_len;
     int pk_leaves;
+    int32_t *pk_l, *pk_r, *pk_hstart;   // numpy recursion tree over the N-long pick weights
+    int pk_heights;
     int64_t *ob_off;
     int32_t *ob_len, *nd_l, *nd_r, *h_start;
     int ob_leaves, ob_heights;

@@ -44,16 +44,6 @@ __device__ __forceinline__ double row_pairwise8(int d, int j, F v) {
     return acc;
 }
 
-// numpy pairwise recursion over precomputed leaf sums (leaves in order).
-__device__ double pw_combine(const double *leaf, int64_t n, int &cur) {
-    if (n <= 128) return leaf[cur++];
-    int64_t h = n / 2;
-    h -= h % 8;
-    double a = pw_combine(leaf, h, cur);
-    double b = pw_combine(leaf, n - h, cur);
-    return __dadd_rn(a, b);
-}
-
 // leaf sum of v over [off, off+len), 8 lanes (len <= 128); numpy leaf rule.
 template <typename F>
 __device__ __forceinline__ double leaf_sum8(int64_t off, int len, int j, F v) {
@@ -97,6 +87,8 @@ struct PPArgs {
     int n_leaves;
     int64_t N;
     int d, K;
+    const int32_t *nd_l, *nd_r, *h_start;   // internal nodes of the pick tree, by height
+    int n_heights;
 };
 
 // rows read as T (double, or float when the plane's float64 rows are all exactly
@@ -104,7 +96,8 @@ struct PPArgs {
 template <typename T>
 __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const T *rows_all, double *sm) {
     double *xc = sm;                       // [d]
-    double *leaf = sm + 128;               // [n_leaves]
+    double *leaf = sm + 128;               // [n_leaves] leaves, then the internal nodes
+    double *dr = leaf + 2 * a.n_leaves - 1;   // [K] this plane's draws
     __shared__ double s_total;
     __shared__ int64_t s_pick;
     __shared__ double s_wsum[32];
@@ -119,6 +112,7 @@ __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const T *rows_all
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int j8 = lane & 7;
 
+    for (int k = tid; k < K; k += blockDim.x) dr[k] = draws[k];
     if (tid == 0) {
         int64_t c = int64_t(draws[0] * double(N));
         s_pick = c < N - 1 ? c : N - 1;
@@ -189,12 +183,17 @@ __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const T *rows_all
             if (j8 == 0 && L < a.n_leaves) leaf[L] = s;
         }
         __syncthreads();
-        if (tid == 0) {
-            int cur = 0;
-            s_total = __dadd_rn(0.0, pw_combine(leaf, N, cur));
+        if (warp == 0) {            // the numpy recursion, level by level (host-built tree)
+            const int nl = a.n_leaves;
+            for (int hh = 0; hh < a.n_heights; hh++) {
+                for (int i = a.h_start[hh] + lane; i < a.h_start[hh + 1]; i += 32)
+                    leaf[nl + i] = __dadd_rn(leaf[a.nd_l[i]], leaf[a.nd_r[i]]);
+                __syncwarp();
+            }
+            if (lane == 0) s_total = __dadd_rn(0.0, leaf[nl > 1 ? 2 * nl - 2 : 0]);
         }
         __syncthreads();
-        const double r = draws[pk + 1];
+        const double r = dr[pk + 1];
         const double total = s_total;
         if (!(total > 0.0)) {     // uniform fallback (Q/clustering.py:41-42)
             if (tid == 0) {
@@ -733,8 +732,9 @@ static void assign_step(const KMeansBuffers &b, int64_t P, int64_t N, int d, int
 
 int run_kmeanspp(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, const double *draws,
                  int64_t draws_stride, cudaStream_t st) {
-    PPArgs pa{b.rows, b.rows32_valid ? b.rows32 : nullptr, b.rows32_ok, draws, draws_stride, b.cent, b.d2, b.pk_off, b.pk_len, b.pk_leaves, N, d, K};
-    size_t smem = sizeof(double) * (128 + b.pk_leaves);
+    PPArgs pa{b.rows, b.rows32_valid ? b.rows32 : nullptr, b.rows32_ok, draws, draws_stride, b.cent, b.d2, b.pk_off, b.pk_len, b.pk_leaves, N, d, K,
+              b.pk_l, b.pk_r, b.pk_hstart, b.pk_heights};
+    size_t smem = sizeof(double) * (128 + 2 * b.pk_leaves - 1 + K);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_kmeanspp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_kmeanspp<<<(unsigned)P, 1024, smem, st>>>(pa);
