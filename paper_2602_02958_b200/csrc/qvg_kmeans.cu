@@ -89,6 +89,7 @@ struct PPArgs {
     int d, K;
     const int32_t *nd_l, *nd_r, *h_start;   // internal nodes of the pick tree, by height
     int n_heights;
+    int d2_smem;             // 1: the N pick weights live in shared memory (after the draws)
 };
 
 // rows read as T (double, or float when the plane's float64 rows are all exactly
@@ -106,7 +107,7 @@ __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const T *rows_all
     const int64_t N = a.N;
     const int d = a.d, K = a.K;
     const T *rows = rows_all + p * N * d;
-    double *d2 = a.d2 + p * N;
+    double *d2 = a.d2_smem ? sm + 128 + 2 * a.n_leaves - 1 + K : a.d2 + p * N;
     double *cent = a.cent + p * int64_t(K) * d;
     const double *draws = a.draws + p * a.draws_stride;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -733,8 +734,13 @@ static void assign_step(const KMeansBuffers &b, int64_t P, int64_t N, int d, int
 int run_kmeanspp(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, const double *draws,
                  int64_t draws_stride, cudaStream_t st) {
     PPArgs pa{b.rows, b.rows32_valid ? b.rows32 : nullptr, b.rows32_ok, draws, draws_stride, b.cent, b.d2, b.pk_off, b.pk_len, b.pk_leaves, N, d, K,
-              b.pk_l, b.pk_r, b.pk_hstart, b.pk_heights};
+              b.pk_l, b.pk_r, b.pk_hstart, b.pk_heights, 0};
     size_t smem = sizeof(double) * (128 + 2 * b.pk_leaves - 1 + K);
+    // the pick weights in shared memory while two 1024-thread CTAs still fit per SM
+    if (smem + sizeof(double) * N <= 100 * 1024) {
+        smem += sizeof(double) * N;
+        pa.d2_smem = 1;
+    }
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_kmeanspp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_kmeanspp<<<(unsigned)P, 1024, smem, st>>>(pa);
