@@ -238,6 +238,7 @@ int qvg_compress(const void *x, int32_t x_dtype, int64_t P, int64_t N, int32_t d
                 cudaMemcpy2DAsync(b.cent, size_t(K) * d * 8, warm_init + int64_t(t) * K * d,
                                   size_t(S) * K * d * 8, size_t(K) * d * 8, size_t(P),
                                   cudaMemcpyDeviceToDevice, st);
+            b.src16 = (t == 0 && x_dtype == QVG_DTYPE_BF16) ? static_cast<const uint16_t *>(x) : nullptr;
             rc = run_kmeans_stage(b, P, N, d, K, cfg->kmeans_max_iters, cfg->kmeans_tol,
                                   warm ? nullptr : pp_draws + int64_t(t) * K, int64_t(S) * K, warm, st);
             if (rc) return set_err(rc, "k-means stage %d: %s", t, cudaGetErrorString(cudaGetLastError()));

@@ -35,6 +35,7 @@ struct KMeansBuffers {
     float *rows32;         // [P][N][d] float32 copy of the stage rows (k_split_rows)
     int32_t *rows32_ok;    // [P] nonzero: the copy is exact for the whole plane
     int rows32_valid;      // set once k_split_rows has filled rows32 for the current rows
+    const uint16_t *src16; // the bf16 input when the current rows are exactly it (stage 1 of a bf16 chunk)
 };
 
 // qvg_codec.cu

@@ -77,6 +77,7 @@ __global__ void k_widen(const void *x, int xbf16, double *rows, int64_t n, int32
 struct PPArgs {
     const double *rows;      // [P][N][d]
     const float *rows32;     // [P][N][d] float32 copy (nullable)
+    const uint16_t *rows16;  // [P][N][d] the bf16 input when the rows are exactly it (nullable)
     const int32_t *rows32_ok;   // [P] 1: the copy is exact
     const double *draws;     // this stage's draws of plane 0; plane p at + p*draws_stride
     int64_t draws_stride;
@@ -94,8 +95,52 @@ struct PPArgs {
 
 // rows read as T (double, or float when the plane's float64 rows are all exactly
 // representable in float32, see k_split_rows): identical values, half the bytes
+// a bf16 element read as its exact double value
+struct Bf16 {
+    uint16_t v;
+    __device__ __forceinline__ operator double() const { return double(__uint_as_float(uint32_t(v) << 16)); }
+};
+
+__device__ __forceinline__ void bf16x8_to_f64(uint4 w, double v[8]) {
+    const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int h = 0; h < 4; h++) {
+        v[2 * h] = double(__uint_as_float(u[h] << 16));
+        v[2 * h + 1] = double(__uint_as_float(u[h] & 0xFFFF0000u));
+    }
+}
+
+// Row sources: row(i)[k] is the exact double value of element (i, k);
+// load8(i, k0, v) fetches elements k0..k0+7 (k0 % 8 == 0) with vector loads.
 template <typename T>
-__device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const T *rows_all, double *sm) {
+struct SrcPlain {                       // rows stored as T (double / float / bf16)
+    static constexpr int kBytes = sizeof(T);
+    const T *rows;
+    int d;
+    struct Row {
+        const T *r;
+        __device__ __forceinline__ double operator[](int k) const { return double(r[k]); }
+    };
+    __device__ __forceinline__ Row row(int64_t i) const { return Row{rows + i * d}; }
+    __device__ __forceinline__ void load8(int64_t i, int k0, double v[8]) const {
+        const T *r = rows + i * d + k0;
+        if constexpr (sizeof(T) == 2) {
+            bf16x8_to_f64(*reinterpret_cast<const uint4 *>(r), v);
+        } else if constexpr (sizeof(T) == 4) {
+            const float4 a = reinterpret_cast<const float4 *>(r)[0], b = reinterpret_cast<const float4 *>(r)[1];
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+        } else {
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+                const double2 t = reinterpret_cast<const double2 *>(r)[h];
+                v[2 * h] = t.x;
+                v[2 * h + 1] = t.y;
+            }
+        }
+    }
+};
+template <typename Src>
+__device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const Src src, double *sm) {
     double *xc = sm;                       // [d]
     double *leaf = sm + 128;               // [n_leaves] leaves, then the internal nodes
     double *dr = leaf + 2 * a.n_leaves - 1;   // [K] this plane's draws
@@ -106,7 +151,6 @@ __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const T *rows_all
     const int64_t p = blockIdx.x;
     const int64_t N = a.N;
     const int d = a.d, K = a.K;
-    const T *rows = rows_all + p * N * d;
     double *d2 = a.d2_smem ? sm + 128 + 2 * a.n_leaves - 1 + K : a.d2 + p * N;
     double *cent = a.cent + p * int64_t(K) * d;
     const double *draws = a.draws + p * a.draws_stride;
@@ -121,28 +165,49 @@ __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const T *rows_all
     __syncthreads();
     for (int pk = 0; pk < K; pk++) {
         const int64_t c = s_pick;
+        const auto rc = src.row(c);
         for (int k = tid; k < d; k += blockDim.x) {
-            double v = double(rows[c * d + k]);
+            double v = rc[k];
             xc[k] = v;
             cent[int64_t(pk) * d + k] = v;
         }
         __syncthreads();
         if (pk == K - 1) break;
         // d2 = min(d2, ((rows - rows[c])**2).sum(axis=1))
-        if (d == 128) {
-            // head_dim 128: all 16 loads of a lane issued before the (ordered) sums,
-            // two rows per 8-lane group in flight
+        if (d == 128 && Src::kBytes == 2) {
+            // head_dim 128, bf16 rows: one row per thread, the eight numpy pairwise-8
+            // accumulators in registers (r_j = sum over i of t(8i + j), i = 0..15, in
+            // order, then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))); 16-byte loads
+            for (int64_t i = tid; i < N; i += blockDim.x) {
+                double r[8];
+#pragma unroll
+                for (int q = 0; q < 16; q++) {
+                    double v[8];
+                    src.load8(i, q * 8, v);
+#pragma unroll
+                    for (int j = 0; j < 8; j++) {
+                        const double t = __dsub_rn(v[j], xc[q * 8 + j]);
+                        r[j] = q == 0 ? __dmul_rn(t, t) : __dadd_rn(r[j], __dmul_rn(t, t));
+                    }
+                }
+                const double sum = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                                             __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+                const double dist = __dadd_rn(0.0, sum);
+                d2[i] = (pk == 0 || dist < d2[i]) ? dist : d2[i];
+            }
+        } else if (d == 128) {
+            // head_dim 128, float / double rows: 8 lanes per row, all 16 loads of a lane
+            // issued before the (ordered) sums, two rows per 8-lane group in flight
             double xcl[16];
 #pragma unroll
             for (int q = 0; q < 16; q++) xcl[q] = xc[q * 8 + j8];
             const int64_t step = blockDim.x >> 3;                      // rows per CTA pass
             for (int64_t i0 = int64_t(warp) * 4; i0 < N; i0 += 2 * step) {   // warp-uniform
                 const int64_t ia = i0 + (lane >> 3), ib = ia + step;
-                const T *ra = rows + (ia < N ? ia : N - 1) * 128 + j8;
-                const T *rb = rows + (ib < N ? ib : N - 1) * 128 + j8;
+                const auto ra = src.row(ia < N ? ia : N - 1), rb = src.row(ib < N ? ib : N - 1);
                 double va[16], vb[16];
 #pragma unroll
-                for (int q = 0; q < 16; q++) { va[q] = double(ra[q * 8]); vb[q] = double(rb[q * 8]); }
+                for (int q = 0; q < 16; q++) { va[q] = ra[q * 8 + j8]; vb[q] = rb[q * 8 + j8]; }
                 double sa, sb;
                 {
                     double t = __dsub_rn(va[0], xcl[0]);
@@ -166,9 +231,9 @@ __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const T *rows_all
             for (int64_t i0 = int64_t(warp) * 4; i0 < N; i0 += blockDim.x >> 3) {  // warp-uniform
                 const int64_t i = i0 + (lane >> 3);
                 const int64_t ii = i < N ? i : N - 1;
-                const T *ri = rows + ii * d;
+                const auto ri = src.row(ii);
                 double dist = row_pairwise8(d, j8, [&](int k) {
-                    double t = __dsub_rn(double(ri[k]), xc[k]);
+                    double t = __dsub_rn(ri[k], xc[k]);
                     return __dmul_rn(t, t);
                 });
                 dist = __dadd_rn(0.0, dist);
@@ -269,8 +334,14 @@ __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const T *rows_all
 
 __global__ void __launch_bounds__(1024) k_kmeanspp(PPArgs a) {
     extern __shared__ double sm[];
-    if (a.rows32 && a.rows32_ok[blockIdx.x]) kmeanspp_body<float>(a, a.rows32, sm);
-    else kmeanspp_body<double>(a, a.rows, sm);
+    const int64_t p = blockIdx.x, nd = a.N * a.d;
+    if (a.rows16) {
+        kmeanspp_body(a, SrcPlain<Bf16>{reinterpret_cast<const Bf16 *>(a.rows16) + p * nd, a.d}, sm);
+    } else if (a.rows32 && a.rows32_ok[p]) {
+        kmeanspp_body(a, SrcPlain<float>{a.rows32 + p * nd, a.d}, sm);
+    } else {
+        kmeanspp_body(a, SrcPlain<double>{a.rows + p * nd, a.d}, sm);
+    }
 }
 
 // ------------------------------------------------------------------------
@@ -733,7 +804,7 @@ static void assign_step(const KMeansBuffers &b, int64_t P, int64_t N, int d, int
 
 int run_kmeanspp(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, const double *draws,
                  int64_t draws_stride, cudaStream_t st) {
-    PPArgs pa{b.rows, b.rows32_valid ? b.rows32 : nullptr, b.rows32_ok, draws, draws_stride, b.cent, b.d2, b.pk_off, b.pk_len, b.pk_leaves, N, d, K,
+    PPArgs pa{b.rows, b.rows32_valid ? b.rows32 : nullptr, b.src16, b.rows32_ok, draws, draws_stride, b.cent, b.d2, b.pk_off, b.pk_len, b.pk_leaves, N, d, K,
               b.pk_l, b.pk_r, b.pk_hstart, b.pk_heights, 0};
     size_t smem = sizeof(double) * (128 + 2 * b.pk_leaves - 1 + K);
     // the pick weights in shared memory while two 1024-thread CTAs still fit per SM
