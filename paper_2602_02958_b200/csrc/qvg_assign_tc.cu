@@ -201,8 +201,11 @@ __global__ void __launch_bounds__(128, 1) k_assign_tc(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem, *sB = smem + kSmemA;
-    double *c2s = reinterpret_cast<double *>(sB + kSmemB);
-    float *cns = reinterpret_cast<float *>(c2s + kNB);
+    // per centroid of the block: c2 rounded to f32, and the two bound coefficients
+    // t1 = 2^-15 |c| and t2 = 2^-22 |c2f| (both rounded up)
+    float *c2f = reinterpret_cast<float *>(sB + kSmemB);
+    float *t2s = c2f + kNB;
+    float *t1s = t2s + kNB;
     __shared__ uint64_t bar_a, bar_mma;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5;
@@ -229,20 +232,31 @@ __global__ void __launch_bounds__(128, 1) k_assign_tc(TcArgs a) {
     const int64_t it1 = (int64_t(blockIdx.x + 1) * n_items) / gridDim.x;
     int64_t cur_p = -1;
     uint32_t pa = 0, pm = 0;          // barrier phases
-    for (int64_t it = it0; it < it1; it++) {
+    // the next item this CTA processes (planes already converged are skipped)
+    auto next_item = [&](int64_t from) {
+        while (from < it1 && a.skip_done && a.st[from / a.T].done) from++;
+        return from;
+    };
+    // stream a row tile (3 splits, one contiguous bulk copy); the next item's tile
+    // is requested as soon as the current item's last MMAs are done, so its
+    // transfer overlaps the epilogue
+    auto load_tile = [&](int64_t item) {
+        if (tid == 0 && item < it1) {
+            expect_tx(&bar_a, uint32_t(kSmemA));
+            bulk_g2s(sA, reinterpret_cast<const uint8_t *>(a.split) + size_t(item) * kSmemA, uint32_t(kSmemA), &bar_a);
+        }
+    };
+    int64_t it = next_item(it0);
+    load_tile(it);
+    for (; it < it1;) {
         const int64_t p = it / a.T;
         const int t = int(it - p * a.T);
-        if (a.skip_done && a.st[p].done) continue;
+        const int64_t it_next = next_item(it + 1);
         const int nblk = (K + kNB - 1) / kNB;
-        // stream the row tile (3 splits, one contiguous bulk copy)
-        if (tid == 0) {
-            expect_tx(&bar_a, uint32_t(kSmemA));
-            bulk_g2s(sA, reinterpret_cast<const uint8_t *>(a.split) + size_t(it) * kSmemA, uint32_t(kSmemA), &bar_a);
-        }
         const int64_t row = int64_t(t) * kM + tid;
         const float xn = row < a.N ? a.xnorm[p * a.N + row] : 0.f;
         // online certified argmin state (thread = row)
-        double bestD = 0.0, bestE = 0.0, others = INFINITY;
+        float bestD = 0.f, bestE = 0.f, others = INFINITY;
         int bestj = -1;
         for (int blk = 0; blk < nblk; blk++) {
             const int j0 = blk * kNB, nb = min(kNB, K - j0);
@@ -275,8 +289,10 @@ __global__ void __launch_bounds__(128, 1) k_assign_tc(TcArgs a) {
                             const double c = a.cent[(p * K + j0 + j) * kD + k];
                             ss = fma(c, c, ss);
                         }
-                    c2s[j] = j < nb ? a.c2[p * K + j0 + j] : 0.0;
-                    cns[j] = float(sqrt(ss) * (1.0 + 1e-6));
+                    const float cf = j < nb ? __double2float_rn(a.c2[p * K + j0 + j]) : 0.f;
+                    c2f[j] = cf;
+                    t2s[j] = __fmul_ru(fabsf(cf), 2.384185791015625e-07f);          // 2^-22
+                    t1s[j] = __fmul_ru(float(sqrt(ss) * (1.0 + 1e-6)), 3.0517578125e-05f);   // 2^-15
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor core
                 __syncthreads();
@@ -308,6 +324,7 @@ __global__ void __launch_bounds__(128, 1) k_assign_tc(TcArgs a) {
             bar_wait(&bar_mma, pm);
             pm ^= 1u;
             fence_after();
+            if (blk == nblk - 1) load_tile(it_next);     // sA no longer read by this item's MMAs
             // ---- epilogue: 32 centroids at a time
             for (int c0 = 0; c0 < nb; c0 += 32) {
                 float cr[32], tmp[32];
@@ -319,19 +336,38 @@ __global__ void __launch_bounds__(128, 1) k_assign_tc(TcArgs a) {
                     for (int i = 0; i < 32; i++) cr[i] += tmp[i];
                 }
                 const int nn = min(32, nb - c0);
+                // certified argmin in f32 with directed rounding: D = c2f - 2 cross (one
+                // rounding), E = 2^-15 |x||c| + 2^-22 (|c2f| + 2 |cross|) covers the split /
+                // accumulation error of the cross term, c2 -> f32 and the rounding of D;
+                // two independent chains (even / odd centroids), merged below
+                float bD[2], bE[2], oth[2] = {INFINITY, INFINITY};
+                int bj[2] = {-1, -1};
 #pragma unroll
                 for (int i = 0; i < 32; i++) {
                     if (i >= nn) break;
-                    const int j = c0 + i;
-                    const double D = c2s[j] - 2.0 * double(cr[i]);
-                    const double E = 3.0517578125e-05 * double(xn) * double(cns[j]) +
-                                     1.1920928955078125e-07 * (fabs(c2s[j]) + 2.0 * fabs(double(cr[i])));
-                    if (bestj < 0) { bestD = D; bestE = E; bestj = j0 + j; }
-                    else if (D < bestD) {
-                        others = fmin(others, bestD - bestE);
-                        bestD = D; bestE = E; bestj = j0 + j;
+                    const int j = c0 + i, ch = i & 1;
+                    const float D = __fmaf_rn(-2.f, cr[i], c2f[j]);
+                    const float E = __fmaf_ru(xn, t1s[j], __fmaf_ru(fabsf(cr[i]), 4.76837158203125e-07f, t2s[j]));
+                    if (bj[ch] < 0) { bD[ch] = D; bE[ch] = E; bj[ch] = j0 + j; }
+                    else if (D < bD[ch]) {
+                        oth[ch] = fminf(oth[ch], __fsub_rd(bD[ch], bE[ch]));
+                        bD[ch] = D; bE[ch] = E; bj[ch] = j0 + j;
                     } else {
-                        others = fmin(others, D - E);
+                        oth[ch] = fminf(oth[ch], __fsub_rd(D, E));
+                    }
+                }
+                // merge the chains and the running state (ties are never certified:
+                // the loser's D - E <= the winner's D keeps `others` below bestD + bestE)
+#pragma unroll
+                for (int ch = 0; ch < 2; ch++) {
+                    if (bj[ch] < 0) continue;
+                    others = fminf(others, oth[ch]);
+                    if (bestj < 0) { bestD = bD[ch]; bestE = bE[ch]; bestj = bj[ch]; }
+                    else if (bD[ch] < bestD || (bD[ch] == bestD && bj[ch] < bestj)) {
+                        others = fminf(others, __fsub_rd(bestD, bestE));
+                        bestD = bD[ch]; bestE = bE[ch]; bestj = bj[ch];
+                    } else {
+                        others = fminf(others, __fsub_rd(bD[ch], bE[ch]));
                     }
                 }
             }
@@ -339,10 +375,11 @@ __global__ void __launch_bounds__(128, 1) k_assign_tc(TcArgs a) {
             __syncthreads();                 // TMEM / sB reads done before the next MMAs
         }
         if (row < a.N) {
-            const bool ok = others > bestD + bestE;
+            const bool ok = others > __fadd_ru(bestD, bestE);
             a.assign[p * a.N + row] = ok ? bestj : -1;
             if (!ok) a.recheck[atomicAdd(a.n_recheck, 1)] = int32_t(p * a.N + row);
         }
+        it = it_next;
     }
     fence_before();
     __syncthreads();
