@@ -54,7 +54,8 @@ __device__ __forceinline__ double leaf_sum8(int64_t off, int len, int j, F v) {
     }
     const int m = len >> 3;
     double acc = v(off + j);
-    for (int i = 1; i < m; i++) acc = __dadd_rn(acc, v(off + i * 8 + j));
+#pragma unroll 4
+    for (int i = 1; i < m; i++) acc = __dadd_rn(acc, v(off + i * 8 + j));   // loads of 4 terms in flight
     acc = pairwise8_tree(acc);
     for (int k = m * 8; k < len; k++) acc = __dadd_rn(acc, v(off + k));
     return acc;
