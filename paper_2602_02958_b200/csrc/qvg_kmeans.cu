@@ -736,16 +736,24 @@ __global__ void k_finalize_cent(const double *cent, uint16_t *cent_out, double *
 __global__ void k_residual(double *rows, const double *cent, const int32_t *assign,
                            uint8_t *assign_out, int32_t *iters_out, const PlaneState *st,
                            int64_t P, int64_t N, int S, int t, int K, int d) {
-    const int64_t n = P * N * d;
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-        int64_t p = i / (N * d), e = i - p * N * d, row = e / d;
-        int col = int(e - row * d);
-        int c = assign[p * N + row];
-        float cb = bf16_to_f32(f32_to_bf16_bits_rne(__double2float_rn(cent[(p * K + c) * int64_t(d) + col])));
-        rows[i] = __dsub_rn(rows[i], double(cb));
-        if (col == 0) assign_out[(p * S + t) * N + row] = uint8_t(c);
-        if (e == 0 && iters_out) iters_out[p * S + t] = st[p].iters;
+    // grid.y = plane, one row per 32-thread group (no 64-bit divisions per element)
+    const int64_t p = blockIdx.y;
+    double *pr = rows + p * N * d;
+    const double *pc = cent + p * int64_t(K) * d;
+    const int32_t *pa = assign + p * N;
+    const int lane = threadIdx.x & 31;
+    for (int64_t row = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < N;
+         row += (int64_t(gridDim.x) * blockDim.x) >> 5) {
+        const int c = pa[row];
+        const double *cr = pc + int64_t(c) * d;
+        double *rr = pr + row * d;
+        for (int col = lane; col < d; col += 32) {
+            const float cb = bf16_to_f32(f32_to_bf16_bits_rne(__double2float_rn(cr[col])));
+            rr[col] = __dsub_rn(rr[col], double(cb));
+        }
+        if (lane == 0) assign_out[(p * S + t) * N + row] = uint8_t(c);
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && iters_out) iters_out[p * S + t] = st[p].iters;
 }
 
 __global__ void k_stage_reset(PlaneState *st, int64_t P) {
@@ -911,8 +919,9 @@ int finalize_stage(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, i
                    uint16_t *cent_out, double *cent64_out, uint8_t *assign_out, int32_t *iters_out,
                    cudaStream_t st) {
     k_finalize_cent<<<g1d(P * K * d, 256), 256, 0, st>>>(b.cent, cent_out, cent64_out, P, S, t, K, d);
-    k_residual<<<g1d(P * N * d, 256), 256, 0, st>>>(b.rows, b.cent, b.assign, assign_out, iters_out,
-                                                    b.st, P, N, S, t, K, d);
+    const int64_t rb = (N + 7) / 8;                       // 8 rows per 256-thread CTA
+    k_residual<<<dim3(unsigned(rb < 4096 ? rb : 4096), unsigned(P)), 256, 0, st>>>(
+        b.rows, b.cent, b.assign, assign_out, iters_out, b.st, P, N, S, t, K, d);
     return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
 }
 
