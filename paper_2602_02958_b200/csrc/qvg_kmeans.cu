@@ -145,10 +145,7 @@ __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const Src src, do
     double *xc = sm;                       // [d]
     double *leaf = sm + 128;               // [n_leaves] leaves, then the internal nodes
     double *dr = leaf + 2 * a.n_leaves - 1;   // [K] this plane's draws
-    __shared__ double s_total;
     __shared__ int64_t s_pick;
-    __shared__ double s_wsum[32];
-    __shared__ double s_base;
     const int64_t p = blockIdx.x;
     const int64_t N = a.N;
     const int d = a.d, K = a.K;
@@ -250,83 +247,82 @@ __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const Src src, do
             if (j8 == 0 && L < a.n_leaves) leaf[L] = s;
         }
         __syncthreads();
-        if (warp == 0) {            // the numpy recursion, level by level (host-built tree)
+        if (warp == 0) {
+            // (1) total = the numpy recursion over the leaves, level by level (host-built tree)
             const int nl = a.n_leaves;
             for (int hh = 0; hh < a.n_heights; hh++) {
                 for (int i = a.h_start[hh] + lane; i < a.h_start[hh + 1]; i += 32)
                     leaf[nl + i] = __dadd_rn(leaf[a.nd_l[i]], leaf[a.nd_r[i]]);
                 __syncwarp();
             }
-            if (lane == 0) s_total = __dadd_rn(0.0, leaf[nl > 1 ? 2 * nl - 2 : 0]);
-        }
-        __syncthreads();
-        const double r = dr[pk + 1];
-        const double total = s_total;
-        if (!(total > 0.0)) {     // uniform fallback (Q/clustering.py:41-42)
-            if (tid == 0) {
-                int64_t i = int64_t(r * double(N));
-                s_pick = i < N - 1 ? i : N - 1;
-            }
-            __syncthreads();
-            continue;
-        }
-        const double target = __dmul_rn(r, total);
-        // searchsorted(cumsum(d2), target, 'right') = #{j : cum_seq[j] <= target}.
-        // cum_seq (sequential f64) and our parallel prefix both lie within
-        // gamma_N * S_j of the exact prefix S_j (all terms >= 0), so a prefix
-        // farther than 2*gamma_N from target decides its element exactly.
-        const double eps = double(2 * N + 64) * 2.220446049250313e-16;
-        int cnt = 0;
-        bool amb = false;
-        if (tid == 0) s_base = 0.0;
-        __syncthreads();
-        for (int64_t b0 = 0; b0 < N; b0 += blockDim.x) {
-            int64_t i = b0 + tid;
-            double v = i < N ? d2[i] : 0.0;
-            double incl = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                double t = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += t;
-            }
-            if (lane == 31) s_wsum[warp] = incl;
-            __syncthreads();
-            if (warp == 0) {
-                double w = lane < int(blockDim.x >> 5) ? s_wsum[lane] : 0.0;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    double t = __shfl_up_sync(0xffffffffu, w, o);
-                    if (lane >= o) w += t;
-                }
-                s_wsum[lane] = w;   // inclusive warp prefix
-            }
-            __syncthreads();
-            double pre = s_base + (warp ? s_wsum[warp - 1] : 0.0) + incl;
-            bool le = false, am = false;
-            if (i < N) {
-                double m = pre * eps;
-                le = pre + m < target;
-                bool gt = pre - m > target;
-                am = !le && !gt;
-            }
-            cnt += __syncthreads_count(le);
-            amb |= __syncthreads_or(am) != 0;
-            if (tid == 0) s_base = s_base + s_wsum[(blockDim.x >> 5) - 1];
-            __syncthreads();
-        }
-        if (tid == 0) {
+            const double total = __dadd_rn(0.0, leaf[nl > 1 ? 2 * nl - 2 : 0]);
+            const double r = dr[pk + 1];
             int64_t pick;
-            if (!amb) pick = cnt;
-            else {                       // exact sequential cumsum (rare)
-                double cs = 0.0;
-                int64_t i = 0;
-                for (; i < N; i++) {
-                    cs = __dadd_rn(cs, d2[i]);
-                    if (cs > target) break;
+            if (!(total > 0.0)) {                         // uniform fallback (Q/clustering.py:41-42)
+                pick = int64_t(r * double(N));
+            } else {
+                // (2) searchsorted(cumsum(d2), target, 'right') = #{j : cum_seq[j] <= target}.
+                // cum_seq (sequential f64) and every prefix computed here (sums of
+                // non-negative terms in another order) lie within gamma_N * S_j of the
+                // exact prefix S_j, so a prefix farther than 2 gamma_N from target decides
+                // its element exactly; undecided elements replay the sequential cumsum.
+                // Leaf level first (whole leaves certainly below target), then the
+                // elements from the first undecided leaf on, 32 at a time.
+                const double target = __dmul_rn(r, total);
+                const double eps = double(2 * N + 64) * 2.220446049250313e-16;
+                double base = 0.0;
+                int lo = nl;
+                for (int L0 = 0; L0 < nl; L0 += 32) {
+                    const int L = L0 + lane;
+                    double incl = L < nl ? leaf[L] : 0.0;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const double t = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += t;
+                    }
+                    const double q = base + incl;
+                    const unsigned und = __ballot_sync(0xffffffffu, L < nl && !(q + q * eps < target));
+                    if (und) {
+                        const int f = __ffs(und) - 1;
+                        lo = L0 + f;
+                        const double before = __shfl_sync(0xffffffffu, incl, f > 0 ? f - 1 : 0);
+                        base = f > 0 ? base + before : base;
+                        break;
+                    }
+                    base += __shfl_sync(0xffffffffu, incl, 31);
                 }
-                pick = i;
+                int64_t cnt = lo < nl ? a.lf_off[lo] : N;
+                bool amb = false;
+                if (lo < nl) {
+                    for (int64_t e0 = cnt; e0 < N; e0 += 32) {
+                        const int64_t i = e0 + lane;
+                        double incl = i < N ? d2[i] : 0.0;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const double t = __shfl_up_sync(0xffffffffu, incl, o);
+                            if (lane >= o) incl += t;
+                        }
+                        const double pre = base + incl, m = pre * eps;
+                        const bool le = i < N && pre + m < target;
+                        const bool gt = i >= N || pre - m > target;
+                        cnt += __popc(__ballot_sync(0xffffffffu, le));
+                        amb |= __any_sync(0xffffffffu, !le && !gt);
+                        if (__any_sync(0xffffffffu, gt)) break;      // monotone: the rest is above
+                        base += __shfl_sync(0xffffffffu, incl, 31);
+                    }
+                }
+                pick = cnt;
+                if (amb && lane == 0) {                  // exact sequential cumsum (rare)
+                    double cs = 0.0;
+                    int64_t i = 0;
+                    for (; i < N; i++) {
+                        cs = __dadd_rn(cs, d2[i]);
+                        if (cs > target) break;
+                    }
+                    pick = i;
+                }
             }
-            s_pick = pick < N - 1 ? pick : N - 1;
+            if (lane == 0) s_pick = pick < N - 1 ? pick : N - 1;
         }
         __syncthreads();
     }
