@@ -239,6 +239,12 @@ int qvg_compress(const void *x, int32_t x_dtype, int64_t P, int64_t N, int32_t d
                                   size_t(S) * K * d * 8, size_t(K) * d * 8, size_t(P),
                                   cudaMemcpyDeviceToDevice, st);
             b.src16 = (t == 0 && x_dtype == QVG_DTYPE_BF16) ? static_cast<const uint16_t *>(x) : nullptr;
+            const bool r2 = t == 1 && x_dtype == QVG_DTYPE_BF16;
+            b.res_x16 = r2 ? static_cast<const uint16_t *>(x) : nullptr;
+            b.res_c1 = r2 ? centroids : nullptr;
+            b.res_a1 = r2 ? assign : nullptr;
+            b.res_c1_stride = int64_t(S) * K * d;
+            b.res_a1_stride = int64_t(S) * N;
             rc = run_kmeans_stage(b, P, N, d, K, cfg->kmeans_max_iters, cfg->kmeans_tol,
                                   warm ? nullptr : pp_draws + int64_t(t) * K, int64_t(S) * K, warm, st);
             if (rc) return set_err(rc, "k-means stage %d: %s", t, cudaGetErrorString(cudaGetLastError()));

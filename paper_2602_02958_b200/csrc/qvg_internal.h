@@ -36,6 +36,10 @@ struct KMeansBuffers {
     int32_t *rows32_ok;    // [P] nonzero: the copy is exact for the whole plane
     int rows32_valid;      // set once k_split_rows has filled rows32 for the current rows
     const uint16_t *src16; // the bf16 input when the current rows are exactly it (stage 1 of a bf16 chunk)
+    // stage 2 of a bf16 chunk: the rows are x - C1_bf16[pi1] (k-means++ rebuilds them)
+    const uint16_t *res_x16, *res_c1;
+    const uint8_t *res_a1;
+    int64_t res_c1_stride, res_a1_stride;
 };
 
 // qvg_codec.cu

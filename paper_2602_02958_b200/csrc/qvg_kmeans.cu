@@ -92,6 +92,13 @@ struct PPArgs {
     const int32_t *nd_l, *nd_r, *h_start;   // internal nodes of the pick tree, by height
     int n_heights;
     int d2_smem;             // 1: the N pick weights live in shared memory (after the draws)
+    // stage 2 of a bf16 chunk: rows rebuilt from the input and the stage-1 table
+    const uint16_t *x16;     // [P][N][d] bf16 input (nullable)
+    const uint16_t *c1;      // stage-1 bf16 centroids of plane 0; plane p at + p*c1_stride
+    int64_t c1_stride;
+    const uint8_t *a1;       // stage-1 assignments of plane 0; plane p at + p*a1_stride
+    int64_t a1_stride;
+    int64_t c1_off;          // shared-memory offset (in doubles) of the padded table copy
 };
 
 // rows read as T (double, or float when the plane's float64 rows are all exactly
@@ -121,6 +128,9 @@ struct SrcPlain {                       // rows stored as T (double / float / bf
     struct Row {
         const T *r;
         __device__ __forceinline__ double operator[](int k) const { return double(r[k]); }
+        __device__ __forceinline__ void load8(int k0, double v[8]) const {   // 2-byte T
+            bf16x8_to_f64(*reinterpret_cast<const uint4 *>(r + k0), v);
+        }
     };
     __device__ __forceinline__ Row row(int64_t i) const { return Row{rows + i * d}; }
     __device__ __forceinline__ void load8(int64_t i, int k0, double v[8]) const {
@@ -140,6 +150,43 @@ struct SrcPlain {                       // rows stored as T (double / float / bf
         }
     }
 };
+struct SrcResid {                       // stage-2 rows x - C1_bf16[pi1] rebuilt from the bf16 input
+    static constexpr int kBytes = 2;    // (the f64 difference of two bf16 values is exact)
+    const uint16_t *x;
+    const uint16_t *c1;                 // shared copy of this plane's stage-1 table, row pitch `cp`
+    const uint8_t *a1;
+    int d, cp;
+    struct Row {
+        const uint16_t *xr, *cr;
+        __device__ __forceinline__ double operator[](int k) const {
+            return __dsub_rn(double(__uint_as_float(uint32_t(xr[k]) << 16)), double(__uint_as_float(uint32_t(cr[k]) << 16)));
+        }
+        __device__ __forceinline__ void load8(int k0, double v[8]) const {
+            const uint4 xw = *reinterpret_cast<const uint4 *>(xr + k0);
+            const uint4 cw = *reinterpret_cast<const uint4 *>(cr + k0);
+            const uint32_t xu[4] = {xw.x, xw.y, xw.z, xw.w}, cu[4] = {cw.x, cw.y, cw.z, cw.w};
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+                v[2 * h] = __dsub_rn(double(__uint_as_float(xu[h] << 16)), double(__uint_as_float(cu[h] << 16)));
+                v[2 * h + 1] = __dsub_rn(double(__uint_as_float(xu[h] & 0xFFFF0000u)),
+                                         double(__uint_as_float(cu[h] & 0xFFFF0000u)));
+            }
+        }
+    };
+    __device__ __forceinline__ Row row(int64_t i) const { return Row{x + i * d, c1 + int(a1[i]) * cp}; }
+    __device__ __forceinline__ void load8(int64_t i, int k0, double v[8]) const {
+        const uint4 xw = *reinterpret_cast<const uint4 *>(x + i * d + k0);
+        const uint4 cw = *reinterpret_cast<const uint4 *>(c1 + int(a1[i]) * cp + k0);
+        const uint32_t xu[4] = {xw.x, xw.y, xw.z, xw.w}, cu[4] = {cw.x, cw.y, cw.z, cw.w};
+#pragma unroll
+        for (int h = 0; h < 4; h++) {
+            v[2 * h] = __dsub_rn(double(__uint_as_float(xu[h] << 16)), double(__uint_as_float(cu[h] << 16)));
+            v[2 * h + 1] = __dsub_rn(double(__uint_as_float(xu[h] & 0xFFFF0000u)),
+                                     double(__uint_as_float(cu[h] & 0xFFFF0000u)));
+        }
+    }
+};
+
 template <typename Src>
 __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const Src src, double *sm) {
     double *xc = sm;                       // [d]
@@ -178,10 +225,11 @@ __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const Src src, do
             // order, then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))); 16-byte loads
             for (int64_t i = tid; i < N; i += blockDim.x) {
                 double r[8];
+                const auto rw = src.row(i);                  // row pointers (and pi1) once
 #pragma unroll
                 for (int q = 0; q < 16; q++) {
                     double v[8];
-                    src.load8(i, q * 8, v);
+                    rw.load8(q * 8, v);
 #pragma unroll
                     for (int j = 0; j < 8; j++) {
                         const double t = __dsub_rn(v[j], xc[q * 8 + j]);
@@ -334,6 +382,15 @@ __global__ void __launch_bounds__(1024) k_kmeanspp(PPArgs a) {
     const int64_t p = blockIdx.x, nd = a.N * a.d;
     if (a.rows16) {
         kmeanspp_body(a, SrcPlain<Bf16>{reinterpret_cast<const Bf16 *>(a.rows16) + p * nd, a.d}, sm);
+    } else if (a.x16) {
+        // padded pitch (d + 8): the lanes' 16-byte reads of random table rows spread
+        // over the banks instead of all hitting the same ones
+        const int cp = a.d + 8;
+        uint16_t *c1s = reinterpret_cast<uint16_t *>(sm + a.c1_off);
+        const uint16_t *c1g = a.c1 + p * a.c1_stride;
+        for (int e = threadIdx.x; e < a.K * a.d; e += blockDim.x) c1s[(e / a.d) * cp + e % a.d] = c1g[e];
+        __syncthreads();
+        kmeanspp_body(a, SrcResid{a.x16 + p * nd, c1s, a.a1 + p * a.a1_stride, a.d, cp}, sm);
     } else if (a.rows32 && a.rows32_ok[p]) {
         kmeanspp_body(a, SrcPlain<float>{a.rows32 + p * nd, a.d}, sm);
     } else {
@@ -810,12 +867,26 @@ static void assign_step(const KMeansBuffers &b, int64_t P, int64_t N, int d, int
 int run_kmeanspp(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, const double *draws,
                  int64_t draws_stride, cudaStream_t st) {
     PPArgs pa{b.rows, b.rows32_valid ? b.rows32 : nullptr, b.src16, b.rows32_ok, draws, draws_stride, b.cent, b.d2, b.pk_off, b.pk_len, b.pk_leaves, N, d, K,
-              b.pk_l, b.pk_r, b.pk_hstart, b.pk_heights, 0};
+              b.pk_l, b.pk_r, b.pk_hstart, b.pk_heights, 0, nullptr, nullptr, 0, nullptr, 0, 0};
     size_t smem = sizeof(double) * (128 + 2 * b.pk_leaves - 1 + K);
     // the pick weights in shared memory while two 1024-thread CTAs still fit per SM
     if (smem + sizeof(double) * N <= 100 * 1024) {
         smem += sizeof(double) * N;
         pa.d2_smem = 1;
+    }
+    // stage 2 of a bf16 chunk (d = 128): rebuild the rows x - C1_bf16[pi1] exactly in
+    // f64 from the bf16 input and a shared copy of the stage-1 table (2 bytes per
+    // element instead of the 4- or 8-byte stage rows)
+    const size_t tab = (size_t(K) * (d + 8) * 2 + 15) & ~size_t(15);
+    if (b.res_x16 && d == 128 && ((smem + 15) & ~size_t(15)) + tab <= 100 * 1024) {
+        smem = (smem + 15) & ~size_t(15);
+        pa.x16 = b.res_x16;
+        pa.c1 = b.res_c1;
+        pa.c1_stride = b.res_c1_stride;
+        pa.a1 = b.res_a1;
+        pa.a1_stride = b.res_a1_stride;
+        pa.c1_off = int64_t(smem / sizeof(double));
+        smem += tab;
     }
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_kmeanspp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
