@@ -575,6 +575,25 @@ __global__ void __launch_bounds__(1024) k_members(MemberArgs a) {
 }
 
 // K3b: per (cluster, channel) ordered sums = np.add.at, then / count.
+// The stage rows of a bf16 chunk rebuilt from the input (exact in f64): stage 1
+// = x, stage 2 = x - C1_bf16[pi1] (c1 != nullptr).  2 bytes per element read
+// instead of the 4/8-byte stage rows.
+struct BfSrc {
+    const uint16_t *x16;       // [P][N][d] (nullptr: not available)
+    const uint16_t *c1;        // stage-1 bf16 table of plane 0, plane p at + p * c1_stride
+    int64_t c1_stride;
+    const uint8_t *a1;         // stage-1 assignments of plane 0, plane p at + p * a1_stride
+    int64_t a1_stride;
+    __device__ __forceinline__ double at(int64_t p, int64_t N, int d, int64_t row, int col) const {
+        double v = double(__uint_as_float(uint32_t(x16[(p * N + row) * d + col]) << 16));
+        if (c1) {
+            const int c = a1[p * a1_stride + row];
+            v = __dsub_rn(v, double(__uint_as_float(uint32_t(c1[p * c1_stride + int64_t(c) * d + col]) << 16)));
+        }
+        return v;
+    }
+};
+
 struct SumArgs {
     const double *rows;
     const float *rows32;        // exact float32 copy when rows32_ok[p] (half the bytes)
@@ -594,23 +613,29 @@ __global__ void __launch_bounds__(128) k_sums(SumArgs a) {
     const int cnt = a.counts[p * K + j];
     if (cnt == 0) return;                         // keep the old centroid
     const int32_t *mem = a.members + p * a.N + a.offsets[p * (K + 1) + j];
-    auto body = [&](auto rows) {
+    auto body = [&](auto val) {
         for (int k = threadIdx.x; k < d; k += blockDim.x) {
             double acc = 0.0;
             int t = 0;
             for (; t + 8 <= cnt; t += 8) {
                 double v[8];
 #pragma unroll
-                for (int u = 0; u < 8; u++) v[u] = double(rows[int64_t(mem[t + u]) * d + k]);
+                for (int u = 0; u < 8; u++) v[u] = val(mem[t + u], k);
 #pragma unroll
                 for (int u = 0; u < 8; u++) acc = __dadd_rn(acc, v[u]);
             }
-            for (; t < cnt; t++) acc = __dadd_rn(acc, double(rows[int64_t(mem[t]) * d + k]));
+            for (; t < cnt; t++) acc = __dadd_rn(acc, val(mem[t], k));
             a.cent[(p * K + j) * int64_t(d) + k] = __ddiv_rn(acc, double(cnt));
         }
     };
-    if (a.rows32 && a.rows32_ok[p]) body(a.rows32 + p * a.N * d);
-    else body(a.rows + p * a.N * d);
+    // (the bf16 source measured slower here: 2-byte member gathers)
+    if (a.rows32 && a.rows32_ok[p]) {
+        const float *rw = a.rows32 + p * a.N * d;
+        body([&](int64_t r, int k) { return double(rw[r * d + k]); });
+    } else {
+        const double *rw = a.rows + p * a.N * d;
+        body([&](int64_t r, int k) { return rw[r * d + k]; });
+    }
 }
 
 // K3c: empty-cluster repair (one CTA of 1024 per plane; returns at once when
@@ -690,6 +715,7 @@ __global__ void __launch_bounds__(1024) k_repair(RepairArgs a) {
 // K4: objective = ((rows - cent[assign])**2).sum() (flat numpy pairwise)
 // ------------------------------------------------------------------------
 struct ObjArgs {
+    BfSrc bf;
     const double *rows;
     const float *rows32;        // exact float32 copy when rows32_ok[p]
     const int32_t *rows32_ok;
@@ -733,6 +759,20 @@ __global__ void __launch_bounds__(256) k_obj_leaves(ObjArgs a) {
             if (j8 == 0 && L < a.n_leaves) a.nodes[p * n_nodes + L] = s;
         }
     };
+    if (a.bf.x16 && a.lgd >= 0) {                    // rows rebuilt from the bf16 input
+        for (int64_t L0 = wg * 4; L0 < a.n_leaves; L0 += nw * 4) {            // warp-uniform
+            const int64_t L = L0 + ((threadIdx.x & 31) >> 3);
+            const int64_t LL = L < a.n_leaves ? L : a.n_leaves - 1;
+            double s = leaf_sum8(a.lf_off[LL], a.lf_len[LL], j8, [&](int64_t e) {
+                const int64_t row = e >> a.lgd;
+                const int col = int(e & (d - 1));
+                double t = __dsub_rn(a.bf.at(p, a.N, d, row, col), cent[int64_t(asg[row]) * d + col]);
+                return __dmul_rn(t, t);
+            });
+            if (j8 == 0 && L < a.n_leaves) a.nodes[p * n_nodes + L] = s;
+        }
+        return;
+    }
     const bool r32 = a.rows32 && a.rows32_ok[p];
     if (a.lgd >= 0) {
         if (r32) run(a.rows32 + p * a.N * d, std::true_type{});
@@ -828,10 +868,16 @@ int launch_widen(const void *x, int xbf16, double *rows, int64_t n, int32_t *sta
     return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
 }
 
+static BfSrc bf_src(const KMeansBuffers &b) {
+    if (b.src16) return BfSrc{b.src16, nullptr, 0, nullptr, 0};
+    if (b.res_x16) return BfSrc{b.res_x16, b.res_c1, b.res_c1_stride, b.res_a1, b.res_a1_stride};
+    return BfSrc{nullptr, nullptr, 0, nullptr, 0};
+}
+
 static void objective(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int mode,
                       double tol, cudaStream_t st) {
     const int lgd = (d & (d - 1)) == 0 ? __builtin_ctz(unsigned(d)) : -1;
-    ObjArgs o{b.rows, b.rows32_valid ? b.rows32 : nullptr, b.rows32_ok, b.cent, b.assign, b.nodes, b.st,
+    ObjArgs o{bf_src(b), b.rows, b.rows32_valid ? b.rows32 : nullptr, b.rows32_ok, b.cent, b.assign, b.nodes, b.st,
               b.ob_off, b.ob_len, b.nd_l, b.nd_r, b.h_start, b.ob_leaves, b.ob_heights, N, d, K, mode, tol,
               lgd};
     dim3 g((unsigned)((int64_t(b.ob_leaves) * 8 + 255) / 256 < 4096 ? (int64_t(b.ob_leaves) * 8 + 255) / 256 : 4096),
