@@ -759,14 +759,26 @@ __global__ void __launch_bounds__(256) k_obj_leaves(ObjArgs a) {
             if (j8 == 0 && L < a.n_leaves) a.nodes[p * n_nodes + L] = s;
         }
     };
-    if (a.bf.x16 && a.lgd >= 0) {                    // rows rebuilt from the bf16 input
+    if (a.bf.x16 && a.lgd >= 7) {                    // rows rebuilt from the bf16 input
+        // d >= 128: a leaf (<= 128 elements) spans at most two rows, whose
+        // assignments (and stage-1 table rows) are looked up once per leaf
+        const uint16_t *xp = a.bf.x16 + p * a.N * d;
+        const uint16_t *c1p = a.bf.c1 ? a.bf.c1 + p * a.bf.c1_stride : nullptr;
+        const uint8_t *a1p = a.bf.c1 ? a.bf.a1 + p * a.bf.a1_stride : nullptr;
         for (int64_t L0 = wg * 4; L0 < a.n_leaves; L0 += nw * 4) {            // warp-uniform
             const int64_t L = L0 + ((threadIdx.x & 31) >> 3);
             const int64_t LL = L < a.n_leaves ? L : a.n_leaves - 1;
-            double s = leaf_sum8(a.lf_off[LL], a.lf_len[LL], j8, [&](int64_t e) {
-                const int64_t row = e >> a.lgd;
+            const int64_t off = a.lf_off[LL];
+            const int64_t r0 = off >> a.lgd, r1 = r0 + 1 < a.N ? r0 + 1 : r0;
+            const double *ce0 = cent + int64_t(asg[r0]) * d, *ce1 = cent + int64_t(asg[r1]) * d;
+            const uint16_t *cb0 = c1p ? c1p + int64_t(a1p[r0]) * d : nullptr;
+            const uint16_t *cb1 = c1p ? c1p + int64_t(a1p[r1]) * d : nullptr;
+            double s = leaf_sum8(off, a.lf_len[LL], j8, [&](int64_t e) {
+                const bool first = (e >> a.lgd) == r0;
                 const int col = int(e & (d - 1));
-                double t = __dsub_rn(a.bf.at(p, a.N, d, row, col), cent[int64_t(asg[row]) * d + col]);
+                double v = double(__uint_as_float(uint32_t(xp[e]) << 16));
+                if (c1p) v = __dsub_rn(v, double(__uint_as_float(uint32_t((first ? cb0 : cb1)[col]) << 16)));
+                double t = __dsub_rn(v, (first ? ce0 : ce1)[col]);
                 return __dmul_rn(t, t);
             });
             if (j8 == 0 && L < a.n_leaves) a.nodes[p * n_nodes + L] = s;
