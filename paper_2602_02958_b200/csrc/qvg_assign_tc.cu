@@ -197,7 +197,10 @@ constexpr size_t kSmemA = size_t(kSplit) * kTileB;
 constexpr size_t kSmemB = size_t(kSplit) * kNB * kD * 2;
 constexpr size_t kSmem = kSmemA + kSmemB + 2 * kNB * sizeof(float) + kNB * sizeof(double) + 1024;
 
-__global__ void __launch_bounds__(128, 1) k_assign_tc(TcArgs a) {
+// 8 warps: warp w reads TMEM lanes 32 (w & 3) (its rows) and takes the 32-centroid
+// chunks c with c % 2 == w >> 2; the two halves' certified states merge in smem
+constexpr int kTcThreads = 256;
+__global__ void __launch_bounds__(kTcThreads, 1) k_assign_tc(TcArgs a) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *sA = smem, *sB = smem + kSmemA;
@@ -225,7 +228,10 @@ __global__ void __launch_bounds__(128, 1) k_assign_tc(TcArgs a) {
     __syncthreads();
     fence_after();
     const uint32_t tmem = tmem_base;
-    const uint32_t t_lane = uint32_t(warp * 32) << 16;
+    const uint32_t t_lane = uint32_t((warp & 3) * 32) << 16;
+    const int hh = warp >> 2, rl = tid & 127;         // centroid-chunk half, row in the tile
+    __shared__ float mD[kM], mE[kM], mO[kM];
+    __shared__ int mJ[kM];
 
     // this CTA's contiguous items (plane, tile)
     const int64_t it0 = (int64_t(blockIdx.x) * n_items) / gridDim.x;
@@ -253,7 +259,7 @@ __global__ void __launch_bounds__(128, 1) k_assign_tc(TcArgs a) {
         const int t = int(it - p * a.T);
         const int64_t it_next = next_item(it + 1);
         const int nblk = (K + kNB - 1) / kNB;
-        const int64_t row = int64_t(t) * kM + tid;
+        const int64_t row = int64_t(t) * kM + rl;
         const float xn = row < a.N ? a.xnorm[p * a.N + row] : 0.f;
         // online certified argmin state (thread = row)
         float bestD = 0.f, bestE = 0.f, others = INFINITY;
@@ -326,7 +332,7 @@ __global__ void __launch_bounds__(128, 1) k_assign_tc(TcArgs a) {
             fence_after();
             if (blk == nblk - 1) load_tile(it_next);     // sA no longer read by this item's MMAs
             // ---- epilogue: 32 centroids at a time
-            for (int c0 = 0; c0 < nb; c0 += 32) {
+            for (int c0 = 32 * hh; c0 < nb; c0 += 64) {
                 float cr[32], tmp[32];
                 tmem_ld32(tmem + t_lane + c0, cr);
 #pragma unroll
@@ -374,7 +380,24 @@ __global__ void __launch_bounds__(128, 1) k_assign_tc(TcArgs a) {
             fence_before();
             __syncthreads();                 // TMEM / sB reads done before the next MMAs
         }
-        if (row < a.N) {
+        // merge the two chunk halves of each row (half 1 hands its state to half 0)
+        if (hh == 1) { mD[rl] = bestD; mE[rl] = bestE; mO[rl] = others; mJ[rl] = bestj; }
+        __syncthreads();
+        if (hh == 0) {
+            others = fminf(others, mO[rl]);
+            const int oj = mJ[rl];
+            if (oj >= 0) {
+                const float oD = mD[rl], oE = mE[rl];
+                if (bestj < 0) { bestD = oD; bestE = oE; bestj = oj; }
+                else if (oD < bestD || (oD == bestD && oj < bestj)) {
+                    others = fminf(others, __fsub_rd(bestD, bestE));
+                    bestD = oD; bestE = oE; bestj = oj;
+                } else {
+                    others = fminf(others, __fsub_rd(oD, oE));
+                }
+            }
+        }
+        if (hh == 0 && row < a.N) {
             const bool ok = others > __fadd_ru(bestD, bestE);
             a.assign[p * a.N + row] = ok ? bestj : -1;
             if (!ok) a.recheck[atomicAdd(a.n_recheck, 1)] = int32_t(p * a.N + row);
@@ -449,7 +472,7 @@ int launch_assign_tc(const uint16_t *split, const float *xnorm, const double *ro
     cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem));
     const int64_t items = P * T;
     const int grid = int(items < 148 ? items : 148);
-    k_assign_tc<<<grid, 128, kSmem, st>>>(ta);
+    k_assign_tc<<<grid, kTcThreads, kSmem, st>>>(ta);
     k_assign_recheck<<<148 * 4, 256, 0, st>>>(rows, cent, c2, assign, recheck, n_recheck, N, K);
     static const bool stats = getenv("QVG_ASSIGN_STATS") != nullptr;
     if (stats) {   // measurement aid: fraction of rows the filter could not certify
