@@ -61,6 +61,22 @@ __device__ __forceinline__ double leaf_sum8(int64_t off, int len, int j, F v) {
     return acc;
 }
 
+template <int U, typename F>
+__device__ __forceinline__ double leaf_sum8u(int64_t off, int len, int j, F v) {
+    if (len < 8) {
+        double s = 0.0;
+        for (int k = 0; k < len; k++) s = __dadd_rn(s, v(off + k));
+        return s;
+    }
+    const int m = len >> 3;
+    double acc = v(off + j);
+#pragma unroll U
+    for (int i = 1; i < m; i++) acc = __dadd_rn(acc, v(off + i * 8 + j));
+    acc = pairwise8_tree(acc);
+    for (int k = m * 8; k < len; k++) acc = __dadd_rn(acc, v(off + k));
+    return acc;
+}
+
 // ------------------------------------------------------------------------
 // widen input to the f64 stage-1 rows (plane.data.astype(np.float64)) + NaN scan
 // ------------------------------------------------------------------------
@@ -773,7 +789,7 @@ __global__ void __launch_bounds__(256) k_obj_leaves(ObjArgs a) {
             const double *ce0 = cent + int64_t(asg[r0]) * d, *ce1 = cent + int64_t(asg[r1]) * d;
             const uint16_t *cb0 = c1p ? c1p + int64_t(a1p[r0]) * d : nullptr;
             const uint16_t *cb1 = c1p ? c1p + int64_t(a1p[r1]) * d : nullptr;
-            double s = leaf_sum8(off, a.lf_len[LL], j8, [&](int64_t e) {
+            double s = leaf_sum8u<8>(off, a.lf_len[LL], j8, [&](int64_t e) {
                 const bool first = (e >> a.lgd) == r0;
                 const int col = int(e & (d - 1));
                 double v = double(__uint_as_float(uint32_t(xp[e]) << 16));
