@@ -1669,6 +1669,8 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
         const uint64_t pN = uint64_t(p) * N;
         const uint8_t *xb = static_cast<const uint8_t *>(a.x) + pN * d * (XBF16 ? 2 : 4);
         const uint8_t *ap = a.asg + pN * S;
+        uint8_t *const pay = a.payload + uint64_t(p) * a.pb;     // this plane's code and scale bytes
+        uint8_t *const scl = a.scales + uint64_t(p) * a.ng;
         uint4 nx0, nx1;
         int na[SS];
         auto fetch = [&](uint32_t i) {
@@ -1772,7 +1774,7 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
                     cert[u] = false;
                     eb[u] = S > 0 ? __fadd_ru(e, mx) : 0.f;
                 }
-                nonfinite |= !(mx <= 3.402823466e38f) || !(e <= 3.402823466e38f);
+                nonfinite |= !(mx <= 3.402823466e38f) || (!kCert && !(e <= 3.402823466e38f));
                 am[u] = mx;
             }
             for (int m = 1; m < glanes; m <<= 1) {
@@ -1925,7 +1927,7 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
                 }
                 if (!valid) continue;
                 const uint32_t e0 = ii[u] * d + col;
-                uint8_t *plp = a.payload + uint64_t(p) * a.pb + ((e0 * BITS) >> 3);
+                uint8_t *plp = pay + ((e0 * BITS) >> 3);
                 if constexpr (NW == 1) *reinterpret_cast<uint32_t *>(plp) = b32[0];
                 else if constexpr (NW == 2) *reinterpret_cast<uint2 *>(plp) = make_uint2(b32[0], b32[1]);
                 else {
@@ -1933,7 +1935,7 @@ __global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
                     for (int w4 = 0; w4 < NW / 4; w4++)
                         reinterpret_cast<uint4 *>(plp)[w4] = make_uint4(b32[4 * w4], b32[4 * w4 + 1], b32[4 * w4 + 2], b32[4 * w4 + 3]);
                 }
-                if ((lane & (glanes - 1)) == 0) a.scales[uint64_t(p) * a.ng + (e0 >> a.lgB)] = uint8_t(code);
+                if ((lane & (glanes - 1)) == 0) scl[e0 >> a.lgB] = uint8_t(code);
             }
         }
         if (flow) {                                               // done reading buffer j&1
