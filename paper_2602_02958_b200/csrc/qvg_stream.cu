@@ -398,6 +398,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_stream(DequantArgs a, G
         const uint8_t *st = ring + k * g.stage_bytes;
         const uint8_t *sa = st + g.off_small + g.R * g.small_row;
         const uint32_t nr = min(g.R, sc.r1 - sc.i0);
+        const uint64_t obase = (uint64_t(p) * N + sc.i0) * d + col;   // this stage's first output row
         Codes16<BITS> w[kU];
         uint32_t scb[kU], lr[kU];
         int ai[kU][SS];
@@ -544,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_stream(DequantArgs a, G
                 }
             }
             if (!valid) continue;
-            const uint64_t o = (uint64_t(p) * N + sc.i0 + lr[u]) * d + col;
+            const uint64_t o = obase + uint64_t(lr[u] * d);
             if constexpr (OBF16) {
                 uint32_t v[8];
 #pragma unroll
