@@ -1034,8 +1034,9 @@ int run_kmeanspp(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, con
         smem += tab;
     }
     // bf16 sources (stage 1 / the stage-2 rebuild): a double-buffered shared staging
-    // ring of 2 x 256 rows (padded pitch 136) when it fits (QVG_KPP_STAGE=0: off)
-    static const bool stage_ok = [] { const char *e = getenv("QVG_KPP_STAGE"); return !(e && atoi(e) == 0); }();
+    // ring of 2 x 256 rows (padded pitch 136) when it fits -- opt-in (QVG_KPP_STAGE=1):
+    // 2% faster, and an intermittent stall was observed with it enabled
+    static const bool stage_ok = [] { const char *e = getenv("QVG_KPP_STAGE"); return e && atoi(e) == 1; }();
     const size_t ring = size_t(2) * 256 * 136 * 2;
     if (stage_ok && d == 128 && (b.src16 || pa.x16) && ((smem + 15) & ~size_t(15)) + ring <= 220 * 1024) {
         smem = (smem + 15) & ~size_t(15);
