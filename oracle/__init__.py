@@ -57,6 +57,8 @@ def lib():
         L.qo_kmeans_pp.argtypes = [_P, _I64, _I32, _I32, _P, _P, _P]
         L.qo_assign.restype = None
         L.qo_assign.argtypes = [_P, _I64, _I32, _P, _I32, _P]
+        L.qo_lloyd_step.restype = _D
+        L.qo_lloyd_step.argtypes = [_P, _I64, _I32, _P, _I32, _P]
         L.qo_kmeans.restype = _I32
         L.qo_kmeans.argtypes = [_P, _I64, _I32, _I32, _I32, _D, _P, _P, _P, _P, _P, _P]
         L.qo_prq_compress.restype = _I32
@@ -166,6 +168,15 @@ def assign(rows, cent) -> np.ndarray:
     out = np.empty(rows.shape[0], np.int32)
     lib().qo_assign(_ptr(rows), rows.shape[0], rows.shape[1], _ptr(cent), cent.shape[0], _ptr(out))
     return out
+
+
+def lloyd_step(rows, cent):
+    """Q/clustering.py:74-107 -> (new centroids, assignments int32, objective)."""
+    rows = _c(rows, np.float64)
+    cent = np.array(cent, dtype=np.float64, copy=True, order="C")
+    asg = np.empty(rows.shape[0], np.int32)
+    obj = lib().qo_lloyd_step(_ptr(rows), rows.shape[0], rows.shape[1], _ptr(cent), cent.shape[0], _ptr(asg))
+    return cent, asg, obj
 
 
 def kmeans(rows, k, max_iters, tol, draws=None, init=None):

@@ -316,6 +316,16 @@ static double lloyd_step(const double *rows, int64_t n, int d, double *cent, int
     return objective(rows, n, d, cent, assign, scratch);
 }
 
+/* Q/clustering.py:74-107 lloyd_step as an entry point: cent [k][d] updated in
+   place, assign [n] out, returns the objective against the new centroids. */
+double qo_lloyd_step(const double *rows, int64_t n, int d, double *cent, int k, int32_t *assign)
+{
+    double *scratch = malloc(sizeof(double) * n * d);
+    double obj = lloyd_step(rows, n, d, cent, k, assign, scratch);
+    free(scratch);
+    return obj;
+}
+
 /* Q/clustering.py:110-160 kmeans.  init == NULL -> k-means++ with draws. */
 int qo_kmeans(const double *rows, int64_t n, int d, int k, int max_iters, double tol,
               const double *draws, const double *init, double *cent, int32_t *assign,

@@ -62,7 +62,7 @@ int run_kmeans_stage(KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int m
                      cudaStream_t st);
 int kmeans_outputs(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, uint8_t *assign,
                    double *objective, int32_t *iters, cudaStream_t st);
-int lloyd_once(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, uint8_t *assign,
+int lloyd_once(KMeansBuffers &b, int64_t P, int64_t N, int d, int K, uint8_t *assign,
                double *objective, cudaStream_t st);
 int run_assign(const double *rows, const double *cent, int32_t *assign, int64_t P, int64_t N, int d,
                int K, cudaStream_t st);

@@ -1064,18 +1064,24 @@ static void lloyd_body(const KMeansBuffers &b, int64_t P, int64_t N, int d, int 
     objective(b, P, N, d, K, mode, tol, st);
 }
 
+// The rows are fixed for a whole stage (or Lloyd step): split them once into the
+// bf16 hi/mid/lo tiles of the tensor-core assignment (every assign_step reads them).
+static int split_rows(KMeansBuffers &b, int64_t P, int64_t N, cudaStream_t st) {
+    b.rows32_valid = 0;
+    if (b.rsplit && assign_tc_enabled()) {
+        if (launch_split_rows(b.rows, b.rsplit, b.xnorm, b.rows32, b.rows32_ok, P, N, st)) return QVG_ERR_CUDA;
+        b.rows32_valid = 1;
+    }
+    return QVG_OK;
+}
+
 // One SAS stage's k-means for all planes (Q/clustering.py:110-160); leaves
 // the final assignment in b.assign and the iteration count in b.st.
 int run_kmeans_stage(KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int max_iters,
                      double tol, const double *draws_stage, int64_t draws_stride, bool warm,
                      cudaStream_t st) {
     k_stage_reset<<<g1d(P, 256), 256, 0, st>>>(b.st, P);
-    // the rows are fixed for the whole stage: split them once for the tensor-core assignment
-    b.rows32_valid = 0;
-    if (b.rsplit && assign_tc_enabled()) {
-        if (launch_split_rows(b.rows, b.rsplit, b.xnorm, b.rows32, b.rows32_ok, P, N, st)) return QVG_ERR_CUDA;
-        b.rows32_valid = 1;
-    }
+    if (split_rows(b, P, N, st)) return QVG_ERR_CUDA;
     if (!warm && run_kmeanspp(b, P, N, d, K, draws_stage, draws_stride, st)) return QVG_ERR_CUDA;
     // objective of the starting centroids (Q/clustering.py:142-143)
     assign_step(b, P, N, d, K, 0, st);
@@ -1105,9 +1111,10 @@ int kmeans_outputs(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, u
     return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
 }
 
-int lloyd_once(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, uint8_t *assign,
+int lloyd_once(KMeansBuffers &b, int64_t P, int64_t N, int d, int K, uint8_t *assign,
                double *objective_out, cudaStream_t st) {
     k_stage_reset<<<g1d(P, 256), 256, 0, st>>>(b.st, P);
+    if (split_rows(b, P, N, st)) return QVG_ERR_CUDA;
     lloyd_body(b, P, N, d, K, 2, 0.0, st);
     k_km_outputs<<<g1d(P * N, 256), 256, 0, st>>>(b.assign, assign, b.st, objective_out, nullptr, P, N);
     return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;

@@ -31,6 +31,7 @@ from .qvgcodec.types import QuantConfig
 __all__ = [
     "DeviceChunks", "stage_seed", "pp_draws", "compress", "quantize", "dequantize",
     "kmeans_pp", "assign", "lloyd_step", "kmeans", "sa_smoothing", "add_back", "attention",
+    "stage_mse_curve",
     "check_status",
 ]
 
@@ -228,6 +229,36 @@ def dequantize(chunks: DeviceChunks, out_dtype=torch.bfloat16, out: Optional[tor
     if check:
         check_status(st)
     return out
+
+
+def stage_mse_curve(x: torch.Tensor, config: QuantConfig, max_stages: int,
+                    chunk_index: Union[int, Sequence[int]] = 0) -> torch.Tensor:
+    """stage_mse_curve (Q/prq.py:135-172) over P planes -> float64 [P, max_stages + 1].
+
+    Stage seeds depend only on (seed, chunk, stage), so one compress with
+    ``max_stages`` stages yields every prefix chain; each prefix s is then
+    quantized given its first s stages' metadata (the residual x - C_1[pi_1]
+    - ... - C_s[pi_s] formed in the kernel), decoded to float32 and compared
+    with x in float64.  The per-plane mean is torch's reduction, not numpy's
+    pairwise order (the host mirror qvgcodec.prq.stage_mse_curve is the
+    bit-exact one); the decoded planes themselves are bit-exact."""
+    _require_cuda(x)
+    P, N, d = x.shape
+    full = compress(x, config.with_stages(max_stages), chunk_index=chunk_index) if max_stages else None
+    x64 = x.to(torch.float64)
+    curve = torch.empty((P, max_stages + 1), dtype=torch.float64, device=x.device)
+    for s in range(max_stages + 1):
+        cfg = config.with_stages(s)
+        if s:
+            cent = full.centroids[:, :s].contiguous()
+            asg = full.assignments[:, :s].contiguous()
+        else:
+            cent = torch.empty((P, 0, config.centroids, d), dtype=torch.bfloat16, device=x.device)
+            asg = torch.empty((P, 0, N), dtype=torch.uint8, device=x.device)
+        pay, sc = quantize(x, cfg, cent, asg)
+        rec = dequantize(DeviceChunks(cfg, N, d, pay, sc, cent, asg), torch.float32)
+        curve[:, s] = ((x64 - rec.to(torch.float64)) ** 2).mean(dim=(1, 2))
+    return curve
 
 
 # ---------------------------------------------------------------------------

@@ -1,5 +1,7 @@
 """The CPU oracle (oracle/qvg_oracle.c) against fixtures written by the
 reference itself (tests/golden/make_golden.py).  Pins the oracle."""
+import os
+
 import numpy as np
 import pytest
 
@@ -63,3 +65,35 @@ def test_kmeanspp_picks_match_reference(oracle_lib, name):
     cent, chosen = oracle_lib.kmeans_pp(x, rec["centroids"], draws)
     ref_rows = x[rec["pp_first_picks"][0]]
     assert np.array_equal(cent, ref_rows)
+
+
+def test_oracle_stage_curve_and_lloyd_vs_reference(oracle_lib):
+    """curves.npz (make_golden_curves.py, the reference's stage_mse_curve and
+    lloyd_step): the oracle's compress/decompress per stage prefix gives the
+    same MSE values (np.mean over the same float64 differences), and its
+    lloyd_step the same centroids, assignments (incl. the empty-cluster
+    repair) and objective."""
+    from paper_2602_02958_b200 import datagen as G
+
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "curves.npz"))
+    xs = {}
+    for name, seed, value in (("key", 10, False), ("value", 11, True)):
+        p = G.StreamParams(n_tokens=1560, drift=0.0125, outlier_scale=100.0 if value else 10.0)
+        x = G.bf16_bits_to_f32(G.round_bf16_bits(G.stream_chunk(seed, 3, p)))
+        xs[name] = x
+        for B in (16, 64):
+            curve = []
+            for S in range(5):
+                draws = oracle_lib.pp_draws(0, 3, S, 64)
+                r = oracle_lib.prq_compress(x, 2, B, S, 64, 10, 1e-4, draws=draws)
+                rec = oracle_lib.prq_decompress(r["payload"], r["scales"], r["centroids"], r["assignments"],
+                                                1560, 128, 2, B)
+                curve.append(float(np.mean((x.astype(np.float64) - rec.astype(np.float64)) ** 2)))
+            assert curve == list(z[f"{name}_curve_b{B}"]), (name, B)
+    rows = xs["value"].astype(np.float64)[:700]
+    init = rows[z["lloyd_pick"]].copy()
+    init[z["lloyd_far"]] = 1e4
+    cent, asg, obj = oracle_lib.lloyd_step(rows, init)
+    assert np.array_equal(cent.view(np.uint64), z["lloyd_cent"].view(np.uint64))
+    assert np.array_equal(asg, z["lloyd_asg"])
+    assert obj == float(z["lloyd_obj"])
