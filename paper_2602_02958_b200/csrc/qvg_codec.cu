@@ -2088,10 +2088,11 @@ static void launch_quant_fast(const QuantArgs &a, bool xbf16, cudaStream_t st) {
     // warps/SM) is still the fastest measured for many planes (2.22 vs 2.12
     // TB/s on the Self-Forcing cache); the per-warp-ring kernel serves the rest
     const int pref = codec_kernel_pref();
+    // the warp-specialised ring kernel (qvg_stream.cu) first
+    if (S > 0 && a.v16 && (pref == 0 || pref == 1) && launch_quantize_stream(a, a.P, BITS, S, xbf16, st)) return;
     if (S > 0 && a.v16 && (pref == 0 || pref == 7) && launch_quant_v5w<BITS, S>(a, xbf16, st)) return;
     const bool v5_ok = a.v16 && a.v5 && (pref == 0 || pref == 5);
     if (S > 0 && a.v16 && !v5_ok && (pref == 0 || pref == 2) && launch_quantize_wring(a, a.P, BITS, S, xbf16, st)) return;
-    if (S > 0 && a.v16 && !v5_ok && pref == 1 && launch_quantize_stream(a, a.P, BITS, S, xbf16, st)) return;
     V6Launch L;
     if (S > 0 && a.v16 && !v5_ok && pref == 6 && v6_plan(a.P, a.N, a.d, S, a.K, L)) {
         if (xbf16) {

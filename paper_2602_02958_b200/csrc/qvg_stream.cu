@@ -29,8 +29,8 @@ namespace stream {
 // ============================================================================
 // K5 quantize
 // ============================================================================
-template <int BITS, int S, bool XBF16>
-__global__ void __launch_bounds__(kThreads, 1) k_quantize_stream(QuantArgs a, Geo g) {
+template <int BITS, int S, bool XBF16, int CW, int QU>
+__global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_stream(QuantArgs a, Geo g) {
     constexpr int QMAX = (1 << (BITS - 1)) - 1;
     constexpr int SS = S > 0 ? S : 1;
     constexpr int FPW = 32 / BITS;
@@ -43,15 +43,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_quantize_stream(QuantArgs a, Ge
     float *const tab = reinterpret_cast<float *>(smem + g.off_tab);
     float2 *const meta = reinterpret_cast<float2 *>(smem + g.off_meta);
     uint8_t *const ring = smem + g.off_ring;
-    __shared__ float rcp_tab[128];          // RN32(1 / e4m3(code)) for the 128 magnitude codes
+    __shared__ float rcp_tab[128];          // 1 / e4m3(code): rounded down for 2-bit (see the codes), else RN
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t d = g.d, N = g.N;
 
-    if (threadIdx.x < 128) rcp_tab[threadIdx.x] = __frcp_rn(e4m3_decode_fast(threadIdx.x));
+    if (threadIdx.x < 128)
+        rcp_tab[threadIdx.x] = QMAX == 1 ? __frcp_rd(e4m3_decode_fast(threadIdx.x)) : __frcp_rn(e4m3_decode_fast(threadIdx.x));
     if (threadIdx.x == 0) {
         for (uint32_t k = 0; k < g.nst; k++) {
             mbar_init(&bars.full[k], 1 + 32);
-            mbar_init(&bars.empty[k], kCW);
+            mbar_init(&bars.empty[k], CW);
         }
         mbar_init(&bars.tab, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -60,7 +61,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_quantize_stream(QuantArgs a, Ge
     Sched sc;
     sc.init(g);
 
-    if (warp == kCW) {
+    if (warp == CW) {
         // ---------------- producer ----------------
         uint32_t s = 0, k = 0, ph = 0;                  // stage, slot, slot phase
         for (; sc.valid(); sc.next(g), s++, k = k + 1 == g.nst ? (ph ^= 1u, 0u) : k + 1) {
@@ -85,223 +86,240 @@ __global__ void __launch_bounds__(kThreads, 1) k_quantize_stream(QuantArgs a, Ge
     }
 
     // ---------------- consumers ----------------
+    // Thread = 16 channels of QU rows per stage.  Per row:
+    //  * r = x - C_1[pi_1] - ... - C_S[pi_S] in f32 (FADD2 over the padded f32
+    //    tables), amax by 3-input |.| max;
+    //  * a lane certificate: when x and the chosen centroid blocks are all
+    //    multiples of a power of two `unit` and every partial sum stays below
+    //    2^23 unit, the f32 chain is exact, i.e. r IS the reference's float64
+    //    residual (Q/smoothing.py:40) and the lane's error bound is 0; else
+    //    E_l = 2^-22 S (max|r_S| + sum_t max|c_t|) bounds |r_f32 - r_ref|;
+    //  * the group's amax lies in [max_l(am_l - E_l), max_l(am_l + E_l)]: the
+    //    E4M3 "up" code (Q/quant.py:40-45) is certain unless that interval
+    //    straddles a code boundary -> exact f64 maxima of the candidates (rare);
+    //  * codes = bits of fma(r, 1/s, 1.5*2^23 + 2^(b-1)) packed by an integer
+    //    multiply-add tree.  2-bit certified lanes: with 1/s rounded DOWN and
+    //    s/2 a multiple of `unit`, every |r| != s/2 is >= unit away from the
+    //    rounding boundary and |r| == s/2 rounds to 0 (half-even), so the codes
+    //    are exact with no further test.  Other lanes test an ambiguity window
+    //    (E_l plus the 1/s rounding) and recompute flagged elements in float64
+    //    (Q/quant.py:48-55).
     const uint32_t lvpr = g.lchunk;                 // log2(threads per row)
     const uint32_t c = threadIdx.x & ((1u << lvpr) - 1u);
     const uint32_t col = c << 4;
     const uint32_t coff = blk_off(c);
-    const uint32_t rslot = threadIdx.x >> lvpr, rpp = (kCW * 32) >> lvpr;
+    const uint32_t rslot = threadIdx.x >> lvpr, rpp = (CW * 32) >> lvpr;
     const int glanes = 1 << a.gshift;
+    const bool slead = (lane & uint32_t(glanes - 1)) == 0;
+    const uint32_t pitch = g.pitch, KK = g.K, big_row = g.big_row;
     bool nonfinite = false;
     uint32_t cur = 0xFFFFFFFFu, jp = 0, k = 0, ph = 0;
+    uint8_t *pay = a.payload, *scl = a.scales;
     if (S > 0 && !g.stg_global && threadIdx.x == 0 && sc.valid()) stage_table(a.cent, sc.p, g.tbytes, stg, &bars.tab);
     for (; sc.valid(); sc.next(g), k = k + 1 == g.nst ? (ph ^= 1u, 0u) : k + 1) {
         const uint32_t p = sc.p;
-        if (S > 0 && p != cur) {
-            named_sync_consumers();
-            if (!g.stg_global) mbar_wait(&bars.tab, jp & 1u);
-            widen(g.stg_global ? a.cent + size_t(p) * (g.tbytes / 2) : stg, tab, meta, g);
-            named_sync_consumers();
-            if (!g.stg_global && threadIdx.x == 0) {
-                const int64_t nx = sc.next_plane(g);
-                if (nx >= 0) {
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    stage_table(a.cent, uint32_t(nx), g.tbytes, stg, &bars.tab);
+        if (p != cur) {
+            if (S > 0) {
+                named_sync_consumers<CW>();
+                if (!g.stg_global) mbar_wait(&bars.tab, jp & 1u);
+                widen(g.stg_global ? a.cent + size_t(p) * (g.tbytes / 2) : stg, tab, meta, g, CW * 32);
+                named_sync_consumers<CW>();
+                if (!g.stg_global && threadIdx.x == 0) {
+                    const int64_t nx = sc.next_plane(g);
+                    if (nx >= 0) {
+                        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                        stage_table(a.cent, uint32_t(nx), g.tbytes, stg, &bars.tab);
+                    }
                 }
+                jp++;
             }
-            jp++;
+            pay = a.payload + uint64_t(p) * a.pb;
+            scl = a.scales + uint64_t(p) * a.ng;
+            cur = p;
         }
-        cur = p;
         mbar_wait(&bars.full[k], ph);
-        if (g.dbg == 1) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&bars.empty[k]);
-            continue;
-        }
         const uint8_t *st = ring + k * g.stage_bytes;
         const uint32_t nr = min(g.R, sc.r1 - sc.i0);
-        float2 r[kU][8];
-        uint32_t lr[kU];
-        int ai[kU][SS];
-        float xmin[kU];
-#pragma unroll
-        for (int u = 0; u < kU; u++) {
+#pragma unroll 1
+        for (int u = 0; u < QU; u++) {
+            // ---- one row: residual, amax, lane certificate
             const uint32_t l = u * rpp + rslot;
-            lr[u] = l < nr ? l : nr - 1;
-            const uint8_t *xr = st + lr[u] * g.big_row + col * XB;
-            xmin[u] = 0.f;
+            const bool valid = l < nr;
+            const uint32_t lr = valid ? l : nr - 1;
+            const uint8_t *xr = st + lr * big_row + col * XB;
+            float2 r[8];
+            float xmn = __int_as_float(0x7F800000);
             if constexpr (XBF16) {
                 const uint4 w0 = *reinterpret_cast<const uint4 *>(xr);
                 const uint4 w1 = *reinterpret_cast<const uint4 *>(xr + 16);
-                cvt16(w0, w1, reinterpret_cast<float *>(r[u]));
-                float mv[8];
+                cvt16(w0, w1, reinterpret_cast<float *>(r));
+                if constexpr (S > 0) {
+                    float m0 = xmn, m1 = xmn;
 #pragma unroll
-                for (int q = 0; q < 8; q++) mv[q] = fminf(fabsf(r[u][q].x), fabsf(r[u][q].y));
-#pragma unroll
-                for (int span = 1; span < 8; span *= 2)
-#pragma unroll
-                    for (int q = 0; q < 8; q += 2 * span) mv[q] = fminf(mv[q], mv[q + span]);
-                xmin[u] = mv[0];
+                    for (int q = 0; q < 8; q += 2) {
+                        m0 = min3_abs(m0, r[q].x, r[q].y);
+                        m1 = min3_abs(m1, r[q + 1].x, r[q + 1].y);
+                    }
+                    xmn = fminf(m0, m1);
+                }
             } else {
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
                     const float4 v = *reinterpret_cast<const float4 *>(xr + 16 * j);
-                    r[u][2 * j] = make_float2(v.x, v.y);
-                    r[u][2 * j + 1] = make_float2(v.z, v.w);
+                    r[2 * j] = make_float2(v.x, v.y);
+                    r[2 * j + 1] = make_float2(v.z, v.w);
                 }
             }
+            int ai[SS];
 #pragma unroll
-            for (int t = 0; t < S; t++) ai[u][t] = st[g.off_small + t * g.R + lr[u]];
-        }
-        float eb[kU], am[kU];
-#pragma unroll
-        for (int u = 0; u < kU; u++) {
-            // error bound input: sum_t max|r_t| <= S*max|r_S| + sum_t t*max|c_{t+1}|
-            // exactness certificate (bf16 x): every term of x - C_1 - ... - C_S is a
-            // multiple of `unit` and the sum of magnitudes < 2^24 unit => the f32
-            // chain is exact (== the reference's float64 residual), E = 0
-            float cb = 0.f, csum = 0.f, cunit = __int_as_float(0x7F800000);
+            for (int t = 0; t < S; t++) ai[t] = st[g.off_small + t * g.R + lr];
+            float csum = 0.f, cunit = __int_as_float(0x7F800000);
 #pragma unroll
             for (int t = 0; t < S; t++) {
-                const float *row = tab + uint32_t(t * int(g.K) + ai[u][t]) * g.pitch + coff;
+                const uint32_t row = uint32_t(t * int(KK) + ai[t]);
+                const float *cr = tab + row * pitch + coff;
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
-                    const float4 cv = *reinterpret_cast<const float4 *>(row + 4 * j);
-                    r[u][2 * j] = __fadd2_rn(r[u][2 * j], make_float2(-cv.x, -cv.y));
-                    r[u][2 * j + 1] = __fadd2_rn(r[u][2 * j + 1], make_float2(-cv.z, -cv.w));
+                    const float4 cv = *reinterpret_cast<const float4 *>(cr + 4 * j);
+                    r[2 * j] = __fadd2_rn(r[2 * j], make_float2(-cv.x, -cv.y));
+                    r[2 * j + 1] = __fadd2_rn(r[2 * j + 1], make_float2(-cv.z, -cv.w));
                 }
-                const float2 m = meta[(uint32_t(t * int(g.K) + ai[u][t]) << lvpr) + c];
-                if (t > 0) cb = __fmaf_ru(float(t), m.y, cb);
+                const float2 m = meta[(row << lvpr) + c];
                 csum = __fadd_ru(csum, m.y);
                 cunit = fminf(cunit, m.x);
             }
-            float mv[8];
+            float m0 = 0.f, m1 = 0.f;
 #pragma unroll
-            for (int q = 0; q < 8; q++) mv[q] = max3_nan_abs(0.f, r[u][q].x, r[u][q].y);
-#pragma unroll
-            for (int span = 1; span < 8; span *= 2)
-#pragma unroll
-                for (int q = 0; q < 8; q += 2 * span) mv[q] = max_nan(mv[q], mv[q + span]);
-            const float mx = mv[0];
-            nonfinite |= !(mx <= 3.402823466e38f) || !(cb <= 3.402823466e38f);
-            am[u] = mx;
-            bool cert = false;
-            if constexpr (XBF16) {
-                const uint32_t eb8 = __float_as_uint(xmin[u]) & 0x7F800000u;
-                const float xunit = eb8 > (7u << 23) ? __uint_as_float(eb8 - (7u << 23)) : 0.f;
-                // |partials| <= max|x| + sum max|c| <= max|r_S| + 2 sum max|c|
-                const float bound = __fmaf_ru(2.f, csum, mx);
-                cert = bound < fminf(xunit, cunit) * 16777216.f;
+            for (int q = 0; q < 8; q += 2) {
+                m0 = max3_nan_abs(m0, r[q].x, r[q].y);
+                m1 = max3_nan_abs(m1, r[q + 1].x, r[q + 1].y);
             }
-            eb[u] = (S > 0 && !cert) ? __fmaf_ru(float(S), mx, cb) : 0.f;
-        }
-        for (int m = 1; m < glanes; m <<= 1) {
-#pragma unroll
-            for (int u = 0; u < kU; u++) {
-                am[u] = fmaxf(am[u], __shfl_xor_sync(0xffffffffu, am[u], m));
-                eb[u] = fmaxf(eb[u], __shfl_xor_sync(0xffffffffu, eb[u], m));
+            const float mx = max_nan(m0, m1);
+            nonfinite |= !(mx <= 3.402823466e38f) && valid;
+            // certificate (bf16 x): |partials| <= max|x| + sum max|c| <= max|r_S| + 2 sum max|c|
+            const uint32_t xe = __float_as_uint(xmn) & 0x7F800000u;
+            const float un = fminf(xe > (7u << 23) ? __uint_as_float(xe - (7u << 23)) : 0.f, cunit);
+            const bool cert = S == 0 || (XBF16 && __fmaf_ru(2.f, csum, mx) < un * 8388608.f);
+            const float El = cert ? 0.f : __fmul_ru(__fmul_ru(float(S), __fadd_ru(mx, csum)), 2.38418579e-7f);
+            // ---- the group's amax interval and its E4M3 "up" code
+            float lo = __fsub_rd(mx, El), hi = __fadd_ru(mx, El);
+            if (glanes == 4) {           // the three partners at once: one shuffle latency
+                const float l1 = __shfl_xor_sync(0xffffffffu, lo, 1), l2 = __shfl_xor_sync(0xffffffffu, lo, 2),
+                            l3 = __shfl_xor_sync(0xffffffffu, lo, 3);
+                const float h1 = __shfl_xor_sync(0xffffffffu, hi, 1), h2 = __shfl_xor_sync(0xffffffffu, hi, 2),
+                            h3 = __shfl_xor_sync(0xffffffffu, hi, 3);
+                lo = fmaxf(fmaxf(lo, l1), fmaxf(l2, l3));
+                hi = fmaxf(fmaxf(hi, h1), fmaxf(h2, h3));
+            } else {
+                for (int m = 1; m < glanes; m <<= 1) {
+                    lo = fmaxf(lo, __shfl_xor_sync(0xffffffffu, lo, m));
+                    hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, m));
+                }
             }
-        }
-        // ---- scale codes for every row (branch-free), then the rare exact fix
-        bool valid[kU], camb[kU];
-        float E[kU];
-        uint32_t code[kU];
-#pragma unroll
-        for (int u = 0; u < kU; u++) {
-            valid[u] = u * rpp + rslot < nr;
-            E[u] = __fmul_ru(eb[u], 2.38418579e-7f);      // 2^-22
-            const float lo = __fsub_rd(am[u], E[u]), hi = __fadd_ru(am[u], E[u]);
             bool cb = false;
-            const uint32_t cc = scale_code<QMAX>(lo > 0.f ? lo : hi, hi, cb);
-            const bool zero = am[u] == 0.f && E[u] == 0.f;
-            code[u] = zero || !(lo > 0.f) ? 0x38u : cc;
-            camb[u] = valid[u] && !zero && (cb || !(lo > 0.f));
-        }
-        if (__any_sync(0xffffffffu, camb[0] || camb[kU - 1])) {      // exact scale (rare, out of line)
+            uint32_t code;
+            if constexpr (QMAX == 1) {
+                // normal E4M3 range: the ceiling code from the f32 bits (3 mantissa
+                // bits kept, rounded up), its lower neighbour's value one step down
+                const float hc = fminf(hi, 448.f);
+                const uint32_t t = (__float_as_uint(hc) + 0xFFFFFu) & 0xFFF00000u;
+                if (hc >= 0.015625f) {
+                    code = (t >> 20) - (120u << 3);
+                    cb = !(lo > __uint_as_float(t - 0x100000u));
+                } else {
+                    code = e4m3_ceil_f32_bf(hi);
+                    cb = !(lo > e4m3_decode_fast(code - 1u));
+                }
+            } else {
+                code = scale_code<QMAX>(lo > 0.f ? lo : hi, hi, cb);
+            }
+            const bool zero = hi == 0.f;                            // exact all-zero group
+            if (zero || !(lo > 0.f)) code = 0x38u;
+            const bool camb = valid && !zero && (cb || !(lo > 0.f));
+            if (__any_sync(0xffffffffu, camb)) {                    // exact scale (rare)
+                double a64 = 0.0;
+                if (camb) {
+                    // elements whose true |r| could reach the group's lower bound
+                    const float thr = __fsub_rd(lo, El);
+                    uint32_t cand = 0;
 #pragma unroll
-            for (int u = 0; u < kU; u++)
-                code[u] = fix_scale<QMAX, S, XBF16>(st + lr[u] * g.big_row + col * XB, tab, g.pitch, coff, int(g.K),
-                                                    ai[u][0], ai[u][SS > 1 ? 1 : 0], ai[u][SS > 2 ? 2 : 0],
-                                                    ai[u][SS > 3 ? 3 : 0], am[u], E[u], camb[u], glanes, code[u]);
-        }
-        // ---- codes: bits of fma(r, 1/s, MAGIC) = 0x4B400000 + q + 2^(b-1), packed by
-        // a multiply-add tree; the ambiguity window reduced over the row
-        Words4 b32[kU];
-        float sv[kU], inv[kU], thr[kU];
-        bool amb[kU], allv[kU];
-#pragma unroll
-        for (int u = 0; u < kU; u++) {
-            sv[u] = e4m3_decode_fast(code[u]);
-            inv[u] = rcp_tab[code[u] & 0x7Fu];
-            const float2 inv2 = make_float2(inv[u], inv[u]);
-            uint32_t f[16];
+                    for (int q = 0; q < 8; q++)
+                        cand |= (fabsf(r[q].x) >= thr ? 1u << (2 * q) : 0u) | (fabsf(r[q].y) >= thr ? 2u << (2 * q) : 0u);
+                    if (cand)
+                        a64 = exact_absmax<S, XBF16>(xr, tab, pitch, coff, int(KK), ai[0], ai[SS > 1 ? 1 : 0],
+                                                     ai[SS > 2 ? 2 : 0], ai[SS > 3 ? 3 : 0], cand);
+                }
+                for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
+                if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
+            }
+            // ---- codes
+            const float sv = e4m3_decode_fast(code);
+            const float inv = rcp_tab[code & 0x7Fu];
+            const float2 inv2 = make_float2(inv, inv);
             float2 yv[8];
 #pragma unroll
-            for (int q = 0; q < 8; q++) {
-                yv[q] = __ffma2_rn(r[u][q], inv2, make_float2(MAGIC, MAGIC));
-                f[2 * q] = __float_as_uint(yv[q].x);
-                f[2 * q + 1] = __float_as_uint(yv[q].y);
-            }
+            for (int q = 0; q < 8; q++) yv[q] = __ffma2_rn(r[q], inv2, make_float2(MAGIC, MAGIC));
+            Words4 b32;
 #pragma unroll
             for (int w = 0; w < BITS / 2; w++) {
                 uint32_t v[FPW];
 #pragma unroll
-                for (int k2 = 0; k2 < FPW; k2++) v[k2] = f[w * FPW + k2];
+                for (int k2 = 0; k2 < FPW; k2++) {
+                    const int e = w * FPW + k2;
+                    v[k2] = __float_as_uint((e & 1) ? yv[e >> 1].y : yv[e >> 1].x);
+                }
 #pragma unroll
                 for (int span = 1; span < FPW; span *= 2)
 #pragma unroll
                     for (int k2 = 0; k2 < FPW; k2 += 2 * span) v[k2] += v[k2 + span] << (BITS * span);
-                b32[u].w[w] = (v[0] - magic_sum<BITS>()) ^ SIGNS;
+                b32.w[w] = (v[0] - magic_sum<BITS>()) ^ SIGNS;
             }
-            allv[u] = !(E[u] < 0.125f * sv[u]) || code[u] == 0x7Eu;
-            thr[u] = window_thr<QMAX>(sv[u], inv[u], E[u]);
-            float wv[8];
+            const bool allv = !(El < 0.125f * sv) || code == 0x7Eu;
+            const float thr = window_thr<QMAX>(sv, inv, El);
+            bool amb;
             if constexpr (QMAX == 1) {
-                const float h = 0.5f * sv[u];
-                const float2 pa = make_float2(-h * h, -h * h);
+                // exact without a window: certified lane, s/2 a multiple of unit
+                // (its lowest set bit >= 2^(exponent(s) - 4)), s/2 < 2^22 unit
+                const float sexp = __uint_as_float(__float_as_uint(sv) & 0x7F800000u);
+                const bool fast = cert && code != 0x7Eu && sexp * 0.0625f >= un && sv < un * 4194304.f;
+                amb = false;
+                if (__any_sync(0xffffffffu, !fast)) {
+                    const float h = 0.5f * sv;
+                    const float2 pa = make_float2(-h * h, -h * h);
+                    float w0 = __int_as_float(0x7F800000), w1 = w0;
 #pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const float2 gg = __ffma2_rn(r[u][q], r[u][q], pa);
-                    wv[q] = fminf(fabsf(gg.x), fabsf(gg.y));
+                    for (int q = 0; q < 8; q += 2) {
+                        const float2 g0 = __ffma2_rn(r[q], r[q], pa);
+                        const float2 g1 = __ffma2_rn(r[q + 1], r[q + 1], pa);
+                        w0 = min3_abs(w0, g0.x, g0.y);
+                        w1 = min3_abs(w1, g1.x, g1.y);
+                    }
+                    amb = !fast && (allv || fminf(w0, w1) <= thr);
                 }
-#pragma unroll
-                for (int span = 1; span < 8; span *= 2)
-#pragma unroll
-                    for (int q = 0; q < 8; q += 2 * span) wv[q] = fminf(wv[q], wv[q + span]);
-                amb[u] = allv[u] || wv[0] <= thr[u];
             } else {
                 const float2 pa = make_float2(-MAGIC, -MAGIC);
+                float w0 = 0.f, w1 = 0.f;
 #pragma unroll
-                for (int q = 0; q < 8; q++) {
-                    const float2 qf = __fadd2_rn(yv[q], pa);
-                    const float2 dist = __ffma2_rn(r[u][q], inv2, make_float2(-qf.x, -qf.y));
-                    wv[q] = fmaxf(fabsf(dist.x), fabsf(dist.y));
+                for (int q = 0; q < 8; q += 2) {
+                    const float2 q0 = __fadd2_rn(yv[q], pa), q1 = __fadd2_rn(yv[q + 1], pa);
+                    const float2 d0 = __ffma2_rn(r[q], inv2, make_float2(-q0.x, -q0.y));
+                    const float2 d1 = __ffma2_rn(r[q + 1], inv2, make_float2(-q1.x, -q1.y));
+                    w0 = max3_abs(w0, d0.x, d0.y);
+                    w1 = max3_abs(w1, d1.x, d1.y);
                 }
-#pragma unroll
-                for (int span = 1; span < 8; span *= 2)
-#pragma unroll
-                    for (int q = 0; q < 8; q += 2 * span) wv[q] = fmaxf(wv[q], wv[q + span]);
-                amb[u] = allv[u] || wv[0] >= thr[u];
+                amb = allv || fmaxf(w0, w1) >= thr;
             }
-            amb[u] &= valid[u];
-        }
-        if (amb[0] || amb[kU - 1]) {      // exact codes (rare, out of line)
-#pragma unroll
-            for (int u = 0; u < kU; u++)
-                if (amb[u])
-                    b32[u] = fix_codes<BITS, S, XBF16>(st + lr[u] * g.big_row + col * XB, tab, g.pitch, coff,
-                                                       int(g.K), ai[u][0], ai[u][SS > 1 ? 1 : 0],
-                                                       ai[u][SS > 2 ? 2 : 0], ai[u][SS > 3 ? 3 : 0], sv[u], inv[u],
-                                                       E[u], thr[u], allv[u], b32[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < kU; u++) {
-            if (!valid[u]) continue;
-            const uint32_t e0 = (sc.i0 + lr[u]) * d + col;
-            uint8_t *plp = a.payload + uint64_t(p) * a.pb + ((e0 * BITS) >> 3);
-            if constexpr (BITS == 2) *reinterpret_cast<uint32_t *>(plp) = b32[u].w[0];
-            else if constexpr (BITS == 4) *reinterpret_cast<uint2 *>(plp) = make_uint2(b32[u].w[0], b32[u].w[1]);
-            else *reinterpret_cast<uint4 *>(plp) = make_uint4(b32[u].w[0], b32[u].w[1], b32[u].w[2], b32[u].w[3]);
-            if ((lane & (glanes - 1)) == 0) a.scales[uint64_t(p) * a.ng + (e0 >> a.lgB)] = uint8_t(code[u]);
+            if (amb && valid)          // exact codes of the flagged elements (rare)
+                b32 = fix_codes<BITS, S, XBF16>(xr, tab, pitch, coff, int(KK), ai[0], ai[SS > 1 ? 1 : 0],
+                                                ai[SS > 2 ? 2 : 0], ai[SS > 3 ? 3 : 0], sv, inv, El, thr, allv, b32);
+            if (valid) {
+                const uint32_t e0 = (sc.i0 + lr) * d + col;
+                uint8_t *plp = pay + ((e0 * BITS) >> 3);
+                if constexpr (BITS == 2) *reinterpret_cast<uint32_t *>(plp) = b32.w[0];
+                else if constexpr (BITS == 4) *reinterpret_cast<uint2 *>(plp) = make_uint2(b32.w[0], b32.w[1]);
+                else *reinterpret_cast<uint4 *>(plp) = make_uint4(b32.w[0], b32.w[1], b32.w[2], b32.w[3]);
+                if (slead) scl[e0 >> a.lgB] = uint8_t(code);
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.empty[k]);
@@ -578,13 +596,13 @@ static int ilog2i(int v) { int l = 0; while ((1 << l) < v) l++; return l; }
 // smem: [bf16 staging][f32 padded tables][metadata][ring]; false when the
 // configuration does not fit this kernel (callers fall back to v4/v5/v6)
 static bool plan(bool quant, int64_t P, int64_t N, int d, int S, int K, int bits, int B, int xbytes,
-                 uintptr_t align_probe, Geo &g, size_t &smem, int &grid) {
+                 uintptr_t align_probe, Geo &g, size_t &smem, int &grid, int cw = kCW, int ru = kU) {
     if (S < 1 || S > 4 || d % 16 != 0 || d > 512 || N < 4 || N % 4 != 0) return false;
     const int n = d / 16;
     if (n & (n - 1)) return false;
     if ((align_probe & 3u) != 0) return false;
     if (P * N >= (int64_t(1) << 31) || N * d >= (int64_t(1) << 31)) return false;
-    const uint32_t R = uint32_t(kCW * 32 / n * kU);
+    const uint32_t R = uint32_t(cw * 32 / n * ru);
     const uint32_t pitch = uint32_t(16 * n + 4 * ((n + 1) / 2));
     const size_t tbytes = size_t(S) * K * d * 2;
     const size_t tabb = size_t(S) * K * pitch * 4;
@@ -607,7 +625,8 @@ static bool plan(bool quant, int64_t P, int64_t N, int d, int S, int K, int bits
     const size_t small = size_t(R) * small_row + size_t(S) * R;
     const size_t stage = (big + ((small + 15) & ~size_t(15)) + 127) & ~size_t(127);
     const size_t budget = 227 * 1024 - 1024;
-    if (off_ring + 2 * stage > budget) {
+    static const bool force_global = [] { const char *e = getenv("QVG_STREAM_STGG"); return e && atoi(e) == 1; }();
+    if (off_ring + 2 * stage > budget || (quant && force_global)) {
         // no room for the bf16 staging copy: widen straight from global memory
         stg_global = 1;
         off_tab = 0;
@@ -636,16 +655,37 @@ static bool plan(bool quant, int64_t P, int64_t N, int d, int S, int K, int bits
     return true;
 }
 
-template <int BITS, int S>
-static int launch_q(const QuantArgs &a, bool xbf16, const Geo &g, size_t smem, int grid, cudaStream_t st) {
-    if (xbf16) {
-        cudaFuncSetAttribute(k_quantize_stream<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k_quantize_stream<BITS, S, true><<<grid, kThreads, smem, st>>>(a, g);
-    } else {
-        cudaFuncSetAttribute(k_quantize_stream<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        k_quantize_stream<BITS, S, false><<<grid, kThreads, smem, st>>>(a, g);
+// consumer warps x rows per thread per stage of the quantize kernel
+struct QCfg { int cw, ru; };
+static QCfg quant_cfg(int bits, int S, bool xbf16) {
+    static const int sel = [] { const char *e = getenv("QVG_QS_CFG"); return e ? atoi(e) : 0; }();
+    if (bits == 2 && S == 2 && xbf16) {      // measurement knob (Self-Forcing bench config)
+        if (sel == 1) return {23, 1};
+        if (sel == 2) return {23, 2};
+        if (sel == 3) return {15, 1};
+        if (sel == 4) return {20, 1};
     }
+    return {kCW, kU};
+}
+
+template <int BITS, int S, bool XB, int CW, int QU>
+static int launch_q1(const QuantArgs &a, const Geo &g, size_t smem, int grid, cudaStream_t st) {
+    cudaFuncSetAttribute(k_quantize_stream<BITS, S, XB, CW, QU>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    k_quantize_stream<BITS, S, XB, CW, QU><<<grid, 32 * (CW + 1), smem, st>>>(a, g);
     return 1;
+}
+
+template <int BITS, int S>
+static int launch_q(const QuantArgs &a, bool xbf16, const Geo &g, size_t smem, int grid, cudaStream_t st,
+                    QCfg qc) {
+    if constexpr (BITS == 2 && S == 2) {
+        if (xbf16 && qc.cw == 23 && qc.ru == 1) return launch_q1<2, 2, true, 23, 1>(a, g, smem, grid, st);
+        if (xbf16 && qc.cw == 23 && qc.ru == 2) return launch_q1<2, 2, true, 23, 2>(a, g, smem, grid, st);
+        if (xbf16 && qc.cw == 15 && qc.ru == 1) return launch_q1<2, 2, true, 15, 1>(a, g, smem, grid, st);
+        if (xbf16 && qc.cw == 20 && qc.ru == 1) return launch_q1<2, 2, true, 20, 1>(a, g, smem, grid, st);
+    }
+    return xbf16 ? launch_q1<BITS, S, true, kCW, kU>(a, g, smem, grid, st)
+                 : launch_q1<BITS, S, false, kCW, kU>(a, g, smem, grid, st);
 }
 
 template <int BITS, int S>
@@ -670,14 +710,15 @@ int launch_quantize_stream(const QuantArgs &a, int64_t P, int bits, int S, bool 
     size_t smem;
     int grid;
     const uintptr_t probe = reinterpret_cast<uintptr_t>(a.asg) | reinterpret_cast<uintptr_t>(a.x);
-    if (!plan(true, P, a.N, a.d, S, a.K, bits, a.B, xbf16 ? 2 : 4, probe, g, smem, grid)) return 0;
+    const QCfg qc = quant_cfg(bits, S, xbf16);
+    if (!plan(true, P, a.N, a.d, S, a.K, bits, a.B, xbf16 ? 2 : 4, probe, g, smem, grid, qc.cw, qc.ru)) return 0;
     if ((reinterpret_cast<uintptr_t>(a.x) & 15u) != 0) return 0;
 #define QV_Q(BB)                                                      \
     switch (S) {                                                      \
-        case 1: return launch_q<BB, 1>(a, xbf16, g, smem, grid, st); \
-        case 2: return launch_q<BB, 2>(a, xbf16, g, smem, grid, st); \
-        case 3: return launch_q<BB, 3>(a, xbf16, g, smem, grid, st); \
-        default: return launch_q<BB, 4>(a, xbf16, g, smem, grid, st); \
+        case 1: return launch_q<BB, 1>(a, xbf16, g, smem, grid, st, qc); \
+        case 2: return launch_q<BB, 2>(a, xbf16, g, smem, grid, st, qc); \
+        case 3: return launch_q<BB, 3>(a, xbf16, g, smem, grid, st, qc); \
+        default: return launch_q<BB, 4>(a, xbf16, g, smem, grid, st, qc); \
     }
     if (bits == 2) { QV_Q(2) }
     if (bits == 4) { QV_Q(4) }

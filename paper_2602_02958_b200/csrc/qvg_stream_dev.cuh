@@ -35,8 +35,9 @@ struct Geo {
 // puts the 8 blocks of a 128-channel row on 8 distinct bank quads
 __host__ __device__ __forceinline__ uint32_t blk_off(uint32_t c) { return 16u * c + 4u * (c >> 1); }
 
+template <int CW = kCW>
 __device__ __forceinline__ void named_sync_consumers() {
-    asm volatile("bar.sync 1, %0;" ::"n"(kCW * 32) : "memory");
+    asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
@@ -57,6 +58,18 @@ __device__ __forceinline__ void bulk_g2s_cta(void *dst, const void *src, uint32_
 __device__ __forceinline__ float max_nan(float a, float b) {
     float d;
     asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+    return d;
+}
+__device__ __forceinline__ float min3_abs(float m, float a, float b) {
+    float t, d;
+    asm("min.f32 %0, %1, %2;" : "=f"(t) : "f"(fabsf(a)), "f"(fabsf(b)));
+    asm("min.f32 %0, %1, %2;" : "=f"(d) : "f"(m), "f"(t));
+    return d;
+}
+__device__ __forceinline__ float max3_abs(float m, float a, float b) {
+    float t, d;
+    asm("max.f32 %0, %1, %2;" : "=f"(t) : "f"(fabsf(a)), "f"(fabsf(b)));
+    asm("max.f32 %0, %1, %2;" : "=f"(d) : "f"(m), "f"(t));
     return d;
 }
 __device__ __forceinline__ float max3_nan_abs(float m, float a, float b) {
@@ -225,6 +238,22 @@ __device__ __noinline__ uint32_t fix_scale(const uint8_t *xrow, const float *tab
     for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
     if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
     return code;
+}
+
+// max over the masked elements of the reference's float64 |residual|
+// (Q/smoothing.py:40) -- the exact group amax when its f32 interval straddles
+// an E4M3 code boundary
+template <int S, bool XBF16>
+__device__ __noinline__ double exact_absmax(const uint8_t *xrow, const float *tab, uint32_t pitch, uint32_t coff,
+                                            int K, int a0, int a1, int a2, int a3, uint32_t mask) {
+    const int ai[4] = {a0, a1, a2, a3};
+    double m = 0.0;
+    while (mask) {
+        const int k = __ffs(mask) - 1;
+        mask &= mask - 1;
+        m = fmax(m, fabs(exact_residual_row<S>(xat<XBF16>(xrow, k), tab, pitch, coff + k, K, ai)));
+    }
+    return m;
 }
 
 // exact codes of the elements in the ambiguity window (or all when `all`):
