@@ -3,18 +3,27 @@
 Headline metric (BASELINE.json): KV quant+dequant GB/s (% HBM roofline);
 quantized-attn latency vs bf16; KV compression.
 
-Workload (N=1, configs[1]): the Self-Forcing / Wan2.1-1.3B-shaped KV cache of
-a 10 s rollout — 30 layers x 12 heads x {K, V} x 14 chunks of 4680 tokens
-(3 latent frames x 1560 tokens) = 10 080 planes of 4680 x 128 bf16
-(12.1 GB), QVG b=2, B=64, S=2, K=64.  One step = quantize every plane
-(given its stage metadata, computed once by the on-device k-means before
-timing) + dequantize every plane to bf16, each one kernel launch over the
-whole cache.  Inputs live in HBM and are ~100x the L2, so no flush is
-needed.  Synthetic clustered data (paper_2602_02958_b200/synth.py).
+Workload (configs[1], C2): the Self-Forcing / Wan2.1-1.3B-shaped KV cache of a
+10 s rollout -- 30 layers x 12 heads x {K, V} x 14 chunks of 4680 tokens
+(3 latent frames x 1560 tokens) = 10 080 planes of 4680 x 128 bf16 (12.1 GB),
+QVG b=2, B=64, S=2, K=64.  One step = quantize every plane (given its stage
+metadata, computed once by the on-device k-means before timing) + dequantize
+every plane to bf16, each one kernel launch over the rank's planes.  Inputs
+live in HBM and are ~100x the L2, so no flush is needed.
+
+Data: the reference generator's planes (Q/datagen.py gen_clustered_stream,
+restated bit-identically in paper_2602_02958_b200/datagen.py), SURVEY §8(d)
+parameters: drift 0.1*sigma_within for C2/C4, K planes x10 / V planes x100 on
+the outlier channels, rounded to bf16 -- the bf16 device input and the CPU
+reference input are the same numbers.
+
+Multi-GPU (python -m torch.distributed.run ... bench.py --gpus N): the fixed
+cache is partitioned by (layer, head) pairs (shard.plane_pairs: 360 pairs,
+45 per GPU at N = 8); stage seeds do not depend on the head (Q/prq.py:32-35),
+so every rank's planes are bit-identical to the 1-GPU run.  No collective on
+the data path; value = all ranks' bytes / max-over-ranks time ("strong").
 
 python bench.py [--gpus N --steps K --warmup W] [--impl reference]
-Under torchrun each rank runs its own cache (weak scaling, no collective on
-the data path); rank 0 prints one JSON line.
 """
 
 from __future__ import annotations
@@ -32,17 +41,22 @@ import torch
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2602_02958_b200 import datagen as G  # noqa: E402
 from paper_2602_02958_b200 import device as D  # noqa: E402
 from paper_2602_02958_b200.qvgcodec.metrics import memory_breakdown  # noqa: E402
 from paper_2602_02958_b200.qvgcodec.types import ChunkSpec, QuantConfig  # noqa: E402
-from paper_2602_02958_b200.synth import kv_cache_planes  # noqa: E402
+from paper_2602_02958_b200.shard import plane_pairs  # noqa: E402
 
 METRIC = "KV quant+dequant GB/s (% HBM roofline); quantized-attn latency vs bf16; KV compression"
+SIGMA_WITHIN = 0.125
 WORKLOADS = {
-    # name: (layers, heads, chunks, tokens per chunk, config)
-    "self_forcing_10s": (30, 12, 14, 4680, dict(bits=2, group_size=64, stages=2, centroids=64)),
-    "config1_cpu_case": (1, 12, 1, 4680, dict(bits=2, group_size=64, stages=2, centroids=64)),
+    # name: (layers, heads, chunks, tokens per chunk, drift, config)
+    "self_forcing_10s": (30, 12, 14, 4680, 0.1 * SIGMA_WITHIN,
+                         dict(bits=2, group_size=64, stages=2, centroids=64)),
+    "config1_cpu_case": (1, 12, 1, 4680, 0.0, dict(bits=2, group_size=64, stages=2, centroids=64)),
 }
+DATA = ("reference generator (Q/datagen.py gen_clustered_stream restated bit-identically in "
+        "paper_2602_02958_b200/datagen.py), bf16-rounded, SURVEY 8(d) parameters")
 
 
 def peaks():
@@ -109,28 +123,48 @@ class Clocks:
                 "samples": len(rows)}
 
 
-def build_cache(workload, rank, device):
-    L, H, C, N, cfgd = WORKLOADS[workload]
+def rank_refs(workload, world, rank):
+    """This rank's planes, chunk-major: per chunk its (layer, head) pairs x {K, V}."""
+    L, H, C, N, drift, _ = WORKLOADS[workload]
+    pairs = plane_pairs(L, H, world, rank)
+    per_chunk = [[G.PlaneRef(l, h, v, c) for (l, h) in pairs for v in (False, True)] for c in range(C)]
+    return per_chunk
+
+
+def host_planes(refs, n_heads, n_tokens, drift):
+    """[P, N, d] bf16 bit patterns (uint16) from the reference generator."""
+    return G.kv_cache_bf16(refs, n_heads, n_tokens, drift=drift)
+
+
+def to_device_bf16(u16, dev):
+    return torch.from_numpy(np.ascontiguousarray(u16).view(np.int16)).to(dev).view(torch.bfloat16)
+
+
+def build_cache(workload, world, rank, device):
+    """Generate this rank's planes of every chunk on the host, compress each
+    chunk on the device (chunk_index = chunk number, Q/prq.py:49)."""
+    L, H, C, N, drift, cfgd = WORKLOADS[workload]
     cfg = QuantConfig(**cfgd)
-    P_chunk = L * H * 2
-    xs, chunks, enc_ms = [], [], []
+    per_chunk = rank_refs(workload, world, rank)
+    t0 = time.perf_counter()
+    host = host_planes([r for ch in per_chunk for r in ch], H, N, drift)
+    gen_s = time.perf_counter() - t0
+    Pc = len(per_chunk[0])
+    x = torch.empty((Pc * C, N, 128), dtype=torch.bfloat16, device=device)
+    chunks, enc_ms = [], []
     for c in range(C):
-        x = kv_cache_planes(L, H, N, 128, seed=1000 * rank + c, device=device)
+        x[c * Pc:(c + 1) * Pc] = to_device_bf16(host[c * Pc:(c + 1) * Pc], device)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        dc = D.compress(x, cfg, chunk_index=c, check=(c == 0))
+        dc = D.compress(x[c * Pc:(c + 1) * Pc], cfg, chunk_index=c, check=(c == 0))
         torch.cuda.synchronize()
         enc_ms.append((time.perf_counter() - t0) * 1e3)
-        xs.append(x)
         chunks.append(dc)
-    x = torch.cat(xs)
-    del xs
     cat = lambda f: torch.cat([getattr(dc, f) for dc in chunks])
-    dc = D.DeviceChunks(cfg, N, 128, cat("payload"), cat("scales"), cat("centroids"),
-                        cat("assignments"))
+    dc = D.DeviceChunks(cfg, N, 128, cat("payload"), cat("scales"), cat("centroids"), cat("assignments"))
     del chunks
     torch.cuda.empty_cache()
-    return cfg, x, dc, P_chunk, enc_ms
+    return cfg, host, x, dc, Pc, enc_ms, gen_s
 
 
 def time_ms(fn, reps=5, warmup=2):
@@ -146,20 +180,30 @@ def time_ms(fn, reps=5, warmup=2):
     return e0.elapsed_time(e1) / reps
 
 
-def bench_attention(dev, rank, world=1, H=32, nc=38400, nq=7800, d=128):
-    """LongCat-Video-shaped layer (configs[2]): 32 heads, ~38K-token cache
-    (QVG b2 S1 K256 B64), current chunk of 7800 tokens attending to cache +
-    itself.  Quantized-cache attention vs the same kernel on the bf16 cache
-    and vs torch SDPA (cuDNN/flash, library comparator).  Under torchrun the
-    heads are sharded over the ranks (shard.head_range, no collective on the
-    hot path) and the per-rank outputs are all-gathered over NCCL; latencies
-    are the max over ranks."""
+def allmax(vals, dev, world):
+    if world == 1:
+        return vals
+    t = torch.tensor([float(v) for v in vals], device=dev, dtype=torch.float64)
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return [float(v) for v in t.tolist()]
+
+
+def bench_attention(dev, rank, world, H=32, nc=38400, nq=7800, d=128):
+    """LongCat-Video-shaped layer (configs[2], C3): 32 heads, 38 400-token
+    cache (QVG b2 S1 K256 B64, reference-generator planes, drift 0), current
+    chunk of 7 800 tokens attending to cache + itself.  Quantized-cache
+    attention vs the same kernel on the bf16 cache and vs torch SDPA
+    (cuDNN/flash, library comparator).  Under torchrun the heads are sharded
+    over the ranks (shard.head_range, no collective on the hot path) and the
+    per-rank outputs are all-gathered (NCCL on the GPU box); latencies are
+    the max over ranks."""
     from paper_2602_02958_b200.shard import gather_heads, head_range
 
     h0, h1 = head_range(H, world, rank)
     Hr = h1 - h0
     cfg = QuantConfig(bits=2, group_size=64, stages=1, centroids=256)
-    planes = kv_cache_planes(1, H, nc, d, seed=77, device=dev)[2 * h0:2 * h1].contiguous()  # this rank's K,V
+    refs = [G.PlaneRef(0, h, v, 0) for h in range(h0, h1) for v in (False, True)]
+    planes = to_device_bf16(host_planes(refs, H, nc, 0.0), dev)            # this rank's K, V planes
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     chunks = D.compress(planes, cfg, chunk_index=0)
@@ -190,10 +234,8 @@ def bench_attention(dev, rank, world=1, H=32, nc=38400, nq=7800, d=128):
         ms_sdpa = time_ms(lambda: torch.nn.functional.scaled_dot_product_attention(qq, kall, vall))
     except Exception:
         ms_sdpa = None
-    if world > 1:
-        t = torch.tensor([ms_q, ms_b, ms_sdpa or 0.0, ms_g], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms_q, ms_b, ms_sdpa, ms_g = (float(v) for v in t.tolist())
+    ms_q, ms_b, ms_sdpa_m, ms_gm = allmax([ms_q, ms_b, ms_sdpa or 0.0, ms_g or 0.0], dev, world)
+    ms_sdpa = ms_sdpa_m or None
     flops = 4.0 * nq * (nc + nq) * d * H          # whole layer, all ranks
     _, tf_peak, tf_sus, kind = peaks()
     res = {
@@ -210,10 +252,54 @@ def bench_attention(dev, rank, world=1, H=32, nc=38400, nq=7800, d=128):
         "encode_s": round(enc_s, 3),
         "kv_compression": round(memory_breakdown(cfg, ChunkSpec(nc, d)).ratio_vs_bf16, 3),
     }
-    if ms_g is not None:
-        res["allgather_ms_nccl"] = round(ms_g, 3)
-        res["latency_ms_quantized_plus_gather"] = round(ms_q + ms_g, 3)
+    if world > 1:
+        backend = torch.distributed.get_backend()
+        res[f"allgather_ms_{backend}"] = round(ms_gm, 3)
+        res["latency_ms_quantized_plus_gather"] = round(ms_q + ms_gm, 3)
     return res
+
+
+def bench_stage_sweep(dev, rank, world, H=24, N=4680, chunks=(0, 1)):
+    """C4 (HY-WorldPlay 60 s long-horizon cache, configs[3]): PRQ stage sweep
+    S = 0..4 x B in {16, 64} on streaming 4680-token chunks (12 latent frames,
+    PAPER.md:462) of one layer's 24 heads x {K, V} (builder's choice: HY-World
+    / HunyuanVideo-class 24 heads x 128; layers and the 120-chunk rollout
+    repeat this per-chunk workload).  Per (S, B): stage_mse_curve's MSE
+    (Q/prq.py:135-172, mean over planes), memory ratio, device encode time.
+    Heads are sharded over the ranks; MSE sums are reduced over ranks."""
+    from paper_2602_02958_b200.shard import head_range
+
+    h0, h1 = head_range(H, world, rank)
+    refs = [G.PlaneRef(0, h, v, c) for c in chunks for h in range(h0, h1) for v in (False, True)]
+    host = host_planes(refs, H, N, 0.1 * SIGMA_WITHIN)
+    x = to_device_bf16(host, dev)
+    P = x.shape[0] // len(chunks)
+    xf = x.double()
+    out = []
+    for B in (16, 64):
+        for S in range(0, 5):
+            cfg = QuantConfig(bits=2, group_size=B, stages=S, centroids=64)
+            se, n, enc = 0.0, 0, 0.0
+            for ci, c in enumerate(chunks):
+                xs = x[ci * P:(ci + 1) * P]
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                dc = D.compress(xs, cfg, chunk_index=c)
+                torch.cuda.synchronize()
+                enc += (time.perf_counter() - t0) * 1e3
+                rec = D.dequantize(dc, torch.float32)
+                se += float(((xf[ci * P:(ci + 1) * P] - rec.double()) ** 2).sum())
+                n += rec.numel()
+            t = torch.tensor([se, n], device=dev, dtype=torch.float64)
+            if world > 1:
+                torch.distributed.all_reduce(t)
+            enc_ms = allmax([enc / len(chunks)], dev, world)[0]
+            out.append({"B": B, "S": S, "mse": float(t[0] / t[1]),
+                        "ratio": round(memory_breakdown(cfg, ChunkSpec(N, 128)).ratio_vs_bf16, 3),
+                        "encode_ms_per_chunk": round(enc_ms, 2)})
+    return {"workload": "hy_worldplay_stage_sweep", "heads": H, "layers_sampled": 1,
+            "chunks": list(chunks), "tokens_per_chunk": N, "planes_per_chunk": 2 * H, "bits": 2,
+            "centroids": 64, "drift": 0.1 * SIGMA_WITHIN, "curve": out}
 
 
 def cpu_sample_gbs(x_s, cent_s, asg_s, cfg, threads, min_seconds=10.0, max_seconds=30.0):
@@ -244,6 +330,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-attention", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -266,10 +353,12 @@ def main():
             dist.init_process_group(backend)
     hbm_peak, _, _, peak_kind = peaks()
 
-    cfg, x, dc, P_chunk, enc_ms = build_cache(args.workload, rank, dev)
+    cfg, host, x, dc, P_chunk, enc_ms, gen_s = build_cache(args.workload, world, rank, dev)
     P, N, d = x.shape
     qb, db = plane_bytes(N, d, cfg)
-    step_bytes = P * (qb + db)
+    L, H, C, _, drift, _ = WORKLOADS[args.workload]
+    P_total = L * H * 2 * C
+    step_bytes_total = P_total * (qb + db)
     payload = torch.empty_like(dc.payload)
     scales = torch.empty_like(dc.scales)
     out = torch.empty((P, N, d), dtype=torch.bfloat16, device=dev)
@@ -306,16 +395,16 @@ def main():
         stop.record()
         torch.cuda.synchronize()
     ms = start.elapsed_time(stop)
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-        torch.distributed.barrier()
     q_ms = float(np.mean([e[0].elapsed_time(e[1]) for e in evs]))
     dq_ms = float(np.mean([e[1].elapsed_time(e[2]) for e in evs]))
+    ms, q_ms, dq_ms = allmax([ms, q_ms, dq_ms], dev, world)
+    if world > 1:
+        torch.distributed.barrier()
     ms_step = ms / args.steps
-    value = world * step_bytes / (ms_step * 1e-3) / 1e9
+    value = step_bytes_total / (ms_step * 1e-3) / 1e9
 
+    # per-kernel rates of this rank's launches (max-over-ranks times, the
+    # largest rank's bytes: the roofline of the kernel as launched)
     kernels = {
         "quantize": {"ms": q_ms, "bytes": P * qb, "GBps": P * qb / q_ms / 1e6},
         "dequantize": {"ms": dq_ms, "bytes": P * db, "GBps": P * db / dq_ms / 1e6},
@@ -334,8 +423,9 @@ def main():
                 "peak_kind": peak_kind,
                 "per_kernel_frac": {k: round(v["GBps"] / hbm_peak, 4) for k, v in kernels.items()}}
 
-    # streaming warm start (SURVEY 8(f) row 1, Q/prq.py:61-71): chunk 1 encoded
-    # from chunk 0's float64 centroids of the same planes -- k-means++ skipped
+    # streaming warm start (SURVEY 8(f) row 1, Q/prq.py:61-71): chunk 1 of the
+    # drifting streams encoded from chunk 0's float64 centroids of the same
+    # (layer, head, K|V) streams -- k-means++ skipped
     warm = None
     if P >= 2 * P_chunk:
         c0 = D.compress(x[:P_chunk], cfg, chunk_index=0, keep_f64=True, check=False)
@@ -349,60 +439,74 @@ def main():
             del cw
         del c0
         warm = float(np.median(wms))
+    enc_chunk = float(np.median(enc_ms[1:] or enc_ms))
+    enc_chunk, warm_m = allmax([enc_chunk, warm or 0.0], dev, world)
+    warm = warm_m if warm is not None else None
+    planes_per_chunk_total = L * H * 2
 
     result = {
         "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": round(ms_step, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
-        "data": "synthetic (clustered bf16 K/V planes, random-init; paper_2602_02958_b200/synth.py)",
-        "config": {"workload": args.workload, "planes": P, "tokens_per_plane": N, "head_dim": d,
-                   "bits": cfg.bits, "group_size": cfg.group_size, "stages": cfg.stages,
-                   "centroids": cfg.centroids, "bytes_per_step": step_bytes,
-                   "parallelism": f"planes-per-rank x{world} (weak)",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": f"synthetic: {DATA}",
+        "config": {"workload": args.workload, "planes": P_total, "planes_per_rank": P,
+                   "tokens_per_plane": N, "head_dim": d, "bits": cfg.bits, "group_size": cfg.group_size,
+                   "stages": cfg.stages, "centroids": cfg.centroids, "drift": drift,
+                   "bytes_per_step": step_bytes_total,
+                   "parallelism": f"(layer, head) pairs partitioned over {world} rank(s) (strong)",
                    "l2": "inputs 100x larger than L2; no flush needed"},
         "roofline": roofline, "kernels": kernels,
         "kv_compression": round(memory_breakdown(cfg, ChunkSpec(N, d)).ratio_vs_bf16, 3),
-        "encode": {"tokens_per_s": round(P_chunk * N / (np.median(enc_ms[1:] or enc_ms) / 1e3), 1),
-                   "ms_per_chunk": round(float(np.median(enc_ms[1:] or enc_ms)), 2),
-                   "planes_per_chunk": P_chunk,
+        "encode": {"tokens_per_s": round(planes_per_chunk_total * N / (enc_chunk / 1e3), 1),
+                   "ms_per_chunk": round(enc_chunk, 2), "planes_per_chunk": planes_per_chunk_total,
+                   "planes_per_chunk_per_rank": P_chunk,
                    "note": "full prq_compress (k-means++ / Lloyd / smoothing / quantize), one chunk",
                    "warm_ms_per_chunk": None if warm is None else round(warm, 2),
-                   "warm_tokens_per_s": None if warm is None else round(P_chunk * N / (warm / 1e3), 1),
-                   "warm_note": "streaming warm start: the previous chunk's float64 centroids as init"},
+                   "warm_tokens_per_s": None if warm is None else round(planes_per_chunk_total * N / (warm / 1e3), 1),
+                   "warm_note": "streaming warm start: the previous chunk's float64 centroids of the "
+                                "same drifting streams as init",
+                   "host_datagen_s": round(gen_s, 1)},
         "gpu_launches": 2 * args.steps,
         "clocks": clk.summary(),
     }
     if not args.no_e2e:
-        result["e2e"] = run_e2e(cfg, x[:P_chunk], dc.select(slice(0, P_chunk)), dev, world)
+        result["e2e"] = run_e2e(cfg, x[:P_chunk], dc.select(slice(0, P_chunk)), dev, world,
+                                planes_total=planes_per_chunk_total)
     if rank == 0 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
         ns = max(threads, 8)
-        idx = torch.arange(ns) * (P // ns)
-        xs = x[idx].float().cpu().numpy()
-        cs = dc.centroids[idx].float().cpu().numpy()
-        asg = dc.assignments[idx].cpu().numpy()
+        idx = np.arange(ns) * (P // ns)
+        xs = G.bf16_bits_to_f32(host[idx])
+        cs = dc.centroids[torch.from_numpy(idx).to(dev)].float().cpu().numpy()
+        asg = dc.assignments[torch.from_numpy(idx).to(dev)].cpu().numpy()
         gbs, el, reps = cpu_sample_gbs(xs, cs, asg, cfg, threads)
         result["cpu_baseline"] = {
             "value": round(gbs, 3), "unit": "GB/s", "cores": threads, "kind": "port",
-            "sample": f"oracle quantize+dequantize of {ns} planes x {reps} reps ({el:.1f} s), "
+            "sample": f"oracle quantize+dequantize of {ns} of the same planes x {reps} reps ({el:.1f} s), "
                       f"same byte accounting"}
-    if not args.no_attention:
+    del host
+    if not args.no_attention or not args.no_sweep:
         del x, out, dq, payload, scales, dc
         torch.cuda.empty_cache()
+    if not args.no_attention:
         result["attention"] = bench_attention(dev, rank, world)
+    if not args.no_sweep:
+        result["stage_sweep"] = bench_stage_sweep(dev, rank, world)
     if rank == 0:
         print(json.dumps(result), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
 
 
-def run_e2e(cfg, x, dc, dev, world, n_chunks=8):
+def run_e2e(cfg, x, dc, dev, world, planes_total, n_chunks=8):
     """Same metric through the public API with HOST buffers: pinned H2D of the
     bf16 planes and their stage metadata, quantize, D2H of the compressed
     chunk (payload + scales), dequantize it, D2H of the decoded bf16 planes —
     all inside the timed region.  The planes go through in `n_chunks` slices
     on three CUDA streams, so one slice's device->host copies overlap other
-    slices' host->device copies and kernels (PCIe is full duplex)."""
+    slices' host->device copies and kernels (PCIe is full duplex).  One chunk
+    of the cache (its planes split over the ranks); value = the chunk's
+    bytes / max-over-ranks time."""
     P, N, d = x.shape
     xh = x.cpu().pin_memory()
     comp = [dc.payload, dc.scales, dc.centroids, dc.assignments]
@@ -457,42 +561,36 @@ def run_e2e(cfg, x, dc, dev, world, n_chunks=8):
         step()
     e1.record()
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / reps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-    return {"value": round(world * P * (qb + db) / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+    ms = allmax([e0.elapsed_time(e1) / reps], dev, world)[0]
+    return {"value": round(planes_total * (qb + db) / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-            "ms_per_step": round(ms, 3), "planes": P,
+            "ms_per_step": round(ms, 3), "planes": planes_total, "planes_per_rank": P,
             "path": "paper_2602_02958_b200.device.quantize/dequantize (C ABI) on pinned host buffers, "
-                "8 slices on 3 streams (copies overlap across slices)"}
+                    "8 slices on 3 streams (copies overlap across slices)"}
 
 
 def run_reference(args, world, rank):
     """--impl reference: the reference's CPU path (oracle C port of the
     numpy reference; the Python reference cannot travel to the box) timed on
     the host cores, same metric / unit / byte accounting, each step one
-    bounded sample of the workload (quantize + dequantize of sampled planes,
-    stage metadata from the oracle's own k-means)."""
+    bounded sample of the workload: quantize + dequantize of the first
+    planes of chunk 0 of the SAME reference-generator planes the GPU arm
+    compresses, with their stage metadata from the oracle's own k-means
+    (identical to the GPU's, parity-tested)."""
     if rank != 0:
         return
     import oracle
 
-    L, H, C, N, cfgd = WORKLOADS[args.workload]
+    L, H, C, N, drift, cfgd = WORKLOADS[args.workload]
     cfg = QuantConfig(**cfgd)
     threads = len(os.sched_getaffinity(0))
     ns = max(threads, 8)
-    rng = np.random.default_rng(0)
-    # clustered planes on the host (same generator family as synth.py)
-    means = rng.normal(0, 2.5, size=(ns, 256, 128))
-    asg0 = rng.integers(0, 256, size=(ns, N))
-    x = np.take_along_axis(means, asg0[:, :, None], 1) + rng.normal(0, 0.125, size=(ns, N, 128))
-    x[:, :, ::16] *= np.where(np.arange(ns) % 2 == 0, 10.0, 100.0)[:, None, None]
-    x = (x.astype(np.float32).view(np.uint32) & 0xFFFF0000).view(np.float32)
-    draws = np.stack([oracle.pp_draws(0, 0, cfg.stages, cfg.centroids)] * ns)
+    refs = rank_refs(args.workload, 1, 0)[0][:ns]
+    x = G.bf16_bits_to_f32(host_planes(refs, H, N, drift))
+    draws = np.stack([oracle.pp_draws(cfg.seed, 0, cfg.stages, cfg.centroids)] * ns)
     _, _, cent, asg, _ = oracle.prq_compress_batch(x, cfg.bits, cfg.group_size, cfg.stages,
-                                                   cfg.centroids, 10, 1e-4, draws, threads)
+                                                   cfg.centroids, cfg.kmeans_max_iters, cfg.kmeans_tol,
+                                                   draws, threads)
     qb, db = plane_bytes(N, 128, cfg)
     times = []
     for i in range(max(args.warmup, 3) + args.steps):
@@ -506,10 +604,10 @@ def run_reference(args, world, rank):
     res = {"metric": METRIC, "value": round(value, 3), "unit": "GB/s", "n_gpus": world,
            "steps": args.steps, "warmup": max(args.warmup, 3),
            "ms_per_step": round(sec / len(times) * 1e3, 3), "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64/f32 (reference numerics)",
-           "data": "synthetic clustered planes (host)", "impl": "reference",
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64/f32 (reference numerics)",
+           "data": f"synthetic: {DATA} (the GPU arm's chunk-0 planes)", "impl": "reference",
            "config": {"workload": args.workload, "sample_planes": ns, "tokens_per_plane": N,
-                      "head_dim": 128, **cfgd},
+                      "head_dim": 128, "drift": drift, **cfgd},
            "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
                             "kind": "port",
                             "sample": f"{ns} planes quantize+dequantize per step (oracle C port)"},

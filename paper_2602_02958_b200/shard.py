@@ -50,6 +50,10 @@ def gather_heads(local: torch.Tensor, n_heads: int, group: Optional[dist.Process
     buf = torch.empty((world, nq, hmax, d), dtype=local.dtype, device=local.device)
     if hasattr(dist, "all_gather_into_tensor") and local.is_cuda and dist.get_backend(group) == "nccl":
         dist.all_gather_into_tensor(buf, pad.contiguous(), group=group)
+    elif local.element_size() == 2 and d % 2 == 0:
+        # gloo has no 16-bit integer / bf16 all_gather: move the bits as int32 pairs
+        b32 = buf.view(torch.int32)
+        dist.all_gather(list(b32.unbind(0)), pad.contiguous().view(torch.int32), group=group)
     else:
         dist.all_gather(list(buf.unbind(0)), pad.contiguous(), group=group)
     out = torch.empty((nq, n_heads, d), dtype=local.dtype, device=local.device)

@@ -23,12 +23,12 @@ def test_head_range_partitions():
     assert kv_plane_index(1, 2, 12, 1) == 2 * (12 + 2) + 1
 
 
-def _worker(rank, world, port, H, ret):
+def _worker(rank, world, port, H, ret, dtype=torch.float32):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.manual_seed(0)
-    full = torch.randn(5, H, 16)                     # what a 1-GPU run would produce
+    full = torch.randn(5, H, 16).to(dtype)           # what a 1-GPU run would produce
     h0, h1 = head_range(H, world, rank)
     local = full[:, h0:h1].clone()                   # this rank's heads
     out = gather_heads(local, H)
@@ -37,11 +37,11 @@ def _worker(rank, world, port, H, ret):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("H", [4, 5])
-def test_gather_heads_gloo_world2(H):
+@pytest.mark.parametrize("H,dtype", [(4, torch.float32), (5, torch.float32), (5, torch.bfloat16)])
+def test_gather_heads_gloo_world2(H, dtype):
     world = 2
-    port = 29500 + H + os.getpid() % 1000
+    port = 29500 + H + (7 if dtype == torch.bfloat16 else 0) + os.getpid() % 1000
     mgr = mp.Manager()
     ret = mgr.dict()
-    mp.spawn(_worker, args=(world, port, H, ret), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, port, H, ret, dtype), nprocs=world, join=True)
     assert ret[0] and ret[1]

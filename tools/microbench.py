@@ -1,5 +1,7 @@
-"""BASELINE config 5 microbench: tokens 4K..256K x centroids 16..256 x bits 2/4
-(d = 128, B = 64, S = 1).  For each point: P planes so that P*N ~ 8M tokens,
+"""BASELINE config 5 microbench (C5): tokens 4K..256K (7 points) x centroids
+16..256 (5 points) x bits 2/4, d = 128, B = 64, S = 1, on the reference
+generator's planes (drift 0, K/V outlier scales as SURVEY 8(d)).  For each
+point: P planes so that P*N ~ 8M tokens,
 full encode (k-means + PRQ) tokens/s, quantize and dequantize GB/s with the
 same algorithmic byte accounting as bench.py (roofline fraction vs the
 measured HBM copy peak).  Writes one JSON document to stdout."""
@@ -14,19 +16,24 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2602_02958_b200 import device as D  # noqa: E402
 from paper_2602_02958_b200.qvgcodec.types import QuantConfig  # noqa: E402
-from paper_2602_02958_b200.synth import kv_cache_planes  # noqa: E402
+from paper_2602_02958_b200 import datagen as G  # noqa: E402
 
 
 def main():
     dev = torch.device("cuda", 0)
     hbm, _, _, kind = bench.peaks()
     points = []
-    for N in (4096, 16384, 65536, 262144):
-        for K in (16, 64, 256):
+    Ns = [int(v) for v in os.environ.get("MB_N", "4096,8192,16384,32768,65536,131072,262144").split(",")]
+    Ks = [int(v) for v in os.environ.get("MB_K", "16,32,64,128,256").split(",")]
+    for N in Ns:
+        P = max(2, (8 << 20) // N)
+        refs = [G.PlaneRef(0, h, v, 0) for h in range(P // 2) for v in (False, True)]
+        xh = G.kv_cache_bf16(refs, P // 2, N)
+        x = bench.to_device_bf16(xh, dev)
+        del xh
+        for K in Ks:
             for bits in (2, 4):
                 cfg = QuantConfig(bits=bits, group_size=64, stages=1, centroids=K)
-                P = max(2, (8 << 20) // N)
-                x = kv_cache_planes(1, P // 2, N, 128, seed=N + K, device=dev)
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 dc = D.compress(x, cfg, chunk_index=0)
@@ -46,9 +53,10 @@ def main():
                 pt["hbm_frac"] = round(pt["quant_dequant_GBps"] / hbm, 4)
                 points.append(pt)
                 print(json.dumps(pt), file=sys.stderr, flush=True)
-                del x, dc, pay, sc, out
+                del dc, pay, sc, out
                 torch.cuda.empty_cache()
-    print(json.dumps({"config": "BASELINE configs[4] microbench, d=128 B=64 S=1", "hbm_peak_GBps": hbm,
+        del x
+    print(json.dumps({"config": "BASELINE configs[4] microbench, d=128 B=64 S=1, reference-generator planes", "hbm_peak_GBps": hbm,
                       "peak_kind": kind, "points": points}))
 
 

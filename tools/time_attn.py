@@ -8,6 +8,6 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 
-r = bench.bench_attention(torch.device("cuda", 0), 0)
+r = bench.bench_attention(torch.device("cuda", 0), 0, 1)
 r["env"] = {k: v for k, v in os.environ.items() if k.startswith("QVG_")}
 print(json.dumps(r))
