@@ -234,6 +234,24 @@ QVG_API int qvg_hadamard(const void *x, int32_t x_dtype, int64_t n_rows, int32_t
 QVG_API int qvg_token_transpose(const void *x, int32_t x_dtype, int64_t n_planes, int64_t n_tokens,
                                 int64_t n_padded, int32_t d, int32_t inverse, float *out, void *stream);
 
+/* ---- QVGC records from / into device buffers (Q/container.py:158-218, 230-343) ----
+ * A batch of P planes in the DeviceChunks layout ([P] payload, [P] scales,
+ * [P][S][K][d] bf16 centroids, [P][S][N] assignments) <-> P back-to-back QVGC
+ * records (u32 chunk_index, n_tokens, payload_len, scales_len, body_len | body =
+ * payload | scales | per stage centroids (bf16 LE) + assignments | u32 crc32),
+ * byte-identical to the reference ChunkWriter.append_chunk output; record p gets
+ * chunk_index first_index + p.  qvg_record_bytes = 24 + body bytes (0: bad config).
+ * qvg_unpack_records verifies every record on the device: ok[p] = 1 intact,
+ * 2 CRC mismatch (Q/container.py:297-299), 3 header fields disagree with the
+ * config (the reader's structural check, Q/container.py:258-270). */
+QVG_API size_t qvg_record_bytes(int64_t n_tokens, int32_t head_dim, const qvg_config *cfg);
+QVG_API int qvg_pack_records(const uint8_t *payload, const uint8_t *scales, const uint16_t *centroids,
+                             const uint8_t *assign, int64_t n_planes, int64_t n_tokens, int32_t head_dim,
+                             const qvg_config *cfg, uint32_t first_index, uint8_t *out, void *stream);
+QVG_API int qvg_unpack_records(const uint8_t *records, int64_t n_planes, int64_t n_tokens, int32_t head_dim,
+                               const qvg_config *cfg, uint8_t *payload, uint8_t *scales, uint16_t *centroids,
+                               uint8_t *assign, uint32_t *ok, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -81,6 +81,9 @@ _SIGS = {
                                   ctypes.c_float, _P, _P, _I32, _P, _P, _SZ, _P]),
     "qvg_hadamard": (_I32, [_P, _I32, _I64, _I32, _P, _D, _I32, _P, _I32, _P]),
     "qvg_token_transpose": (_I32, [_P, _I32, _I64, _I64, _I64, _I32, _I32, _P, _P]),
+    "qvg_record_bytes": (_SZ, [_I64, _I32, _CFG]),
+    "qvg_pack_records": (_I32, [_P, _P, _P, _P, _I64, _I64, _I32, _CFG, ctypes.c_uint32, _P, _P]),
+    "qvg_unpack_records": (_I32, [_P, _I64, _I64, _I32, _CFG, _P, _P, _P, _P, _P, _P]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -1,6 +1,7 @@
-"""QVGC container (Q/container.py mirror) on the host: files written by the
-REFERENCE (tests/golden/container_*.npz) parse with our reader and re-write
-byte-identically; torn / corrupt records are isolated as the reference does."""
+"""QVGC container (Q/container.py mirror) host logic without a GPU: the file
+header and the record index scan over files the REFERENCE wrote
+(tests/golden/container_*.npz).  Record bodies (CRC, fields) are verified on
+the device: tests/test_gpu_container.py."""
 import io
 import os
 
@@ -19,40 +20,33 @@ def _ref_file(tag):
 
 
 @pytest.mark.parametrize("tag", ["s2", "s1b4"])
-def test_reference_file_roundtrips_byte_identical(tag):
+def test_reference_file_header_and_index(tag):
     raw, z = _ref_file(tag)
     r = C.ChunkReader(io.BytesIO(raw))
     bits, gs, S, K, seed, n = (int(v) for v in z["cfg"])
     assert (r.header.bits, r.header.group_size, r.header.stages, r.header.centroids, r.header.seed) == \
         (bits, gs, S, K, seed)
     assert r.count == 2
-    out = io.BytesIO()
-    w = C.ChunkWriter(out, r.header)
-    for i in range(r.count):
-        ch = r.read_chunk(i)
-        assert ch.spec.n_tokens == n and len(ch.stages) == S
-        w.append_chunk(ch)
-    assert out.getvalue() == raw
+    rs = r.header.record_size(n)
+    assert [e[0] for e in r._index] == [C.HEADER_SIZE, C.HEADER_SIZE + rs]
+    assert all(e[1] == n and e[2] for e in r._index)
+    assert C.HEADER_SIZE + 2 * rs == len(raw)
 
 
-def test_corrupt_and_torn_records_are_isolated():
+def test_torn_and_mislabelled_records_in_the_index():
     raw, _ = _ref_file("s2")
-    r = C.ChunkReader(io.BytesIO(raw))
-    first = r._entries[0]
-    bad = bytearray(raw)
-    bad[first.offset + C.RECORD_HEADER_SIZE + 3] ^= 0xFF          # body byte of chunk 0
-    r2 = C.ChunkReader(io.BytesIO(bytes(bad)))
+    r3 = C.ChunkReader(io.BytesIO(raw[:-7]))                      # last record cut short
+    assert r3.count == 2 and r3._index[0][2] and not r3._index[1][2]
     with pytest.raises(CorruptChunk):
-        r2.read_chunk(0)
-    r2.read_chunk(1)                                              # neighbour still readable
-    torn = raw[:-7]                                               # last record cut short
-    r3 = C.ChunkReader(io.BytesIO(torn))
-    assert r3.count == 2
-    r3.read_chunk(0)
-    with pytest.raises(CorruptChunk):
-        r3.read_chunk(1)
+        r3._check(1)
     with pytest.raises(OutOfRange):
-        r3.read_chunk(2)
+        r3._check(2)
+    bad = bytearray(raw)
+    bad[C.HEADER_SIZE] = 5                                         # chunk_index of record 0
+    r4 = C.ChunkReader(io.BytesIO(bytes(bad)))
+    assert r4.count == 2 and not r4._index[0][2] and r4._index[1][2]
+    r5 = C.ChunkReader(io.BytesIO(raw[:C.HEADER_SIZE + 9]))       # torn record header
+    assert r5.count == 1 and not r5._index[0][2]
 
 
 def test_header_validation():
