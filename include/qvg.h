@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define QVG_ABI_VERSION 1
+#define QVG_ABI_VERSION 2
 
 #if defined(__GNUC__)
 #define QVG_API __attribute__((visibility("default")))
@@ -193,7 +193,11 @@ QVG_API int qvg_add_back(const double *residual, const uint16_t *centroids, cons
  *   q       [nq][H][d] bf16      k_cur, v_cur [n_cur][H][d] bf16
  *   out     [nq][H][d] bf16
  * With payload == NULL the cache is taken as plain bf16 planes
- * kv_bf16 [2H][n_cache][d] (the bf16 comparator of the same kernel). */
+ * kv_bf16 [2H][n_cache][d] (the bf16 comparator of the same kernel).
+ * status (device int32, may be NULL): OR-ed with QVG_STATUS_NAN_SCALE /
+ * QVG_STATUS_BAD_ASSIGN when the cache holds an E4M3 NaN-pattern scale or an
+ * assignment >= K (that element decodes with centroid 0; read the word after
+ * the stream synchronises, as for qvg_dequantize). */
 QVG_API size_t qvg_attention_workspace_size(int64_t nq, int64_t n_cache, int64_t n_cur, int32_t n_heads,
                                     int32_t head_dim, const qvg_config *cfg /* host */);
 QVG_API int qvg_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scales,
@@ -201,7 +205,7 @@ QVG_API int qvg_attention(const uint16_t *q, const uint8_t *payload, const uint8
                   const uint16_t *k_cur, const uint16_t *v_cur, int64_t nq, int64_t n_cache,
                   int64_t n_cur, int32_t n_heads, int32_t head_dim,
                   const qvg_config *cfg /* host */, float softmax_scale, uint16_t *out,
-                  void *workspace, size_t workspace_bytes, void *stream);
+                  void *workspace, size_t workspace_bytes, int32_t *status, void *stream);
 
 /* qvg_attention with PRE-RoPE cached keys: the
  * cache holds keys before the rotary embedding; after the reconstruction
@@ -216,7 +220,7 @@ QVG_API int qvg_attention_rope(const uint16_t *q, const uint8_t *payload, const 
                                int64_t n_cur, int32_t n_heads, int32_t head_dim, const qvg_config *cfg,
                                float softmax_scale, const float *rope_cos, const float *rope_sin,
                                int32_t rope_mode, uint16_t *out, void *workspace, size_t workspace_bytes,
-                               void *stream);
+                               int32_t *status, void *stream);
 
 /* Baseline competitors (Q/baselines.py), composed with qvg_quantize /
  * qvg_dequantize at S = 0 (= RTN, Q/baselines.py:20-42):

@@ -76,9 +76,9 @@ _SIGS = {
     "qvg_add_back": (_I32, [_P, _P, _P, _I64, _I64, _I32, _I32, _P, _P]),
     "qvg_attention_workspace_size": (_SZ, [_I64, _I64, _I64, _I32, _I32, _CFG]),
     "qvg_attention": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _CFG,
-                             ctypes.c_float, _P, _P, _SZ, _P]),
+                             ctypes.c_float, _P, _P, _SZ, _P, _P]),
     "qvg_attention_rope": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _I64, _I64, _I32, _I32, _CFG,
-                                  ctypes.c_float, _P, _P, _I32, _P, _P, _SZ, _P]),
+                                  ctypes.c_float, _P, _P, _I32, _P, _P, _SZ, _P, _P]),
     "qvg_hadamard": (_I32, [_P, _I32, _I64, _I32, _P, _D, _I32, _P, _I32, _P]),
     "qvg_token_transpose": (_I32, [_P, _I32, _I64, _I64, _I64, _I32, _I32, _P, _P]),
     "qvg_record_bytes": (_SZ, [_I64, _I32, _CFG]),
@@ -108,7 +108,7 @@ def load() -> ctypes.CDLL:
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
-    if lib.qvg_abi_version() != 1:
+    if lib.qvg_abi_version() != 2:
         raise NativeLibraryError("libqvg_b200.so ABI version mismatch")
     _lib = lib
     return lib

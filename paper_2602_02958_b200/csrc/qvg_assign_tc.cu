@@ -19,7 +19,8 @@
 //  3. the epilogue (thread = row = TMEM lane) forms D'[j] = c2[j] - 2 cross'[j]
 //     with the exact float64 c2 and keeps, online, the first argmin j* and
 //     min_{j != j*} (D'[j] - E[j]) with the rigorous error bound
-//     E[j] = 2^-15 ||x_i|| ||c_j|| (Cauchy-Schwarz on sum |x_k c_jk|; covers the
+//     E[j] = 2^-15 ||x_i|| ||c_j|| + 2^-100 (Cauchy-Schwarz on sum |x_k c_jk|, an
+//     absolute floor for underflow of tiny data; covers the
 //     split, the fp32 accumulation and summation, and the reference's own
 //     float64 rounding).  The row is certified when that minimum exceeds
 //     D'[j*] + E[j*]: then the reference's argmin is j* (exact ties are never
@@ -297,7 +298,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_assign_tc(TcArgs a) {
                         }
                     const float cf = j < nb ? __double2float_rn(a.c2[p * K + j0 + j]) : 0.f;
                     c2f[j] = cf;
-                    t2s[j] = __fmul_ru(fabsf(cf), 2.384185791015625e-07f);          // 2^-22
+                    // 2^-22 |c2f| plus an absolute floor of 2^-100: bf16 splits, f32 products
+                    // and c2 -> f32 lose at most ~2^-130 absolutely to underflow, so rows of
+                    // tiny data are never certified and take the exact float64 recheck
+                    t2s[j] = __fadd_ru(__fmul_ru(fabsf(cf), 2.384185791015625e-07f), 7.888609052210118e-31f);
                     t1s[j] = __fmul_ru(float(sqrt(ss) * (1.0 + 1e-6)), 3.0517578125e-05f);   // 2^-15
                 }
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic smem writes -> tensor core

@@ -170,6 +170,7 @@ struct AttnArgs {
     int64_t nq, n_cache, n_cur;
     int H, bits, B, S, K;
     float scale_log2;
+    int32_t *status;        // NaN-pattern scale / assignment >= K flags (may be NULL)
 };
 
 // One token row (128 channels) of plane `pl` of the quantized cache,
@@ -183,7 +184,11 @@ __device__ __forceinline__ void dequant_row(const AttnArgs &a, int64_t pl, int64
     const uint16_t *crow[S > 0 ? S : 1];
 #pragma unroll
     for (int t = 0; t < S; t++) {
-        const int ai = __ldg(a.asg + (pl * S + t) * N + tok);
+        int ai = __ldg(a.asg + (pl * S + t) * N + tok);
+        if (ai >= a.K) {                   // corrupt cache: flag it, decode with centroid 0
+            if (a.status) atomicOr(a.status, int(QVG_STATUS_BAD_ASSIGN));
+            ai = 0;
+        }
         crow[t] = a.cent + ((pl * S + t) * a.K + ai) * kD;
     }
     constexpr uint32_t mask = (1u << BITS) - 1u, sign = 1u << (BITS - 1);
@@ -194,7 +199,9 @@ __device__ __forceinline__ void dequant_row(const AttnArgs &a, int64_t pl, int64
         if constexpr (BITS == 2) w = __ldg(reinterpret_cast<const uint16_t *>(pp) + c);
         else if constexpr (BITS == 4) w = __ldg(reinterpret_cast<const uint32_t *>(pp) + c);
         else { const uint2 v = __ldg(reinterpret_cast<const uint2 *>(pp) + c); w = uint64_t(v.x) | (uint64_t(v.y) << 32); }
-        const float s = e4m3_to_f32(__ldg(sp + (c * 8) / a.B));
+        const uint32_t sb = __ldg(sp + (c * 8) / a.B);
+        if ((sb & 0x7Fu) == 0x7Fu && a.status) atomicOr(a.status, int(QVG_STATUS_NAN_SCALE));
+        const float s = e4m3_to_f32(sb);
         float y[8];
 #pragma unroll
         for (int k = 0; k < 8; k++) {
@@ -1693,7 +1700,7 @@ int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scal
                   const uint16_t *cent, const uint8_t *assign, const uint16_t *kv_bf16,
                   const uint16_t *k_cur, const uint16_t *v_cur, int64_t nq, int64_t n_cache,
                   int64_t n_cur, int H, int d, const qvg_config *cfg, float scale, uint16_t *out,
-                  void *workspace, size_t wbytes, cudaStream_t st, const float *rope_cos,
+                  void *workspace, size_t wbytes, int32_t *status, cudaStream_t st, const float *rope_cos,
                   const float *rope_sin, int rope_mode) {
     using namespace attn;
     if (d != kD) return set_err(QVG_ERR_UNSUPPORTED, "attention kernel supports head_dim 128, got %d", d);
@@ -1709,7 +1716,7 @@ int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scal
         if (cfg->group_size % 8 != 0 || kD % cfg->group_size != 0)
             return set_err(QVG_ERR_UNSUPPORTED, "attention needs group_size | 128 and 8 | group_size");
         AttnArgs ia{q, k_cur, v_cur, nullptr, payload, scales, assign, cent, out, nq, n_cache, n_cur, H,
-                    cfg->bits, cfg->group_size, cfg->stages, cfg->centroids, sl2};
+                    cfg->bits, cfg->group_size, cfg->stages, cfg->centroids, sl2, status};
         int rc = cfg->bits == 2 ? dispatch_s<2>(ia, st) : cfg->bits == 4 ? dispatch_s<4>(ia, st) : dispatch_s<8>(ia, st);
         return rc ? set_err(rc, "attention launch failed: %s", cudaGetErrorString(cudaGetLastError())) : QVG_OK;
     }
@@ -1718,11 +1725,14 @@ int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scal
         const size_t need = attention_workspace_size(nq, n_cache, n_cur, H, d, cfg);
         if (wbytes < need) return set_err(QVG_ERR_WORKSPACE, "attention workspace needs %zu bytes", need);
         uint16_t *rec = static_cast<uint16_t *>(workspace);
-        int32_t *status = reinterpret_cast<int32_t *>(static_cast<uint8_t *>(workspace) + need - 256);
-        cudaMemsetAsync(status, 0, sizeof(int32_t), st);
+        int32_t *stw = status;
+        if (!stw) {                        // no caller word: a scratch one at the end of the workspace
+            stw = reinterpret_cast<int32_t *>(static_cast<uint8_t *>(workspace) + need - 256);
+            cudaMemsetAsync(stw, 0, sizeof(int32_t), st);
+        }
         int rc = launch_dequantize(payload, scales, cent, assign, 2 * int64_t(H), n_cache, d, cfg->bits,
                                    cfg->group_size, cfg->stages, cfg->centroids, rec, QVG_DTYPE_BF16,
-                                   status, st);
+                                   stw, st);
         if (rc) return set_err(rc, "cache reconstruction failed");
         kv = rec;
         if (rope_mode && run_rope_cache(rec, nullptr, H, n_cache, d, rope_cos, rope_sin, rope_mode, st))

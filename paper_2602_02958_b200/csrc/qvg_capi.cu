@@ -439,7 +439,7 @@ int qvg_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scal
                   const uint16_t *centroids, const uint8_t *assign, const uint16_t *kv_bf16,
                   const uint16_t *k_cur, const uint16_t *v_cur, int64_t nq, int64_t n_cache,
                   int64_t n_cur, int32_t H, int32_t d, const qvg_config *cfg, float softmax_scale,
-                  uint16_t *out, void *workspace, size_t workspace_bytes, void *stream) {
+                  uint16_t *out, void *workspace, size_t workspace_bytes, int32_t *status, void *stream) {
     int rc;
     if ((rc = check_config(cfg, false))) return rc;
     if (nq < 0 || n_cache < 0 || n_cur < 0 || H < 1) return set_err(QVG_ERR_BAD_CONFIG, "bad attention sizes");
@@ -448,7 +448,7 @@ int qvg_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scal
     if (n_cache > 0 && d % cfg->group_size != 0)
         return set_err(QVG_ERR_DIMENSION_MISMATCH, "group_size %d does not divide head_dim %d", cfg->group_size, d);
     return run_attention(q, payload, scales, centroids, assign, kv_bf16, k_cur, v_cur, nq, n_cache,
-                         n_cur, H, d, cfg, softmax_scale, out, workspace, workspace_bytes,
+                         n_cur, H, d, cfg, softmax_scale, out, workspace, workspace_bytes, status,
                          static_cast<cudaStream_t>(stream));
 }
 
@@ -457,7 +457,7 @@ int qvg_attention_rope(const uint16_t *q, const uint8_t *payload, const uint8_t 
                        const uint16_t *k_cur, const uint16_t *v_cur, int64_t nq, int64_t n_cache,
                        int64_t n_cur, int32_t H, int32_t d, const qvg_config *cfg, float softmax_scale,
                        const float *rope_cos, const float *rope_sin, int32_t rope_mode, uint16_t *out,
-                       void *workspace, size_t workspace_bytes, void *stream) {
+                       void *workspace, size_t workspace_bytes, int32_t *status, void *stream) {
     int rc;
     if ((rc = check_config(cfg, false))) return rc;
     if (nq < 0 || n_cache < 0 || n_cur < 0 || H < 1) return set_err(QVG_ERR_BAD_CONFIG, "bad attention sizes");
@@ -466,7 +466,7 @@ int qvg_attention_rope(const uint16_t *q, const uint8_t *payload, const uint8_t 
     if (n_cache > 0 && payload && d % cfg->group_size != 0)
         return set_err(QVG_ERR_DIMENSION_MISMATCH, "group_size %d does not divide head_dim %d", cfg->group_size, d);
     return run_attention(q, payload, scales, centroids, assign, kv_bf16, k_cur, v_cur, nq, n_cache,
-                         n_cur, H, d, cfg, softmax_scale, out, workspace, workspace_bytes,
+                         n_cur, H, d, cfg, softmax_scale, out, workspace, workspace_bytes, status,
                          static_cast<cudaStream_t>(stream), rope_cos, rope_sin, rope_mode);
 }
 

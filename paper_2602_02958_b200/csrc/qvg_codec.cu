@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(256) k_quantize_v3(QuantArgs a) {
                     const float hb = (fl + 0.5f) * s;                    // exact
                     const float w = __fmaf_ru(hb, 2.38418579e-7f, E);
                     if (fl < float(QMAX) && av >= __fsub_rd(hb, w) && av <= __fadd_ru(hb, w)) el_amb |= 1u << k;
-                    int q = min(int(rintf(t)), QMAX);
+                    int q = min(int(rintf(fminf(t, float(QMAX + 1)))), QMAX);   // saturated scales: |r/s| >> QMAX
                     if (r[u][k] < 0.f) q = -q;
                     bits |= (uint64_t(uint32_t(q)) & FMASK) << (k * BITS);
                 }
@@ -659,7 +659,7 @@ __global__ void __launch_bounds__(256) k_quantize_v4(QuantArgs a) {
                     const float hb = (fl + 0.5f) * s;                    // exact
                     const float w = __fmaf_ru(hb, 2.38418579e-7f, E);
                     amb |= fl < float(QMAX) && av >= __fsub_rd(hb, w) && av <= __fadd_ru(hb, w);
-                    int q = min(int(rintf(t)), QMAX);
+                    int q = min(int(rintf(fminf(t, float(QMAX + 1)))), QMAX);   // saturated scales: |r/s| >> QMAX
                     if (r[u][k] < 0.f) q = -q;
                     b32[(k * BITS) >> 5] |= (uint32_t(q) & ((1u << BITS) - 1u)) << ((k * BITS) & 31);
                 }

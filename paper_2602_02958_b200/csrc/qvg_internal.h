@@ -88,7 +88,7 @@ int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scal
                   const uint16_t *cent, const uint8_t *assign, const uint16_t *kv_bf16,
                   const uint16_t *k_cur, const uint16_t *v_cur, int64_t nq, int64_t n_cache,
                   int64_t n_cur, int H, int d, const qvg_config *cfg, float scale, uint16_t *out,
-                  void *workspace, size_t wbytes, cudaStream_t st, const float *rope_cos = nullptr,
+                  void *workspace, size_t wbytes, int32_t *status, cudaStream_t st, const float *rope_cos = nullptr,
                   const float *rope_sin = nullptr, int rope_mode = 0);
 
 }  // namespace qvg

@@ -115,7 +115,6 @@ struct PPArgs {
     const uint8_t *a1;       // stage-1 assignments of plane 0; plane p at + p*a1_stride
     int64_t a1_stride;
     int64_t c1_off;          // shared-memory offset (in doubles) of the padded table copy
-    int64_t stg_off;         // >= 0: shared-memory offset (doubles) of the bf16 row staging ring
 };
 
 // rows read as T (double, or float when the plane's float64 rows are all exactly
@@ -252,68 +251,7 @@ __device__ __forceinline__ void kmeanspp_body(const PPArgs &a, const Src src, do
             }
         };
         if constexpr (Src::kBytes == 2) {
-            if (d == 128 && a.stg_off >= 0) {
-                // bf16 rows staged through shared memory: blocks of kRB rows copied with
-                // coalesced 16-byte cp.async (double-buffered, padded pitch), then four
-                // threads per row, thread h holding the numpy accumulators r_2h, r_2h+1
-                // (each an ordered sum over i of t(8i + j)); the tree
-                // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by two xor shuffles
-                constexpr int kRB = 256, kPitch = 136;
-                uint16_t *stg = reinterpret_cast<uint16_t *>(sm + a.stg_off);
-                const uint16_t *xrows;
-                if constexpr (Src::kResid) xrows = src.x;
-                else xrows = reinterpret_cast<const uint16_t *>(src.rows);
-                const int64_t nblk = (N + kRB - 1) / kRB;
-                auto issue = [&](int64_t blk) {
-                    uint16_t *buf = stg + (blk & 1) * kRB * kPitch;
-                    for (int c = tid; c < kRB * 16; c += blockDim.x) {
-                        const int rr = c >> 4, ch = c & 15;
-                        const int64_t row = blk * kRB + rr;
-                        if (row < N)
-                            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(uint32_t(__cvta_generic_to_shared(buf + rr * kPitch + ch * 8))),
-                                         "l"(xrows + row * 128 + ch * 8)
-                                         : "memory");
-                    }
-                    asm volatile("cp.async.commit_group;" ::: "memory");
-                };
-                const int rr = tid >> 2, h = tid & 3;
-                issue(0);
-                for (int64_t blk = 0; blk < nblk; blk++) {
-                    if (blk + 1 < nblk) issue(blk + 1);
-                    else asm volatile("cp.async.commit_group;" ::: "memory");
-                    asm volatile("cp.async.wait_group 1;" ::: "memory");
-                    __syncthreads();
-                    const int64_t i = blk * kRB + rr;
-                    {   // every lane computes (rows past N on unused staging data) so the
-                        // full-warp shuffles below see all lanes; only rows < N are stored
-                        const int64_t ic = i < N ? i : N - 1;
-                        const uint16_t *xr = stg + (blk & 1) * kRB * kPitch + rr * kPitch + 2 * h;
-                        const uint16_t *cr = nullptr;
-                        if constexpr (Src::kResid) cr = src.c1 + int(src.a1[ic]) * src.cp + 2 * h;
-                        double r0 = 0.0, r1 = 0.0;
-#pragma unroll
-                        for (int q = 0; q < 16; q++) {
-                            const uint32_t w = *reinterpret_cast<const uint32_t *>(xr + 8 * q);
-                            double v0 = double(__uint_as_float(w << 16)), v1 = double(__uint_as_float(w & 0xFFFF0000u));
-                            if constexpr (Src::kResid) {
-                                const uint32_t cw = *reinterpret_cast<const uint32_t *>(cr + 8 * q);
-                                v0 = __dsub_rn(v0, double(__uint_as_float(cw << 16)));
-                                v1 = __dsub_rn(v1, double(__uint_as_float(cw & 0xFFFF0000u)));
-                            }
-                            const double t0 = __dsub_rn(v0, xc[8 * q + 2 * h]), t1 = __dsub_rn(v1, xc[8 * q + 2 * h + 1]);
-                            r0 = q == 0 ? __dmul_rn(t0, t0) : __dadd_rn(r0, __dmul_rn(t0, t0));
-                            r1 = q == 0 ? __dmul_rn(t1, t1) : __dadd_rn(r1, __dmul_rn(t1, t1));
-                        }
-                        double sum = __dadd_rn(r0, r1);
-                        sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, 1));
-                        sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, 2));
-                        const double dist = __dadd_rn(0.0, sum);
-                        if (h == 0 && i < N) d2[i] = (pk == 0 || dist < d2[i]) ? dist : d2[i];
-                    }
-                    __syncthreads();                      // buffer blk & 1 is refilled next
-                }
-                asm volatile("cp.async.wait_group 0;" ::: "memory");
-            } else if (d == 128) {
+            if (d == 128) {
             // head_dim 128, bf16 rows: one row per thread, the eight numpy pairwise-8
             // accumulators in registers (r_j = sum over i of t(8i + j), i = 0..15, in
             // order, then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))); 16-byte loads
@@ -1012,7 +950,7 @@ static void assign_step(const KMeansBuffers &b, int64_t P, int64_t N, int d, int
 int run_kmeanspp(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, const double *draws,
                  int64_t draws_stride, cudaStream_t st) {
     PPArgs pa{b.rows, b.rows32_valid ? b.rows32 : nullptr, b.src16, b.rows32_ok, draws, draws_stride, b.cent, b.d2, b.pk_off, b.pk_len, b.pk_leaves, N, d, K,
-              b.pk_l, b.pk_r, b.pk_hstart, b.pk_heights, 0, nullptr, nullptr, 0, nullptr, 0, 0, -1};
+              b.pk_l, b.pk_r, b.pk_hstart, b.pk_heights, 0, nullptr, nullptr, 0, nullptr, 0, 0};
     size_t smem = sizeof(double) * (128 + 2 * b.pk_leaves - 1 + K);
     // the pick weights in shared memory while two 1024-thread CTAs still fit per SM
     if (smem + sizeof(double) * N <= 100 * 1024) {
@@ -1032,16 +970,6 @@ int run_kmeanspp(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, con
         pa.a1_stride = b.res_a1_stride;
         pa.c1_off = int64_t(smem / sizeof(double));
         smem += tab;
-    }
-    // bf16 sources (stage 1 / the stage-2 rebuild): a double-buffered shared staging
-    // ring of 2 x 256 rows (padded pitch 136) when it fits -- opt-in (QVG_KPP_STAGE=1):
-    // 2% faster, and an intermittent stall was observed with it enabled
-    static const bool stage_ok = [] { const char *e = getenv("QVG_KPP_STAGE"); return e && atoi(e) == 1; }();
-    const size_t ring = size_t(2) * 256 * 136 * 2;
-    if (stage_ok && d == 128 && (b.src16 || pa.x16) && ((smem + 15) & ~size_t(15)) + ring <= 220 * 1024) {
-        smem = (smem + 15) & ~size_t(15);
-        pa.stg_off = int64_t(smem / sizeof(double));
-        smem += ring;
     }
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(k_kmeanspp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -285,7 +285,7 @@ __device__ __noinline__ Words4 fix_codes(const uint8_t *xrow, const float *tab, 
         uint32_t qv;
         if (E == 0.f) {
             const float av = fabsf(r[k]);
-            int nq = int(rintf(av * inv));
+            int nq = int(rintf(fminf(av * inv, float(QMAX + 1))));   // saturated scale: |r/s| >> QMAX
             const float up = (float(nq) + 0.5f) * sv, dn = (float(nq) - 0.5f) * sv;
             if (av > up || (av == up && (nq & 1))) nq++;
             else if (nq > 0 && (av < dn || (av == dn && (nq & 1)))) nq--;

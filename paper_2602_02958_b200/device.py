@@ -165,6 +165,10 @@ def compress(x: torch.Tensor, config: QuantConfig, chunk_index: Union[int, Seque
     out = _alloc_chunks(config, P, N, d, dev, keep_f64 or warm_init is not None, True)
     if S > 0 and warm_init is None and draws is None:
         draws = pp_draws(config, chunk_index, P, dev)
+    elif draws is not None:
+        draws = draws.to(torch.float64).contiguous()
+        if tuple(draws.shape) != (P, S, K):
+            raise ValueError("draws must be [P, S, K] float64")
     if warm_init is not None:
         warm_init = warm_init.to(torch.float64).contiguous()
         if tuple(warm_init.shape) != (P, S, K, d):
@@ -377,7 +381,7 @@ def attention(q: torch.Tensor, cache: Optional[DeviceChunks], k_cur: torch.Tenso
               v_cur: torch.Tensor, softmax_scale: Optional[float] = None,
               kv_bf16: Optional[torch.Tensor] = None,
               out: Optional[torch.Tensor] = None, fused: bool = False,
-              workspace: Optional[torch.Tensor] = None, rope=None) -> torch.Tensor:
+              workspace: Optional[torch.Tensor] = None, rope=None, check: bool = True) -> torch.Tensor:
     """O = softmax(q [Khat; k_cur]^T * scale) [Vhat; v_cur] per head.
 
     q [Nq, H, d] bf16; cache: 2H planes (plane 2h = K of head h, 2h+1 = V)
@@ -388,15 +392,31 @@ def attention(q: torch.Tensor, cache: Optional[DeviceChunks], k_cur: torch.Tenso
     rope=(cos, sin, "rotate_half"|"interleaved") marks the cached keys as
     pre-RoPE: the reconstructed keys are rotated with cos/sin [n_cache, d/2]
     (float32, CUDA) before the attention; q and k_cur are post-RoPE.
+    check: synchronise and raise NaNPattern / DimensionMismatch when the
+    cache holds an E4M3 NaN-pattern scale or an assignment >= K (the codec
+    status word, as dequantize does); check=False leaves the launch async.
     """
     _require_cuda(q, k_cur, v_cur, kv_bf16, out)
+    for name, t in (("q", q), ("k_cur", k_cur), ("v_cur", v_cur), ("kv_bf16", kv_bf16), ("out", out)):
+        if t is not None and t.dtype != torch.bfloat16:
+            raise ValueError(f"{name} must be bfloat16, got {t.dtype}")
+    if q.dim() != 3:
+        raise ValueError("q must be [Nq, H, d]")
     nq, H, d = q.shape
+    if k_cur.dim() != 3 or tuple(k_cur.shape[1:]) != (H, d) or tuple(v_cur.shape) != tuple(k_cur.shape):
+        raise ValueError("k_cur / v_cur must be [Ncur, H, d] matching q")
+    if out is not None and tuple(out.shape) != (nq, H, d):
+        raise ValueError("out must be [Nq, H, d]")
     ncur = k_cur.shape[0]
     if cache is not None:
         if cache.n_planes != 2 * H:
             raise ValueError("cache must hold 2*H planes (K, V per head)")
+        if cache.head_dim != d:
+            raise ValueError(f"cache head_dim {cache.head_dim} != q head_dim {d}")
         nc, cfg = cache.n_tokens, cache.config
     elif kv_bf16 is not None:
+        if kv_bf16.dim() != 3 or kv_bf16.shape[0] != 2 * H or kv_bf16.shape[2] != d:
+            raise ValueError("kv_bf16 must be [2H, Nc, d]")
         nc, cfg = kv_bf16.shape[1], QuantConfig(stages=0)
     else:
         nc, cfg = 0, QuantConfig(stages=0)
@@ -413,12 +433,15 @@ def attention(q: torch.Tensor, cache: Optional[DeviceChunks], k_cur: torch.Tenso
             torch.empty(max(n, 1), dtype=torch.uint8, device=q.device)
         nbytes = ws.numel()
     c = cache
+    st = torch.zeros(1, dtype=torch.int32, device=q.device) if c is not None else None
     if rope is None:
         _lib.check(lib.qvg_attention(
             _ptr(q), _ptr(c.payload if c else None), _ptr(c.scales if c else None),
             _ptr(c.centroids if c else None), _ptr(c.assignments if c else None), _ptr(kv_bf16),
             _ptr(k_cur), _ptr(v_cur), nq, nc, ncur, H, d, cp, scale, _ptr(out), _ptr(ws), nbytes,
-            _stream(q.device)))
+            _ptr(st), _stream(q.device)))
+        if check and st is not None:
+            check_status(st)
         return out
     cos_t, sin_t, mode = rope
     _require_cuda(cos_t, sin_t)
@@ -429,7 +452,9 @@ def attention(q: torch.Tensor, cache: Optional[DeviceChunks], k_cur: torch.Tenso
         _ptr(q), _ptr(c.payload if c else None), _ptr(c.scales if c else None),
         _ptr(c.centroids if c else None), _ptr(c.assignments if c else None), _ptr(kv_bf16),
         _ptr(k_cur), _ptr(v_cur), nq, nc, ncur, H, d, cp, scale, _ptr(cos_t), _ptr(sin_t),
-        {"rotate_half": 1, "interleaved": 2}[mode], _ptr(out), _ptr(ws), nbytes, _stream(q.device)))
+        {"rotate_half": 1, "interleaved": 2}[mode], _ptr(out), _ptr(ws), nbytes, _ptr(st), _stream(q.device)))
+    if check and st is not None:
+        check_status(st)
     return out
 
 

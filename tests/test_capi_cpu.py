@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared_symbols():
         assert hasattr(lib, name), name
     assert set(declared_symbols()) == set(_lib.EXPORTED)
-    assert lib.qvg_abi_version() == 1
+    assert lib.qvg_abi_version() == 2
 
 
 def _cfg(**kw):

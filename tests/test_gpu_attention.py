@@ -174,3 +174,42 @@ def test_pre_rope_cached_keys_vs_oracle(oracle_lib, mode, quant):
     ref = oracle_lib.attention(q.float().cpu().numpy(), kr, vcache, kc.float().cpu().numpy(),
                                vc.float().cpu().numpy(), d ** -0.5, 8)
     _check(out, ref)
+
+
+@pytest.mark.parametrize("fused", [False, True])
+def test_attention_reports_corrupt_cache(fused):
+    """a NaN-pattern scale or an assignment >= K in the cache is
+    reported (NaNPattern / DimensionMismatch) like dequantize does, and the
+    corrupt assignment decodes with centroid 0 instead of reading past the
+    centroid table."""
+    from paper_2602_02958_b200.qvgcodec.errors import DimensionMismatch, NaNPattern
+
+    H, nc, nq, d = 1, 256, 64, 128
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = (torch.randn((2 * H, nc, d), generator=g, device="cuda") * 2).to(torch.bfloat16)
+    cfg = QuantConfig(bits=2, group_size=64, stages=1, centroids=8)
+    chunks = D.compress(x, cfg, chunk_index=0)
+    q, kc, vc = (torch.randn((nq, H, d), generator=g, device="cuda").to(torch.bfloat16) for _ in range(3))
+    D.attention(q, chunks, kc, vc, fused=fused)                       # clean cache: no error
+    bad = D.DeviceChunks(cfg, nc, d, chunks.payload, chunks.scales, chunks.centroids,
+                         chunks.assignments.clone())
+    bad.assignments[0, 0, 5] = 200
+    with pytest.raises(DimensionMismatch):
+        D.attention(q, bad, kc, vc, fused=fused)
+    bad2 = D.DeviceChunks(cfg, nc, d, chunks.payload, chunks.scales.clone(), chunks.centroids,
+                          chunks.assignments)
+    bad2.scales[1, 7] = 0x7F
+    with pytest.raises(NaNPattern):
+        D.attention(q, bad2, kc, vc, fused=fused)
+
+
+def test_attention_validates_inputs():
+    H, nc, nq, d = 2, 128, 32, 128
+    kv = torch.zeros((2 * H, nc, d), dtype=torch.bfloat16, device="cuda")
+    q = torch.zeros((nq, H, d), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(ValueError):
+        D.attention(q.float(), None, q, q, kv_bf16=kv)                 # fp32 q
+    with pytest.raises(ValueError):
+        D.attention(q, None, q[:, :1], q[:, :1], kv_bf16=kv)            # k_cur heads != q heads
+    with pytest.raises(ValueError):
+        D.attention(q, None, q, q, kv_bf16=kv[:, :, :64])                # head_dim mismatch

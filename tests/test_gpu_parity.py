@@ -294,6 +294,28 @@ def test_compress_longcat_k256_vs_oracle(oracle_lib):
     assert np.array_equal(dc.payload.cpu().numpy(), pay)
 
 
+@pytest.mark.parametrize("scale_exp", [-112, -60, 90])
+def test_compress_tiny_and_huge_scale_planes_vs_oracle(oracle_lib, scale_exp):
+    """planes scaled far from 1 (bf16 near its underflow / large
+    range): the tensor-core filter must not certify rows whose split products
+    underflow -- assignments, centroids and codes stay bit-exact."""
+    from paper_2602_02958_b200.synth import kv_cache_planes
+
+    cfg = QuantConfig(bits=2, group_size=64, stages=2, centroids=16)
+    x = (kv_cache_planes(1, 1, 1024, 128, seed=21, device="cuda").float() * 2.0 ** scale_exp).to(torch.bfloat16)
+    P = x.shape[0]
+    dc = D.compress(x, cfg, chunk_index=0)
+    draws = np.stack([oracle_lib.pp_draws(0, 0, 2, 16)] * P)
+    pay, sc, cent, asg, iters = oracle_lib.prq_compress_batch(x.float().cpu().numpy(), 2, 64, 2, 16, 10, 1e-4,
+                                                              draws, 4)
+    assert np.array_equal(dc.assignments.cpu().numpy(), asg)
+    assert np.array_equal(dc.payload.cpu().numpy(), pay)
+    assert np.array_equal(dc.scales.cpu().numpy(), sc)
+    ref = oracle_lib.prq_decompress_batch(pay, sc, cent, asg, 1024, 128, 2, 64, 4)
+    out = D.dequantize(dc, torch.float32).cpu().numpy()
+    assert np.array_equal(out.view(np.uint32), ref.view(np.uint32))
+
+
 @pytest.mark.parametrize("bits,B,S", [(2, 64, 2), (2, 16, 1), (4, 32, 3), (8, 64, 2), (2, 128, 4)])
 def test_many_planes_bf16_certificate_stress(oracle_lib, bits, B, S):
     """>= 148 bf16 planes select the certified persistent quantize (v5w):
