@@ -483,196 +483,7 @@ struct Bars {
     uint32_t tmem;
 };
 
-__global__ void __launch_bounds__(192, 1)
-k_attention_tma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
-                const __grid_constant__ CUtensorMap tmKc, const __grid_constant__ CUtensorMap tmVc, Args a) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *sQ = smem;
-    uint8_t *sKV = smem + kOpTile;                  // stage s: K at +s*2*kOpTile, V at +kOpTile
-    uint8_t *sP = smem + kOpTile + 4 * kOpTile;
-    __shared__ Bars bars;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int h = blockIdx.y;
-    const int64_t q0 = int64_t(blockIdx.x) * kTile;
-    const int64_t cb = (a.n_cache + kTile - 1) / kTile;
-    const int64_t nb = cb + (a.n_cur + kTile - 1) / kTile;
-
-    if (tid == 0) {
-        attn::bar_init(&bars.q_full, 1);
-        for (int i = 0; i < 2; i++) {
-            attn::bar_init(&bars.kv_full[i], 1);
-            attn::bar_init(&bars.kv_empty[i], 1);
-            attn::bar_init(&bars.s_full[i], 1);
-            attn::bar_init(&bars.s_free[i], 128);
-        }
-        attn::bar_init(&bars.p_full, 128);
-        attn::bar_init(&bars.o_done, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 5) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(attn::su32(&bars.tmem)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    attn::fence_before();
-    __syncthreads();
-    attn::fence_after();
-    const uint32_t tmem = bars.tmem;
-
-    if (warp == 4) {
-        // ---------------- TMA producer ----------------
-        if (lane == 0) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
-            expect_tx(&bars.q_full, kOpTile);
-            tma_load_2d(sQ, &tmQ, h * kD, int(q0), &bars.q_full);
-            tma_load_2d(sQ + kBox, &tmQ, h * kD + 64, int(q0), &bars.q_full);
-            for (int64_t j = 0; j < nb; j++) {
-                const int st = int(j & 1);
-                if (j >= 2) attn::bar_wait(&bars.kv_empty[st], uint32_t(((j - 2) >> 1) & 1));
-                uint8_t *sK = sKV + st * 2 * kOpTile, *sV = sK + kOpTile;
-                expect_tx(&bars.kv_full[st], 2 * kOpTile);
-                if (j < cb) {
-                    const int yk = int(2 * h * a.n_cache + j * kTile), yv = int((2 * h + 1) * a.n_cache + j * kTile);
-                    tma_load_2d(sK, &tmKV, 0, yk, &bars.kv_full[st]);
-                    tma_load_2d(sK + kBox, &tmKV, 64, yk, &bars.kv_full[st]);
-                    tma_load_2d(sV, &tmKV, 0, yv, &bars.kv_full[st]);
-                    tma_load_2d(sV + kBox, &tmKV, 64, yv, &bars.kv_full[st]);
-                } else {
-                    const int y = int((j - cb) * kTile);
-                    tma_load_2d(sK, &tmKc, h * kD, y, &bars.kv_full[st]);
-                    tma_load_2d(sK + kBox, &tmKc, h * kD + 64, y, &bars.kv_full[st]);
-                    tma_load_2d(sV, &tmVc, h * kD, y, &bars.kv_full[st]);
-                    tma_load_2d(sV + kBox, &tmVc, h * kD + 64, y, &bars.kv_full[st]);
-                }
-            }
-        }
-    } else if (warp == 5) {
-        // ---------------- MMA issuer ----------------
-        if (lane == 0) {
-            constexpr uint32_t idK = attn::umma_idesc(false), idV = attn::umma_idesc(true);
-            const uint32_t sq = attn::su32(sQ);
-            const uint64_t dP = attn::umma_desc(attn::su32(sP), attn::kLbo, attn::kSbo);
-            attn::bar_wait(&bars.q_full, 0);
-            auto issue_s = [&](int64_t j) {
-                const int st = int(j & 1), sb = int(j & 1);
-                const uint32_t sk = attn::su32(sKV + st * 2 * kOpTile);
-                attn::bar_wait(&bars.kv_full[st], uint32_t((j >> 1) & 1));
-                if (j >= 2) attn::bar_wait(&bars.s_free[sb], uint32_t(((j - 2) >> 1) & 1));
-                attn::fence_after();
-#pragma unroll
-                for (int k = 0; k < kD / 16; k++) {
-                    const uint32_t off = (k >> 2) * kBox + (k & 3) * 32;   // K-major SW128, 16-element step
-                    attn::mma_f16(tmem + sb * 128, desc_sw128(sq + off, 16, 1024), desc_sw128(sk + off, 16, 1024),
-                                  idK, k > 0);
-                }
-                attn::mma_commit(&bars.s_full[sb]);
-            };
-            auto issue_pv = [&](int64_t j) {
-                const int st = int(j & 1);
-                const uint32_t sv = attn::su32(sKV + st * 2 * kOpTile + kOpTile);
-                attn::bar_wait(&bars.p_full, uint32_t(j & 1));
-                attn::fence_after();
-#pragma unroll
-                for (int k = 0; k < kTile / 16; k++)
-                    attn::mma_f16(tmem + 256, dP + uint64_t((k * 2 * attn::kLbo) >> 4),
-                                  desc_sw128(sv + k * 2048, kBox, 1024), idV, (j > 0 || k > 0) ? 1u : 0u);
-                attn::mma_commit(&bars.o_done);
-                attn::mma_commit(&bars.kv_empty[st]);
-            };
-            for (int64_t j = 0; j < nb; j++) {
-                issue_s(j);
-                if (j >= 1) issue_pv(j - 1);
-            }
-            if (nb > 0) issue_pv(nb - 1);
-        }
-    } else {
-        // ---------------- softmax warps (rows) ----------------
-        const uint32_t t_lane = uint32_t(warp * 32) << 16;
-        float m_run = -INFINITY, l_run = 0.f;
-        for (int64_t j = 0; j < nb; j++) {
-            const int sb = int(j & 1);
-            const int64_t cnt = j < cb ? a.n_cache - j * kTile : a.n_cur - (j - cb) * kTile;
-            const int nvalid = int(cnt < kTile ? cnt : kTile);
-            const uint32_t tS = tmem + sb * 128 + t_lane;
-            attn::bar_wait(&bars.s_full[sb], uint32_t((j >> 1) & 1));
-            attn::fence_after();
-            float mx = -INFINITY;
-#pragma unroll
-            for (int ch = 0; ch < 4; ch++) {
-                float sv[32];
-                attn::tmem_ld32(tS + ch * 32, sv);
-#pragma unroll
-                for (int i = 0; i < 32; i++)
-                    if (ch * 32 + i < nvalid) mx = fmaxf(mx, sv[i]);
-            }
-            mx *= a.scale_log2;
-            const bool grow = mx > m_run + 8.f;       // lazy rescale (FA4): only when the max grows by > 2^8
-            const float m_new = grow ? mx : m_run;
-            const float alpha = grow ? ex2(m_run - m_new) : 1.f;
-            uint32_t pk[64];
-            float lsum = 0.f;
-#pragma unroll
-            for (int ch = 0; ch < 4; ch++) {
-                float sv[32];
-                attn::tmem_ld32(tS + ch * 32, sv);
-#pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    const float p0 = ch * 32 + i < nvalid ? ex2(fmaf(sv[i], a.scale_log2, -m_new)) : 0.f;
-                    const float p1 = ch * 32 + i + 1 < nvalid ? ex2(fmaf(sv[i + 1], a.scale_log2, -m_new)) : 0.f;
-                    lsum += p0 + p1;
-                    pk[ch * 16 + (i >> 1)] = attn::pack_bf16(p0, p1);
-                }
-            }
-            attn::fence_before();
-            arrive(&bars.s_free[sb]);                 // S buffer may be overwritten by S_{j+2}
-            if (j > 0) {
-                attn::bar_wait(&bars.o_done, uint32_t((j - 1) & 1));   // PV_{j-1} done: P and O free
-                attn::fence_after();
-                if (__any_sync(0xffffffffu, grow)) {
-#pragma unroll
-                    for (int ch = 0; ch < 4; ch++) {
-                        float ov[32];
-                        attn::tmem_ld32(tmem + 256 + t_lane + ch * 32, ov);
-#pragma unroll
-                        for (int i = 0; i < 32; i++) ov[i] *= alpha;
-                        attn::tmem_st32(tmem + 256 + t_lane + ch * 32, ov);
-                    }
-                }
-            }
-            l_run = l_run * alpha + lsum;
-            m_run = m_new;
-#pragma unroll
-            for (int c = 0; c < 16; c++)
-                *reinterpret_cast<uint4 *>(sP + attn::kmaj_off(tid, c)) =
-                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-            attn::fence_proxy_async();
-            attn::fence_before();
-            arrive(&bars.p_full);
-        }
-        // ---------------- epilogue ----------------
-        if (nb > 0) attn::bar_wait(&bars.o_done, uint32_t((nb - 1) & 1));
-        attn::fence_after();
-        const float inv_l = 1.f / l_run;
-        const int64_t qi = q0 + tid;
-#pragma unroll
-        for (int ch = 0; ch < 4; ch++) {
-            float ov[32];
-            attn::tmem_ld32(tmem + 256 + t_lane + ch * 32, ov);
-            if (qi < a.nq) {
-                uint4 *dst = reinterpret_cast<uint4 *>(a.out + (qi * a.H + h) * kD + ch * 32);
-#pragma unroll
-                for (int c = 0; c < 4; c++)
-                    dst[c] = make_uint4(attn::pack_bf16(ov[8 * c] * inv_l, ov[8 * c + 1] * inv_l),
-                                        attn::pack_bf16(ov[8 * c + 2] * inv_l, ov[8 * c + 3] * inv_l),
-                                        attn::pack_bf16(ov[8 * c + 4] * inv_l, ov[8 * c + 5] * inv_l),
-                                        attn::pack_bf16(ov[8 * c + 6] * inv_l, ov[8 * c + 7] * inv_l));
-            }
-        }
-    }
-    attn::fence_before();
-    __syncthreads();
-    if (warp == 5) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
+// (the v2 single-tile kernel is gone; these helpers serve the pp4 / in-tile kernels)
 
 // ---- host: tensor maps via the driver entry point (no -lcuda needed) -------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -705,40 +516,12 @@ static bool make_map(CUtensorMap *m, const void *base, uint64_t rows, uint64_t c
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const uint16_t *vc, int64_t nq,
-               int64_t nc, int64_t ncur, int H, float scale_log2, uint16_t *out, cudaStream_t st) {
-    CUtensorMap mQ, mKV, mKc, mVc;
-    // Q, k_cur, v_cur: [n][H*128]; cache: [2H*n_cache][128].  Empty operands get a
-    // 1-row dummy map over q (never loaded).
-    const bool okq = make_map(&mQ, q, uint64_t(nq), uint64_t(H) * kD, uint64_t(H) * kD);
-    const bool okkv = nc > 0 ? make_map(&mKV, kv, uint64_t(2 * H) * nc, kD, kD) : make_map(&mKV, q, 1, kD, kD);
-    const bool okk = ncur > 0 ? make_map(&mKc, kc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
-                              : make_map(&mKc, q, 1, kD, kD);
-    const bool okv = ncur > 0 ? make_map(&mVc, vc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
-                              : make_map(&mVc, q, 1, kD, kD);
-    if (!(okq && okkv && okk && okv)) return set_err(QVG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    const size_t smem = kSmem + 1024;
-    cudaFuncSetAttribute(k_attention_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    dim3 grid(unsigned((nq + kTile - 1) / kTile), unsigned(H));
-    Args a{nq, nc, ncur, H, scale_log2, out};
-    k_attention_tma<<<grid, 192, smem, st>>>(mQ, mKV, mKc, mVc, a);
-    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
-}
 }  // namespace attn2
 
+
 // ============================================================================
-// v3 (FA4-style ping-pong): one CTA = 2 query tiles (256 rows) of one head.
-//   warps 0-3 / 4-7  softmax of tile A / tile B (thread = TMEM lane = row)
-//   warp  8          TMA producer (Q_A, Q_B once; K/V 2-stage ring)
-//   warp  9          TMEM allocator + MMA issuer
-// TMEM (512 cols): S_A [0,128), S_B [128,256), O_A [256,384), O_B [384,512).
-// P (bf16 pairs) is written back over the first 64 columns of its S tile and
-// consumed as the TMEM A operand of O += P V.  MMAs issue in the order
-//   S_A(j) S_B(j) PV_A(j) PV_B(j) S_A(j+1) ...
-// so the tensor core computes S_B while softmax A runs and PV_A/S_A(j+1)
-// while softmax B runs; because tcgen05 MMAs complete in issue order, the
-// arrival of S_X(j) also certifies PV_X(j-1) done, which is what makes the
-// in-place O rescale and the P aliasing safe without extra barriers.
+// helpers shared by the two-tile (ping-pong) kernel below: TMEM-A MMA, TMEM
+// stores of P, the barrier set
 // ============================================================================
 namespace attn3 {
 using attn::kTile;
@@ -771,211 +554,6 @@ struct Bars {
     uint32_t tmem;
 };
 
-__global__ void __launch_bounds__(320, 1)
-k_attention_pp(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
-               const __grid_constant__ CUtensorMap tmKc, const __grid_constant__ CUtensorMap tmVc, attn2::Args a) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *sQ = smem;                              // tile A at +0, tile B at +kOpTile
-    uint8_t *sKV = smem + 2 * kOpTile;               // stage s: K at +s*2*kOpTile, V at +kOpTile
-    __shared__ Bars bars;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int h = blockIdx.y;
-    const int64_t q0 = int64_t(blockIdx.x) * 2 * kTile;
-    const int64_t cb = (a.n_cache + kTile - 1) / kTile;
-    const int64_t nb = cb + (a.n_cur + kTile - 1) / kTile;
-
-    if (tid == 0) {
-        attn::bar_init(&bars.q_full, 1);
-        for (int i = 0; i < 2; i++) {
-            attn::bar_init(&bars.kv_full[i], 1);
-            attn::bar_init(&bars.kv_empty[i], 1);
-            attn::bar_init(&bars.s_full[i], 1);
-            attn::bar_init(&bars.p_full[i], 128);
-        }
-        attn::bar_init(&bars.o_final, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 9) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(attn::su32(&bars.tmem)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    attn::fence_before();
-    __syncthreads();
-    attn::fence_after();
-    const uint32_t tmem = bars.tmem;
-
-    if (warp == 8) {
-        if (lane == 0) {                              // ---- TMA producer
-            attn2::expect_tx(&bars.q_full, 2 * kOpTile);
-            for (int t = 0; t < 2; t++) {
-                attn2::tma_load_2d(sQ + t * kOpTile, &tmQ, h * kD, int(q0 + t * kTile), &bars.q_full);
-                attn2::tma_load_2d(sQ + t * kOpTile + kBox, &tmQ, h * kD + 64, int(q0 + t * kTile), &bars.q_full);
-            }
-            for (int64_t j = 0; j < nb; j++) {
-                const int st = int(j & 1);
-                if (j >= 2) attn::bar_wait(&bars.kv_empty[st], uint32_t(((j - 2) >> 1) & 1));
-                uint8_t *sK = sKV + st * 2 * kOpTile, *sV = sK + kOpTile;
-                attn2::expect_tx(&bars.kv_full[st], 2 * kOpTile);
-                if (j < cb) {
-                    const int yk = int(2 * h * a.n_cache + j * kTile), yv = int((2 * h + 1) * a.n_cache + j * kTile);
-                    attn2::tma_load_2d(sK, &tmKV, 0, yk, &bars.kv_full[st]);
-                    attn2::tma_load_2d(sK + kBox, &tmKV, 64, yk, &bars.kv_full[st]);
-                    attn2::tma_load_2d(sV, &tmKV, 0, yv, &bars.kv_full[st]);
-                    attn2::tma_load_2d(sV + kBox, &tmKV, 64, yv, &bars.kv_full[st]);
-                } else {
-                    const int y = int((j - cb) * kTile);
-                    attn2::tma_load_2d(sK, &tmKc, h * kD, y, &bars.kv_full[st]);
-                    attn2::tma_load_2d(sK + kBox, &tmKc, h * kD + 64, y, &bars.kv_full[st]);
-                    attn2::tma_load_2d(sV, &tmVc, h * kD, y, &bars.kv_full[st]);
-                    attn2::tma_load_2d(sV + kBox, &tmVc, h * kD + 64, y, &bars.kv_full[st]);
-                }
-            }
-        }
-    } else if (warp == 9) {
-        if (lane == 0) {                              // ---- MMA issuer
-            constexpr uint32_t idK = attn::umma_idesc(false), idV = attn::umma_idesc(true);
-            attn::bar_wait(&bars.q_full, 0);
-            for (int64_t j = 0; j < nb; j++) {
-                const int st = int(j & 1);
-                const uint32_t sk = attn::su32(sKV + st * 2 * kOpTile), sv = sk + kOpTile;
-                attn::bar_wait(&bars.kv_full[st], uint32_t((j >> 1) & 1));
-                attn::fence_after();
-                for (int t = 0; t < 2; t++) {         // S_t = Q_t K_j^T
-                    const uint32_t sq = attn::su32(sQ + t * kOpTile);
-#pragma unroll
-                    for (int k = 0; k < kD / 16; k++) {
-                        const uint32_t off = (k >> 2) * kBox + (k & 3) * 32;
-                        attn::mma_f16(tmem + t * 128, attn2::desc_sw128(sq + off, 16, 1024),
-                                      attn2::desc_sw128(sk + off, 16, 1024), idK, k > 0);
-                    }
-                    attn::mma_commit(&bars.s_full[t]);
-                }
-                for (int t = 0; t < 2; t++) {         // O_t += P_t V_j  (P in TMEM over S_t)
-                    attn::bar_wait(&bars.p_full[t], uint32_t(j & 1));
-                    attn::fence_after();
-#pragma unroll
-                    for (int k = 0; k < kTile / 16; k++)
-                        mma_f16_tmem_a(tmem + 256 + t * 128, tmem + t * 128 + k * 8,
-                                       attn2::desc_sw128(sv + k * 2048, kBox, 1024), idV, (j > 0 || k > 0) ? 1u : 0u);
-                }
-                attn::mma_commit(&bars.kv_empty[st]);
-            }
-            attn::mma_commit(&bars.o_final);
-        }
-    } else {
-        // ---- softmax (tile t = warp / 4) ----
-        const int t = warp >> 2;
-        const uint32_t t_lane = uint32_t((warp & 3) * 32) << 16;
-        const uint32_t tS = tmem + t * 128 + t_lane, tO = tmem + 256 + t * 128 + t_lane;
-        float m_run = -INFINITY, l_run = 0.f;
-        for (int64_t j = 0; j < nb; j++) {
-            const int64_t cnt = j < cb ? a.n_cache - j * kTile : a.n_cur - (j - cb) * kTile;
-            const int nvalid = int(cnt < kTile ? cnt : kTile);
-            attn::bar_wait(&bars.s_full[t], uint32_t(j & 1));
-            attn::fence_after();
-            float mx = -INFINITY;
-#pragma unroll
-            for (int ch = 0; ch < 4; ch++) {
-                float sv[32];
-                attn::tmem_ld32(tS + ch * 32, sv);
-                if (nvalid == kTile) {
-#pragma unroll
-                    for (int i = 0; i < 32; i++) mx = fmaxf(mx, sv[i]);
-                } else {
-#pragma unroll
-                    for (int i = 0; i < 32; i++)
-                        if (ch * 32 + i < nvalid) mx = fmaxf(mx, sv[i]);
-                }
-            }
-            mx *= a.scale_log2;
-            const bool grow = mx > m_run + 8.f;      // lazy rescale: only when the max grows by > 2^8
-            const float m_new = grow ? mx : m_run;
-            const float alpha = grow ? attn2::ex2(m_run - m_new) : 1.f;
-            // S_t(j) arrived => PV_t(j-1) (issued earlier) has completed: O_t is quiescent
-            if (j > 0 && __any_sync(0xffffffffu, grow)) {
-#pragma unroll
-                for (int ch = 0; ch < 4; ch++) {
-                    float ov[32];
-                    attn::tmem_ld32(tO + ch * 32, ov);
-#pragma unroll
-                    for (int i = 0; i < 32; i++) ov[i] *= alpha;
-                    attn::tmem_st32(tO + ch * 32, ov);
-                }
-            }
-            float lsum = 0.f;
-#pragma unroll
-            for (int half = 0; half < 2; half++) {
-                uint32_t pk[32];
-#pragma unroll
-                for (int cc = 0; cc < 2; cc++) {
-                    const int ch = half * 2 + cc;
-                    float sv[32];
-                    attn::tmem_ld32(tS + ch * 32, sv);
-#pragma unroll
-                    for (int i = 0; i < 32; i += 2) {
-                        float p0 = attn2::ex2(fmaf(sv[i], a.scale_log2, -m_new));
-                        float p1 = attn2::ex2(fmaf(sv[i + 1], a.scale_log2, -m_new));
-                        if (nvalid != kTile) {
-                            p0 = ch * 32 + i < nvalid ? p0 : 0.f;
-                            p1 = ch * 32 + i + 1 < nvalid ? p1 : 0.f;
-                        }
-                        lsum += p0 + p1;
-                        pk[cc * 16 + (i >> 1)] = attn::pack_bf16(p0, p1);
-                    }
-                }
-                // P columns [32*half, 32*half+32) overwrite S columns already consumed
-                tmem_st32u(tS + half * 32, pk);
-            }
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            l_run = l_run * alpha + lsum;
-            m_run = m_new;
-            attn::fence_before();
-            attn2::arrive(&bars.p_full[t]);
-        }
-        // ---- epilogue ----
-        attn::bar_wait(&bars.o_final, 0);
-        attn::fence_after();
-        const float inv_l = 1.f / l_run;
-        const int64_t qi = q0 + t * kTile + (tid & 127);
-#pragma unroll
-        for (int ch = 0; ch < 4; ch++) {
-            float ov[32];
-            attn::tmem_ld32(tO + ch * 32, ov);
-            if (qi < a.nq) {
-                uint4 *dst = reinterpret_cast<uint4 *>(a.out + (qi * a.H + h) * kD + ch * 32);
-#pragma unroll
-                for (int c = 0; c < 4; c++)
-                    dst[c] = make_uint4(attn::pack_bf16(ov[8 * c] * inv_l, ov[8 * c + 1] * inv_l),
-                                        attn::pack_bf16(ov[8 * c + 2] * inv_l, ov[8 * c + 3] * inv_l),
-                                        attn::pack_bf16(ov[8 * c + 4] * inv_l, ov[8 * c + 5] * inv_l),
-                                        attn::pack_bf16(ov[8 * c + 6] * inv_l, ov[8 * c + 7] * inv_l));
-            }
-        }
-    }
-    attn::fence_before();
-    __syncthreads();
-    if (warp == 9) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
-static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const uint16_t *vc, int64_t nq,
-               int64_t nc, int64_t ncur, int H, float scale_log2, uint16_t *out, cudaStream_t st) {
-    CUtensorMap mQ, mKV, mKc, mVc;
-    const bool okq = attn2::make_map(&mQ, q, uint64_t(nq), uint64_t(H) * kD, uint64_t(H) * kD);
-    const bool okkv = nc > 0 ? attn2::make_map(&mKV, kv, uint64_t(2 * H) * nc, kD, kD)
-                             : attn2::make_map(&mKV, q, 1, kD, kD);
-    const bool okk = ncur > 0 ? attn2::make_map(&mKc, kc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
-                              : attn2::make_map(&mKc, q, 1, kD, kD);
-    const bool okv = ncur > 0 ? attn2::make_map(&mVc, vc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
-                              : attn2::make_map(&mVc, q, 1, kD, kD);
-    if (!(okq && okkv && okk && okv)) return set_err(QVG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    const size_t smem = kSmem + 1024;
-    cudaFuncSetAttribute(k_attention_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    dim3 grid(unsigned((nq + 2 * kTile - 1) / (2 * kTile)), unsigned(H));
-    attn2::Args args{nq, nc, ncur, H, scale_log2, out};
-    k_attention_pp<<<grid, 320, smem, st>>>(mQ, mKV, mKc, mVc, args);
-    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
-}
 }  // namespace attn3
 
 // ============================================================================
@@ -1339,310 +917,6 @@ static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const 
 }
 }  // namespace attn4
 
-// ============================================================================
-// attn5: the attn4 schedule with every S row split over TWO softmax warps
-// (columns 0-63 / 64-127 of the same TMEM lanes), so each SMSP runs two
-// softmax warps of the active tile and hides the MUFU / TMEM / FMA latencies
-// of a single warp.  18 warps: 16 softmax (tile t = warp >> 3, column half
-// hf = (warp >> 2) & 1, lane quarter = warp & 3), TMA producer, MMA issuer.
-// The halves exchange row maxima through shared memory (one 64-thread named
-// barrier per phase), keep separate running sums (same max frame), and write
-// P into their OWN S columns (half hf at TMEM columns 64 hf .. 64 hf + 31); the
-// PV MMA takes its A operand for k-steps 4..7 from the second half.  Each half
-// rescales and stores its 64 output columns.
-// ============================================================================
-namespace attn5 {
-using attn::kTile;
-using attn::kD;
-using attn2::kBox;
-using attn2::kOpTile;
-constexpr uint32_t kSmem = attn3::kSmem;
-constexpr int kThreads = 18 * 32;
-
-struct Bars {
-    uint64_t q_full, kv_full[2], kv_empty[2], s_full[2], p_full[2], o_final;
-    uint32_t tmem;
-    float xmax[2][2][128];      // [tile][half][row] partial row maxima
-    float lsum[2][2][128];      // final partial row sums
-};
-
-__device__ __forceinline__ void tmem_ld64(uint32_t taddr, float v[64]) {
-    uint32_t *r = reinterpret_cast<uint32_t *>(v);
-#pragma unroll
-    for (int c = 0; c < 2; c++) {
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(r[32 * c + 0]), "=r"(r[32 * c + 1]), "=r"(r[32 * c + 2]), "=r"(r[32 * c + 3]),
-              "=r"(r[32 * c + 4]), "=r"(r[32 * c + 5]), "=r"(r[32 * c + 6]), "=r"(r[32 * c + 7]),
-              "=r"(r[32 * c + 8]), "=r"(r[32 * c + 9]), "=r"(r[32 * c + 10]), "=r"(r[32 * c + 11]),
-              "=r"(r[32 * c + 12]), "=r"(r[32 * c + 13]), "=r"(r[32 * c + 14]), "=r"(r[32 * c + 15]),
-              "=r"(r[32 * c + 16]), "=r"(r[32 * c + 17]), "=r"(r[32 * c + 18]), "=r"(r[32 * c + 19]),
-              "=r"(r[32 * c + 20]), "=r"(r[32 * c + 21]), "=r"(r[32 * c + 22]), "=r"(r[32 * c + 23]),
-              "=r"(r[32 * c + 24]), "=r"(r[32 * c + 25]), "=r"(r[32 * c + 26]), "=r"(r[32 * c + 27]),
-              "=r"(r[32 * c + 28]), "=r"(r[32 * c + 29]), "=r"(r[32 * c + 30]), "=r"(r[32 * c + 31])
-            : "r"(taddr + 32 * c));
-    }
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-__device__ __forceinline__ void tmem_st16u(uint32_t taddr, const uint32_t v[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-            taddr),
-        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
-        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-        : "memory");
-}
-
-__device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
-
-// columns [POLY_FROM, 64) of each half row use the polynomial exp2
-template <int POLY_FROM>
-__global__ void __launch_bounds__(kThreads, 1)
-k_attention_pp5(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmKV,
-                const __grid_constant__ CUtensorMap tmKc, const __grid_constant__ CUtensorMap tmVc, attn2::Args a) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *sQ = smem;
-    uint8_t *sKV = smem + 2 * kOpTile;
-    __shared__ Bars bars;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int h = blockIdx.y;
-    const int64_t q0 = int64_t(blockIdx.x) * 2 * kTile;
-    const int64_t cb = (a.n_cache + kTile - 1) / kTile;
-    const int64_t nb = cb + (a.n_cur + kTile - 1) / kTile;
-
-    if (tid == 0) {
-        attn::bar_init(&bars.q_full, 1);
-        for (int i = 0; i < 2; i++) {
-            attn::bar_init(&bars.kv_full[i], 1);
-            attn::bar_init(&bars.kv_empty[i], 1);
-            attn::bar_init(&bars.s_full[i], 1);
-            attn::bar_init(&bars.p_full[i], 256);
-        }
-        attn::bar_init(&bars.o_final, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 17) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(attn::su32(&bars.tmem)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    attn::fence_before();
-    __syncthreads();
-    attn::fence_after();
-    const uint32_t tmem = bars.tmem;
-
-    if (warp == 16) {
-        if (lane == 0) {                              // ---- TMA producer
-            attn2::expect_tx(&bars.q_full, 2 * kOpTile);
-            for (int t = 0; t < 2; t++) {
-                attn2::tma_load_2d(sQ + t * kOpTile, &tmQ, h * kD, int(q0 + t * kTile), &bars.q_full);
-                attn2::tma_load_2d(sQ + t * kOpTile + kBox, &tmQ, h * kD + 64, int(q0 + t * kTile), &bars.q_full);
-            }
-            for (int64_t j = 0; j < nb; j++) {
-                const int st = int(j & 1);
-                if (j >= 2) attn::bar_wait_nap(&bars.kv_empty[st], uint32_t(((j - 2) >> 1) & 1), a.nap_tma);
-                uint8_t *sK = sKV + st * 2 * kOpTile, *sV = sK + kOpTile;
-                attn2::expect_tx(&bars.kv_full[st], 2 * kOpTile);
-                if (j < cb) {
-                    const int yk = int(2 * h * a.n_cache + j * kTile), yv = int((2 * h + 1) * a.n_cache + j * kTile);
-                    attn2::tma_load_2d(sK, &tmKV, 0, yk, &bars.kv_full[st]);
-                    attn2::tma_load_2d(sK + kBox, &tmKV, 64, yk, &bars.kv_full[st]);
-                    attn2::tma_load_2d(sV, &tmKV, 0, yv, &bars.kv_full[st]);
-                    attn2::tma_load_2d(sV + kBox, &tmKV, 64, yv, &bars.kv_full[st]);
-                } else {
-                    const int y = int((j - cb) * kTile);
-                    attn2::tma_load_2d(sK, &tmKc, h * kD, y, &bars.kv_full[st]);
-                    attn2::tma_load_2d(sK + kBox, &tmKc, h * kD + 64, y, &bars.kv_full[st]);
-                    attn2::tma_load_2d(sV, &tmVc, h * kD, y, &bars.kv_full[st]);
-                    attn2::tma_load_2d(sV + kBox, &tmVc, h * kD + 64, y, &bars.kv_full[st]);
-                }
-            }
-        }
-    } else if (warp == 17) {
-        if (lane == 0) {                              // ---- MMA issuer
-            constexpr uint32_t idK = attn::umma_idesc(false), idV = attn::umma_idesc(true);
-            auto issue_s = [&](int t, int64_t j) {    // S_t = Q_t K_j^T
-                const int st = int(j & 1);
-                const uint32_t sk = attn::su32(sKV + st * 2 * kOpTile);
-                const uint32_t sq = attn::su32(sQ + t * kOpTile);
-#pragma unroll
-                for (int k = 0; k < kD / 16; k++) {
-                    const uint32_t off = (k >> 2) * kBox + (k & 3) * 32;
-                    attn::mma_f16(tmem + t * 128, attn2::desc_sw128(sq + off, 16, 1024),
-                                  attn2::desc_sw128(sk + off, 16, 1024), idK, k > 0);
-                }
-                attn::mma_commit(&bars.s_full[t]);
-            };
-            auto issue_pv = [&](int t, int64_t j) {   // O_t += P_t V_j; P of keys 64.. at S columns 64..
-                const int st = int(j & 1);
-                const uint32_t sv = attn::su32(sKV + st * 2 * kOpTile) + kOpTile;
-#pragma unroll
-                for (int k = 0; k < kTile / 16; k++)
-                    attn3::mma_f16_tmem_a(tmem + 256 + t * 128, tmem + t * 128 + (k >> 2) * 64 + (k & 3) * 8,
-                                          attn2::desc_sw128(sv + k * 2048, kBox, 1024), idV,
-                                          (j > 0 || k > 0) ? 1u : 0u);
-            };
-            attn::bar_wait(&bars.q_full, 0);
-            attn::bar_wait(&bars.kv_full[0], 0);
-            attn::fence_after();
-            issue_s(0, 0);
-            issue_s(1, 0);
-            for (int64_t j = 0; j < nb; j++) {
-                attn::bar_wait_nap(&bars.p_full[0], uint32_t(j & 1), a.nap_mma);
-                attn::fence_after();
-                issue_pv(0, j);
-                if (j + 1 < nb) {
-                    attn::bar_wait_nap(&bars.kv_full[(j + 1) & 1], uint32_t(((j + 1) >> 1) & 1), a.nap_mma);
-                    attn::fence_after();
-                    issue_s(0, j + 1);
-                }
-                attn::bar_wait_nap(&bars.p_full[1], uint32_t(j & 1), a.nap_mma);
-                attn::fence_after();
-                issue_pv(1, j);
-                attn::mma_commit(&bars.kv_empty[j & 1]);
-                if (j + 1 < nb) issue_s(1, j + 1);
-            }
-            attn::mma_commit(&bars.o_final);
-        }
-    } else {
-        // ---- softmax: tile t, column half hf, rows = TMEM lanes of quarter qd ----
-        const int t = warp >> 3, hf = (warp >> 2) & 1, qd = warp & 3;
-        const int row = qd * 32 + lane;
-        const uint32_t t_lane = uint32_t(qd * 32) << 16;
-        const uint32_t tS = tmem + t * 128 + hf * 64 + t_lane, tO = tmem + 256 + t * 128 + hf * 64 + t_lane;
-        const int bar_id = 1 + t * 4 + qd;            // the two halves of these 32 rows
-        const float sl2 = a.scale_log2;
-        float m_run = -INFINITY, l_run = 0.f;
-        for (int64_t j = 0; j < nb; j++) {
-            const int64_t cnt = j < cb ? a.n_cache - j * kTile : a.n_cur - (j - cb) * kTile;
-            const int nvalid = int(cnt < kTile ? cnt : kTile) - hf * 64;     // valid columns of this half
-            attn::bar_wait_nap(&bars.s_full[t], uint32_t(j & 1), a.nap_sm);
-            attn::fence_after();
-            float s[64];
-            tmem_ld64(tS, s);
-            float2 acc4[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
-                              make_float2(0.f, 0.f)};
-            float m_new, alpha;
-            bool grow;
-            auto phase = [&](auto mask_tag) {
-                constexpr bool MASK = decltype(mask_tag)::value;
-                if constexpr (MASK) {
-#pragma unroll
-                    for (int i = 0; i < 64; i++) s[i] = i < nvalid ? s[i] : -INFINITY;
-                }
-                // 3-input max tree: 64 -> 22 -> 8 -> 3 -> 1, then the other half's
-                float m22[22];
-#pragma unroll
-                for (int i = 0; i < 21; i++) m22[i] = fmaxf(fmaxf(s[3 * i], s[3 * i + 1]), s[3 * i + 2]);
-                m22[21] = s[63];
-                float m8[8];
-#pragma unroll
-                for (int i = 0; i < 7; i++) m8[i] = fmaxf(fmaxf(m22[3 * i], m22[3 * i + 1]), m22[3 * i + 2]);
-                m8[7] = m22[21];
-                const float mh = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                                       fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-                bars.xmax[t][hf][row] = mh;
-                pair_sync(bar_id);
-                const float mx = fmaxf(mh, bars.xmax[t][hf ^ 1][row]) * sl2;
-                grow = mx > m_run + 16.f;     // lazy rescale (identical decision in both halves)
-                m_new = grow ? mx : m_run;
-                alpha = grow ? attn4::ex2_mufu(m_run - m_new) : 1.f;
-                const float2 sc2 = make_float2(sl2, sl2), nm2 = make_float2(-m_new, -m_new);
-#pragma unroll
-                for (int hq = 0; hq < 2; hq++) {
-                    uint32_t pk[16];
-#pragma unroll
-                    for (int i2 = 0; i2 < 16; i2++) {
-                        const int i = hq * 16 + i2;
-                        const float2 x = __ffma2_rn(make_float2(s[2 * i], s[2 * i + 1]), sc2, nm2);
-                        float2 e;
-                        if (2 * i < POLY_FROM) e = make_float2(attn4::ex2_mufu(x.x), attn4::ex2_mufu(x.y));
-                        else e = attn4::ex2_poly2(make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f)));
-                        if constexpr (MASK) {
-                            e.x = 2 * i < nvalid ? e.x : 0.f;
-                            e.y = 2 * i + 1 < nvalid ? e.y : 0.f;
-                        }
-                        acc4[i2 & 3] = __fadd2_rn(acc4[i2 & 3], e);
-                        pk[i2] = attn::pack_bf16(e.x, e.y);
-                    }
-                    tmem_st16u(tS + hq * 16, pk);
-                }
-            };
-            if (nvalid >= 64) phase(std::false_type{});
-            else phase(std::true_type{});
-            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-            if (j > 0 && __any_sync(0xffffffffu, grow)) {
-#pragma unroll
-                for (int ch = 0; ch < 2; ch++) {
-                    float ov[32];
-                    attn::tmem_ld32(tO + ch * 32, ov);
-#pragma unroll
-                    for (int i = 0; i < 32; i++) ov[i] *= alpha;
-                    attn::tmem_st32(tO + ch * 32, ov);
-                }
-            }
-            const float2 acc = __fadd2_rn(__fadd2_rn(acc4[0], acc4[1]), __fadd2_rn(acc4[2], acc4[3]));
-            l_run = l_run * alpha + (acc.x + acc.y);
-            m_run = m_new;
-            attn::fence_before();
-            attn2::arrive(&bars.p_full[t]);
-        }
-        // ---- epilogue: combine the halves' sums, each half stores 64 columns ----
-        bars.lsum[t][hf][row] = l_run;
-        attn::bar_wait(&bars.o_final, 0);
-        attn::fence_after();
-        pair_sync(bar_id);
-        const float inv_l = 1.f / (bars.lsum[t][0][row] + bars.lsum[t][1][row]);
-        const int64_t qi = q0 + t * kTile + row;
-#pragma unroll
-        for (int ch = 0; ch < 2; ch++) {
-            float ov[32];
-            attn::tmem_ld32(tO + ch * 32, ov);
-            if (qi < a.nq) {
-                uint4 *dst = reinterpret_cast<uint4 *>(a.out + (qi * a.H + h) * kD + hf * 64 + ch * 32);
-#pragma unroll
-                for (int c = 0; c < 4; c++)
-                    dst[c] = make_uint4(attn::pack_bf16(ov[8 * c] * inv_l, ov[8 * c + 1] * inv_l),
-                                        attn::pack_bf16(ov[8 * c + 2] * inv_l, ov[8 * c + 3] * inv_l),
-                                        attn::pack_bf16(ov[8 * c + 4] * inv_l, ov[8 * c + 5] * inv_l),
-                                        attn::pack_bf16(ov[8 * c + 6] * inv_l, ov[8 * c + 7] * inv_l));
-            }
-        }
-    }
-    attn::fence_before();
-    __syncthreads();
-    if (warp == 17) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
-static int run(const uint16_t *q, const uint16_t *kv, const uint16_t *kc, const uint16_t *vc, int64_t nq,
-               int64_t nc, int64_t ncur, int H, float scale_log2, uint16_t *out, cudaStream_t st) {
-    CUtensorMap mQ, mKV, mKc, mVc;
-    const bool okq = attn2::make_map(&mQ, q, uint64_t(nq), uint64_t(H) * kD, uint64_t(H) * kD);
-    const bool okkv = nc > 0 ? attn2::make_map(&mKV, kv, uint64_t(2 * H * nc), kD, kD)
-                             : attn2::make_map(&mKV, kc, 1, uint64_t(H) * kD, uint64_t(H) * kD);
-    const bool okk = ncur > 0 ? attn2::make_map(&mKc, kc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
-                              : attn2::make_map(&mKc, q, 1, kD, kD);
-    const bool okv = ncur > 0 ? attn2::make_map(&mVc, vc, uint64_t(ncur), uint64_t(H) * kD, uint64_t(H) * kD)
-                              : attn2::make_map(&mVc, q, 1, kD, kD);
-    if (!(okq && okkv && okk && okv)) return set_err(QVG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
-    const size_t smem = kSmem + 1024;
-    dim3 grid(unsigned((nq + 2 * kTile - 1) / (2 * kTile)), unsigned(H));
-    attn2::Args args{nq, nc, ncur, H, scale_log2, out};
-    static const int poly = [] { const char *e = getenv("QVG_ATTN_POLY5"); return e ? atoi(e) : 48; }();
-    auto go = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-        kern<<<grid, kThreads, smem, st>>>(mQ, mKV, mKc, mVc, args);
-    };
-    nap_args(args);
-    if (poly >= 64) go(k_attention_pp5<64>);
-    else if (poly >= 48) go(k_attention_pp5<48>);
-    else if (poly >= 40) go(k_attention_pp5<40>);
-    else go(k_attention_pp5<32>);
-    return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
-}
-}  // namespace attn5
 
 // ============================================================================
 // pre-RoPE key caching: the cache stores keys BEFORE the
@@ -1748,13 +1022,7 @@ int run_attention(const uint16_t *q, const uint8_t *payload, const uint8_t *scal
     } else if (n_cache > 0 && !kv) {
         return set_err(QVG_ERR_BAD_CONFIG, "cache is NULL");
     }
-    static const int kern = [] {
-        const char *e = getenv("QVG_ATTN_KERNEL");
-        return !e ? 0 : !strcmp(e, "v3") ? 3 : !strcmp(e, "pp5") ? 5 : 0;
-    }();
-    const int rc = kern == 3 ? attn3::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st)
-                 : kern == 5 ? attn5::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st)
-                             : attn4::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st);
+    const int rc = attn4::run(q, kv, k_cur, v_cur, nq, n_cache, n_cur, H, sl2, out, st);
     return rc ? set_err(rc, "attention launch failed: %s", cudaGetErrorString(cudaGetLastError())) : QVG_OK;
 }
 

@@ -707,1247 +707,6 @@ __global__ void __launch_bounds__(256) k_quantize_v4(QuantArgs a) {
 }
 
 // ------------------------------------------------------------------------
-// v5: persistent CTAs over planes, centroid tables TMA-staged in shared memory
-// (cp.async.bulk, double-buffered on mbarriers) so the per-token centroid
-// gather is an LDS instead of a dependent L2 round trip.
-// ------------------------------------------------------------------------
-template <int BITS, int S, bool OBF16>
-__global__ void __launch_bounds__(256) k_dequant_v5(DequantArgs a, PlaneLoop pl) {
-    constexpr int SS = S > 0 ? S : 1;
-    constexpr int kUnroll = 2;     // rows in flight per thread
-    constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint64_t bars[2];
-    uint16_t *const tab0 = reinterpret_cast<uint16_t *>(smem);
-    uint16_t *const tab1 = reinterpret_cast<uint16_t *>(smem + pl.tbytes);
-    const uint32_t mhi = ((1u << BITS) - 1u) << (23 - BITS), one = 0x3F800000u;
-    const uint32_t d = uint32_t(a.d), N = a.N;
-    const int col = int(threadIdx.x & ((1u << a.lvpr) - 1u)) << 4;
-    const uint32_t rslot = threadIdx.x >> a.lvpr, rpp = 256u >> a.lvpr;
-    bool bad_scale = false, bad_asg = false;
-    if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (S > 0 && threadIdx.x == 0 && blockIdx.x < pl.P) stage_table(a.cent, blockIdx.x, pl.tbytes, tab0, &bars[0]);
-    uint32_t j = 0;
-    for (uint32_t p = blockIdx.x; p < pl.P; p += gridDim.x, j++) {
-        const uint32_t b = j & 1u;
-        // prefetch the next plane's table into the other buffer (freed by the
-        // __syncthreads that ended the previous plane)
-        if (S > 0 && threadIdx.x == 0 && p + gridDim.x < pl.P)
-            stage_table(a.cent, p + gridDim.x, pl.tbytes, b ? tab0 : tab1, b ? &bars[0] : &bars[1]);
-        if (S > 0) mbar_wait(b ? &bars[1] : &bars[0], (j >> 1) & 1u);
-        const uint16_t *ct = b ? tab1 : tab0;
-        const uint64_t pN = uint64_t(p) * N;
-        const uint8_t *pp = a.payload + uint64_t(p) * a.pb;
-        const uint8_t *sp = a.scales + uint64_t(p) * a.ng;
-        const uint8_t *ap = a.asg + pN * S;
-        for (uint32_t i0 = 0; i0 < N; i0 += rpp * kUnroll) {       // CTA-uniform
-            Codes16<BITS> w[kUnroll];
-            uint32_t sc[kUnroll], ii[kUnroll];
-            int ai[kUnroll][SS];
-#pragma unroll
-            for (int u = 0; u < kUnroll; u++) {
-                const uint32_t i = i0 + u * rpp + rslot;
-                ii[u] = i < N ? i : N - 1;
-                const uint32_t e0 = ii[u] * d + col;
-                w[u] = load_codes16<BITS>(pp + ((e0 * BITS) >> 3));
-                sc[u] = __ldg(sp + (e0 >> a.lgB));
-#pragma unroll
-                for (int t = 0; t < S; t++) {
-                    int at = __ldg(ap + t * N + ii[u]);
-                    bad_asg |= at >= a.K;
-                    ai[u][t] = at < a.K ? at : 0;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kUnroll; u++) {
-                const bool valid = i0 + u * rpp + rslot < N;
-                bad_scale |= (sc[u] & 0x7Fu) == 0x7Fu;
-                const float s = e4m3_decode_fast(sc[u]);
-                Codes16<BITS> wx;
-#pragma unroll
-                for (int q = 0; q < Codes16<BITS>::NW; q++) wx.w[q] = w[u].w[q] ^ SIGNS;
-                const float s_hi = s * float(1 << BITS), s_off = s * (-1.5f * float(1 << BITS));
-                float y[16];
-#pragma unroll
-                for (int k = 0; k < 16; k++) y[k] = qs16<BITS>(wx, k, mhi, one, s_hi, s_off);   // exact
-                bool inexact = false;
-#pragma unroll
-                for (int t = S - 1; t >= 0; t--) {                 // reversed(stages)
-                    const uint4 *c4 = reinterpret_cast<const uint4 *>(ct + uint32_t(t * a.K + ai[u][t]) * d + col);
-                    float c[16];
-                    cvt16(c4[0], c4[1], c);
-#pragma unroll
-                    for (int k = 0; k < 16; k++) {
-                        const float s2 = __fadd_rn(y[k], c[k]);
-                        if (t > 0) inexact |= (__fsub_rn(s2, y[k]) != c[k]) | (__fsub_rn(s2, c[k]) != y[k]);
-                        y[k] = s2;
-                    }
-                }
-                if (inexact) {  // rare: a non-final partial sum needed > 24 bits -> f64 chain
-#pragma unroll
-                    for (int k = 0; k < 16; k++)
-                        y[k] = exact_addback1<BITS, S>(qs16<BITS>(wx, k, mhi, one, s_hi, s_off), ct, col + k, d,
-                                                       a.K, ai[u][0], ai[u][SS > 1 ? 1 : 0],
-                                                       ai[u][SS > 2 ? 2 : 0], ai[u][SS > 3 ? 3 : 0]);
-                }
-                if (!valid) continue;
-                const uint64_t o = (pN + ii[u]) * d + col;
-                if constexpr (OBF16) {
-                    uint32_t v[8];
-#pragma unroll
-                    for (int q = 0; q < 8; q++) {
-                        __nv_bfloat162 h = __floats2bfloat162_rn(y[2 * q], y[2 * q + 1]);
-                        v[q] = *reinterpret_cast<uint32_t *>(&h);
-                    }
-                    uint4 *op = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(a.out) + o);
-                    op[0] = make_uint4(v[0], v[1], v[2], v[3]);
-                    op[1] = make_uint4(v[4], v[5], v[6], v[7]);
-                } else {
-                    float4 *op = reinterpret_cast<float4 *>(static_cast<float *>(a.out) + o);
-#pragma unroll
-                    for (int q = 0; q < 4; q++) op[q] = make_float4(y[4 * q], y[4 * q + 1], y[4 * q + 2], y[4 * q + 3]);
-                }
-            }
-        }
-        __syncthreads();    // everyone is done with tab[b] before it is refilled
-    }
-    const uint32_t stat = (bad_scale ? QVG_STATUS_NAN_SCALE : 0u) | (bad_asg ? QVG_STATUS_BAD_ASSIGN : 0u);
-    const uint32_t all = __reduce_or_sync(0xffffffffu, stat);
-    if (all && (threadIdx.x & 31) == 0) atomicOr(a.status, int(all));
-}
-
-__device__ __forceinline__ float v5_max3_nan_abs(float m, float a, float b) {
-    float t, d;
-    asm("max.NaN.f32 %0, %1, %2;" : "=f"(t) : "f"(fabsf(a)), "f"(fabsf(b)));
-    asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(m), "f"(t));
-    return d;
-}
-template <int BITS>
-__host__ __device__ constexpr uint32_t v5_magic_sum() {
-    uint32_t acc = 0;
-    for (int k = 0; k < 32 / BITS; k++) acc += 0x4B400000u << (BITS * k);
-    return acc;
-}
-
-template <int BITS, int S, bool XBF16>
-__global__ void __launch_bounds__(256) k_quantize_v5(QuantArgs a, PlaneLoop pl) {
-    constexpr int QMAX = (1 << (BITS - 1)) - 1;
-    constexpr int SS = S > 0 ? S : 1;
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint64_t bars[2];
-    __shared__ float rcp_tab[128];          // RN32(1 / e4m3(code))
-    uint16_t *const tab0 = reinterpret_cast<uint16_t *>(smem);
-    uint16_t *const tab1 = reinterpret_cast<uint16_t *>(smem + pl.tbytes);
-    const uint32_t d = uint32_t(a.d), N = a.N;
-    const int col = int(threadIdx.x & ((1u << a.lvpr) - 1u)) << 4;
-    const uint32_t rslot = threadIdx.x >> a.lvpr, rpp = 256u >> a.lvpr;
-    const int glanes = 1 << a.gshift;
-    const int lane = threadIdx.x & 31;
-    bool nonfinite = false;
-    if (threadIdx.x < 128) rcp_tab[threadIdx.x] = __frcp_rn(e4m3_decode_fast(threadIdx.x));
-    if (threadIdx.x == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (S > 0 && threadIdx.x == 0 && blockIdx.x < pl.P) stage_table(a.cent, blockIdx.x, pl.tbytes, tab0, &bars[0]);
-    uint32_t j = 0;
-    for (uint32_t p = blockIdx.x; p < pl.P; p += gridDim.x, j++) {
-        const uint32_t b = j & 1u;
-        if (S > 0 && threadIdx.x == 0 && p + gridDim.x < pl.P)
-            stage_table(a.cent, p + gridDim.x, pl.tbytes, b ? tab0 : tab1, b ? &bars[0] : &bars[1]);
-        if (S > 0) mbar_wait(b ? &bars[1] : &bars[0], (j >> 1) & 1u);
-        const uint16_t *ct = b ? tab1 : tab0;
-        const uint64_t pN = uint64_t(p) * N;
-        const uint8_t *xb = static_cast<const uint8_t *>(a.x) + pN * d * (XBF16 ? 2 : 4);
-        const uint8_t *ap = a.asg + pN * S;
-        for (uint32_t i0 = 0; i0 < N; i0 += rpp * kUnroll) {
-            float r[kUnroll][16];
-            uint32_t ii[kUnroll];
-            int ai[kUnroll][SS];
-#pragma unroll
-            for (int u = 0; u < kUnroll; u++) {
-                const uint32_t i = i0 + u * rpp + rslot;
-                ii[u] = i < N ? i : N - 1;
-                load_x16<XBF16>(xb, ii[u] * d + col, r[u]);
-#pragma unroll
-                for (int t = 0; t < S; t++) ai[u][t] = __ldg(ap + t * N + ii[u]);
-            }
-            float eb[kUnroll], am[kUnroll];
-#pragma unroll
-            for (int u = 0; u < kUnroll; u++) {
-                // e = sum_{t<S} max_k |r_t,k| + max_k |r_S,k| bounds every element's
-                // sum_t |r_t,k| (the error-bound input); the maxima propagate NaN, so a
-                // NaN/Inf in x or a centroid makes e non-finite: the finiteness check
-                float2 *r2 = reinterpret_cast<float2 *>(r[u]);
-                float e = 0.f;
-#pragma unroll
-                for (int t = 0; t < S; t++) {
-                    const uint4 *c4 = reinterpret_cast<const uint4 *>(ct + uint32_t(t * a.K + ai[u][t]) * d + col);
-                    float c[16];
-                    cvt16(c4[0], c4[1], c);
-#pragma unroll
-                    for (int q = 0; q < 8; q++) r2[q] = __fadd2_rn(r2[q], make_float2(-c[2 * q], -c[2 * q + 1]));
-                    if (t < S - 1) {
-                        float m = 0.f;
-#pragma unroll
-                        for (int q = 0; q < 8; q++) m = v5_max3_nan_abs(m, r2[q].x, r2[q].y);
-                        e = __fadd_ru(e, m);
-                    }
-                }
-                float mx = 0.f;
-#pragma unroll
-                for (int q = 0; q < 8; q++) mx = v5_max3_nan_abs(mx, r2[q].x, r2[q].y);
-                nonfinite |= !(mx <= 3.402823466e38f) || !(e <= 3.402823466e38f);
-                eb[u] = S > 0 ? __fadd_ru(e, mx) : 0.f;
-                am[u] = mx;
-            }
-            for (int m = 1; m < glanes; m <<= 1) {
-#pragma unroll
-                for (int u = 0; u < kUnroll; u++) {
-                    am[u] = fmaxf(am[u], __shfl_xor_sync(0xffffffffu, am[u], m));
-                    eb[u] = fmaxf(eb[u], __shfl_xor_sync(0xffffffffu, eb[u], m));
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < kUnroll; u++) {
-                const bool valid = i0 + u * rpp + rslot < N;
-                const float E = __fmul_ru(eb[u], 2.38418579e-7f);
-                uint32_t code;
-                bool camb = false;
-                if (am[u] == 0.f && E == 0.f) code = 0x38u;
-                else {
-                    const float lo = __fsub_rd(am[u], E), hi = __fadd_ru(am[u], E);
-                    if (lo > 0.f) code = scale_code<QMAX>(lo, hi, camb);
-                    else { code = 0x38u; camb = true; }
-                }
-                camb &= valid;
-                auto exact_r = [&](int k) {
-                    return exact_residual<XBF16, S>(xb, ct, ii[u] * d + col + k, col + k, d, a.K, ai[u][0],
-                                                    ai[u][SS > 1 ? 1 : 0], ai[u][SS > 2 ? 2 : 0],
-                                                    ai[u][SS > 3 ? 3 : 0]);
-                };
-                if (__any_sync(0xffffffffu, camb)) {          // exact scale (rare)
-                    const float thr = __fsub_rd(am[u], __fmul_ru(E, 2.f));
-                    uint32_t cand = 0;
-#pragma unroll
-                    for (int k = 0; k < 16; k++) cand |= (camb && fabsf(r[u][k]) >= thr) ? 1u << k : 0u;
-                    double a64 = 0.0;
-                    while (cand) {
-                        const int k = __ffs(cand) - 1;
-                        cand &= cand - 1;
-                        a64 = fmax(a64, fabs(exact_r(k)));
-                    }
-                    for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
-                    if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
-                }
-                const float s = e4m3_decode_fast(code);
-                const float inv = rcp_tab[code & 0x7Fu];
-                const float2 inv2 = make_float2(inv, inv);
-                const float2 *r2 = reinterpret_cast<const float2 *>(r[u]);
-                // codes: the bits of fma(r, 1/s, 1.5*2^23 + 2^(b-1)) are 0x4B400000 + q + 2^(b-1);
-                // a multiply-add tree packs the fields (no carries: q + 2^(b-1) < 2^b)
-                constexpr float MAGIC = 12582912.f + float(1 << (BITS - 1));
-                constexpr int FPW = 32 / BITS;
-                constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
-                float2 yv[8];
-#pragma unroll
-                for (int q = 0; q < 8; q++) yv[q] = __ffma2_rn(r2[q], inv2, make_float2(MAGIC, MAGIC));
-                uint32_t b32[BITS / 2];
-#pragma unroll
-                for (int wd = 0; wd < BITS / 2; wd++) {
-                    uint32_t v[FPW];
-#pragma unroll
-                    for (int k2 = 0; k2 < FPW; k2++) {
-                        const int e = wd * FPW + k2;
-                        v[k2] = __float_as_uint((e & 1) ? yv[e >> 1].y : yv[e >> 1].x);
-                    }
-#pragma unroll
-                    for (int span = 1; span < FPW; span *= 2)
-#pragma unroll
-                        for (int k2 = 0; k2 < FPW; k2 += 2 * span) v[k2] += v[k2 + span] << (BITS * span);
-                    b32[wd] = (v[0] - v5_magic_sum<BITS>()) ^ SIGNS;
-                }
-                // ambiguity: per-element window predicate (E plus the 1/s rounding),
-                // reduced over the row, re-evaluated identically for the fix-up
-                const bool all = !(E < 0.125f * s) || code == 0x7Eu;
-                float thr;
-                float2 pa;
-                if constexpr (QMAX == 1) {
-                    const float h = 0.5f * s;
-                    const float W = __fmaf_ru(h, 2.38418579e-7f, E);
-                    thr = __fmul_ru(__fmul_ru(W, __fadd_ru(s, W)), 1.00000095367f);
-                    pa = make_float2(-h * h, -h * h);
-                } else {
-                    const float delta = __fmaf_ru(__fmul_ru(E, inv), 1.0000002f, float(QMAX + 1) * 2.38418579e-7f);
-                    thr = __fsub_rd(0.5f, delta);
-                    pa = make_float2(-MAGIC, -MAGIC);
-                }
-                auto window = [&](int q) -> float2 {
-                    if constexpr (QMAX == 1) {
-                        const float2 gg = __ffma2_rn(r2[q], r2[q], pa);
-                        return make_float2(fabsf(gg.x), fabsf(gg.y));
-                    } else {
-                        const float2 qf = __fadd2_rn(yv[q], pa);
-                        const float2 dist = __ffma2_rn(r2[q], inv2, make_float2(-qf.x, -qf.y));
-                        return make_float2(fabsf(dist.x), fabsf(dist.y));
-                    }
-                };
-                bool amb;
-                {
-                    float wv[8];
-#pragma unroll
-                    for (int q = 0; q < 8; q++) {
-                        const float2 w = window(q);
-                        wv[q] = QMAX == 1 ? fminf(w.x, w.y) : fmaxf(w.x, w.y);
-                    }
-#pragma unroll
-                    for (int span = 1; span < 8; span *= 2)
-#pragma unroll
-                        for (int q = 0; q < 8; q += 2 * span) wv[q] = QMAX == 1 ? fminf(wv[q], wv[q + span]) : fmaxf(wv[q], wv[q + span]);
-                    amb = all || (QMAX == 1 ? wv[0] <= thr : wv[0] >= thr);
-                }
-                amb &= valid;
-                if (__any_sync(0xffffffffu, amb) && amb) {   // exact codes (rare)
-                    uint32_t todo = 0;
-#pragma unroll
-                    for (int q = 0; q < 8; q++) {
-                        const float2 w = window(q);
-                        bool in0, in1;
-                        if constexpr (QMAX == 1) { in0 = w.x <= thr; in1 = w.y <= thr; }
-                        else { in0 = w.x >= thr; in1 = w.y >= thr; }
-                        in0 |= all || !(fabsf(r2[q].x) <= 3.402823466e38f);
-                        in1 |= all || !(fabsf(r2[q].y) <= 3.402823466e38f);
-                        todo |= (in0 ? 1u << (2 * q) : 0u) | (in1 ? 2u << (2 * q) : 0u);
-                    }
-                    while (todo) {
-                        const int k = __ffs(todo) - 1;
-                        todo &= todo - 1;
-                        const uint32_t q = exact_code<QMAX>(exact_r(k), s) & ((1u << BITS) - 1u);
-                        const int sh = (k * BITS) & 31, wi = (k * BITS) >> 5;
-#pragma unroll
-                        for (int q2 = 0; q2 < BITS / 2; q2++)
-                            if (q2 == wi) b32[q2] = (b32[q2] & ~(((1u << BITS) - 1u) << sh)) | (q << sh);
-                    }
-                }
-                if (!valid) continue;
-                const uint32_t e0 = ii[u] * d + col;
-                uint8_t *plp = a.payload + uint64_t(p) * a.pb + ((e0 * BITS) >> 3);
-                if constexpr (BITS == 2) *reinterpret_cast<uint32_t *>(plp) = b32[0];
-                else if constexpr (BITS == 4) *reinterpret_cast<uint2 *>(plp) = make_uint2(b32[0], b32[1]);
-                else *reinterpret_cast<uint4 *>(plp) = make_uint4(b32[0], b32[1], b32[2], b32[3]);
-                if ((lane & (glanes - 1)) == 0) a.scales[uint64_t(p) * a.ng + (e0 >> a.lgB)] = uint8_t(code);
-            }
-        }
-        __syncthreads();
-    }
-    const uint32_t all = __reduce_or_sync(0xffffffffu, nonfinite ? uint32_t(QVG_STATUS_NONFINITE) : 0u);
-    if (all && lane == 0) atomicOr(a.status, int(all));
-}
-
-// ------------------------------------------------------------------------
-// v6: the per-plane centroid tables are widened ONCE to f32 in shared memory
-// (XOR-swizzled so the 8 threads of a row read 8 distinct bank groups), next
-// to per-(stage, centroid, 16-channel chunk) metadata {ulp of the smallest
-// non-zero |c|, max |c|}.  The element loop is then pure packed f32x2
-// arithmetic (FADD2/FFMA2) plus 3-input max/min reductions:
-//  * quantize: codes come from the magic-number rounding fma(r, 1/s, 1.5*2^23
-//    + 2^(b-1)) whose float bits carry q + 2^(b-1) in the low mantissa, and
-//    are packed with one integer multiply-add per element; the ambiguity
-//    test is one reduction per row (2-bit: min |r^2 - (s/2)^2|, b>2: max
-//    distance to the rounded value), and the residual error bound comes
-//    from the metadata instead of a per-element max;
-//  * dequantize: the exactness of the non-final f32 partial sums is
-//    certified per row from the metadata (every term is a multiple of the
-//    smallest ulp and the sum stays below 2^24 of it); a row without the
-//    certificate is recomputed with the reference's float64 chain.
-// ------------------------------------------------------------------------
-struct V6Plane {
-    uint32_t P;        // planes
-    uint32_t tbytes;   // bf16 table bytes per plane (S*K*d*2)
-    uint32_t nchunk;   // S*K*d/16 metadata entries per plane
-    uint32_t lchunk;   // log2(d/16)
-    uint32_t ipp;      // work items (row ranges) per plane
-    uint32_t rpi;      // rows per item
-    uint32_t n_items;  // P * ipp; CTA b owns the contiguous items [b*n/G, (b+1)*n/G)
-};
-
-// swizzled float offset of channel ch inside a table row: 16-byte chunk L
-// goes to L ^ ((L >> 3) & 3)
-__device__ __forceinline__ uint32_t v6_swz(uint32_t ch) {
-    const uint32_t L = ch >> 2;
-    return ((L ^ ((L >> 3) & 3u)) << 2) | (ch & 3u);
-}
-
-__device__ __forceinline__ float max3_nan_abs(float m, float a, float b) {
-    float t, d;
-    asm("max.NaN.f32 %0, %1, %2;" : "=f"(t) : "f"(fabsf(a)), "f"(fabsf(b)));
-    asm("max.NaN.f32 %0, %1, %2;" : "=f"(d) : "f"(m), "f"(t));
-    return d;
-}
-
-// widen the staged bf16 tables [S*K][d] to swizzled f32 + chunk metadata
-__device__ __forceinline__ void v6_widen(const uint16_t *stg, float *tab, float2 *meta, const V6Plane &pl,
-                                         uint32_t d) {
-    const uint32_t cmask = (1u << pl.lchunk) - 1u;
-    for (uint32_t q = threadIdx.x; q < pl.nchunk; q += blockDim.x) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(stg + size_t(q) * 16);
-        float c[16];
-        cvt16(src[0], src[1], c);
-        float mx = 0.f, mn = __int_as_float(0x7F800000);
-#pragma unroll
-        for (int k = 0; k < 16; k++) {
-            const float a = fabsf(c[k]);
-            mx = fmaxf(mx, a);
-            mn = a > 0.f ? fminf(mn, a) : mn;
-        }
-        float *dst = tab + size_t(q >> pl.lchunk) * d;
-        const uint32_t ch0 = (q & cmask) << 4;
-#pragma unroll
-        for (int j = 0; j < 4; j++)
-            *reinterpret_cast<float4 *>(dst + v6_swz(ch0 + 4 * j)) =
-                make_float4(c[4 * j], c[4 * j + 1], c[4 * j + 2], c[4 * j + 3]);
-        // ulp of a bf16 value with the exponent of mn: 2^(e-7); 0 when that is
-        // not a normal float (certificate then fails, conservatively); +inf
-        // when the chunk is all zero (no constraint)
-        float unit;
-        if (mn == __int_as_float(0x7F800000)) unit = mn;
-        else {
-            const uint32_t eb = __float_as_uint(mn) & 0x7F800000u;
-            unit = eb > (7u << 23) ? __uint_as_float(eb - (7u << 23)) : 0.f;
-        }
-        // NaN/Inf anywhere in the chunk: max is NaN/Inf, which fails every
-        // certificate below (comparisons with NaN are false)
-        meta[q] = make_float2(unit, mx);
-    }
-}
-
-// item-loop prologue shared by K5/K6 v6 on a plane change: wait for plane
-// p's staged table, widen it, then stage the next plane this CTA will visit
-__device__ __forceinline__ void v6_plane_tables(const uint16_t *cent, uint32_t j, int64_t next_p,
-                                                const V6Plane &pl, uint16_t *stg, float *tab, float2 *meta,
-                                                uint64_t *bar, uint32_t d) {
-    __syncthreads();                          // everyone done with the previous plane's tables
-    mbar_wait(bar, j & 1u);
-    v6_widen(stg, tab, meta, pl, d);
-    __syncthreads();                          // tables ready; staging buffer free
-    if (threadIdx.x == 0 && next_p >= 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        stage_table(cent, uint32_t(next_p), pl.tbytes, stg, bar);
-    }
-}
-
-// this CTA's contiguous item range
-__device__ __forceinline__ void v6_items(const V6Plane &pl, uint32_t &it0, uint32_t &it1) {
-    it0 = uint32_t((uint64_t(blockIdx.x) * pl.n_items) / gridDim.x);
-    it1 = uint32_t((uint64_t(blockIdx.x + 1) * pl.n_items) / gridDim.x);
-}
-
-// the reference's float64 add-back for one element (Q/prq.py:113-132), f32 table
-template <int S>
-__device__ __noinline__ float v6_exact_addback(float qs, const float *tab, uint32_t off, uint32_t d, int K,
-                                               int a0, int a1, int a2, int a3) {
-    const int ai[4] = {a0, a1, a2, a3};
-    double acc = double(qs);
-#pragma unroll
-    for (int t = S - 1; t >= 0; t--) acc = __dadd_rn(acc, double(tab[uint32_t(t * K + ai[t]) * d + off]));
-    return __double2float_rn(acc);
-}
-
-// the reference's float64 residual x - C_1[pi_1] - ... (Q/smoothing.py:40), f32 table
-template <bool XBF16, int S>
-__device__ __noinline__ double v6_exact_residual(const uint8_t *xb, const float *tab, uint32_t e, uint32_t off,
-                                                 uint32_t d, int K, int a0, int a1, int a2, int a3) {
-    double v = double(load_x1f<XBF16>(xb, e));
-    const int ai[4] = {a0, a1, a2, a3};
-#pragma unroll
-    for (int t = 0; t < S; t++) v = __dsub_rn(v, double(tab[uint32_t(t * K + ai[t]) * d + off]));
-    return v;
-}
-
-template <int BITS, int S, bool OBF16>
-__global__ void __launch_bounds__(256, 2) k_dequant_v6(DequantArgs a, V6Plane pl) {
-    constexpr int SS = S > 0 ? S : 1;
-    constexpr int U = 2;
-    constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint64_t bar;
-    uint16_t *const stg = reinterpret_cast<uint16_t *>(smem);
-    float *const tab = reinterpret_cast<float *>(smem + pl.tbytes);
-    float2 *const meta = reinterpret_cast<float2 *>(smem + 3 * size_t(pl.tbytes));
-    const uint32_t mhi = ((1u << BITS) - 1u) << (23 - BITS), one = 0x3F800000u;
-    const uint32_t d = uint32_t(a.d), N = a.N;
-    const uint32_t c = threadIdx.x & ((1u << a.lvpr) - 1u);
-    const int col = int(c) << 4;
-    const uint32_t rslot = threadIdx.x >> a.lvpr, rpp = 256u >> a.lvpr;
-    uint32_t off[4];
-#pragma unroll
-    for (int j = 0; j < 4; j++) off[j] = v6_swz(uint32_t(col + 4 * j));
-    bool bad_scale = false, bad_asg = false;
-    if (threadIdx.x == 0) {
-        mbar_init(&bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    uint32_t it0, it1;
-    v6_items(pl, it0, it1);
-    if (S > 0 && threadIdx.x == 0 && it0 < it1) stage_table(a.cent, it0 / pl.ipp, pl.tbytes, stg, &bar);
-    uint32_t jp = 0, cur = 0xFFFFFFFFu;
-    for (uint32_t it = it0; it < it1; it++) {
-        const uint32_t p = it / pl.ipp;
-        const uint32_t r0 = (it - p * pl.ipp) * pl.rpi, r1 = min(N, r0 + pl.rpi);
-        if (p != cur) {
-            const int64_t nxt = int64_t(p + 1) * pl.ipp < int64_t(it1) ? int64_t(p + 1) : -1;
-            if (S > 0) v6_plane_tables(a.cent, jp, nxt, pl, stg, tab, meta, &bar, d);
-            cur = p;
-            jp++;
-        }
-        const uint64_t pN = uint64_t(p) * N;
-        const uint8_t *pp = a.payload + uint64_t(p) * a.pb;
-        const uint8_t *sp = a.scales + uint64_t(p) * a.ng;
-        const uint8_t *ap = a.asg + pN * S;
-        for (uint32_t i0 = r0; i0 < r1; i0 += rpp * U) {
-            Codes16<BITS> w[U];
-            uint32_t sc[U], ii[U];
-            int ai[U][SS];
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                const uint32_t i = i0 + u * rpp + rslot;
-                ii[u] = i < r1 ? i : r1 - 1;
-                const uint32_t e0 = ii[u] * d + col;
-                w[u] = load_codes16<BITS>(pp + ((e0 * BITS) >> 3));
-                sc[u] = __ldg(sp + (e0 >> a.lgB));
-#pragma unroll
-                for (int t = 0; t < S; t++) {
-                    const int at = __ldg(ap + t * N + ii[u]);
-                    bad_asg |= at >= a.K;
-                    ai[u][t] = at < a.K ? at : 0;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                const bool valid = i0 + u * rpp + rslot < r1;
-                bad_scale |= (sc[u] & 0x7Fu) == 0x7Fu;
-                const float s = e4m3_decode_fast(sc[u]);
-                Codes16<BITS> wx;
-#pragma unroll
-                for (int q = 0; q < Codes16<BITS>::NW; q++) wx.w[q] = w[u].w[q] ^ SIGNS;
-                const float2 s_hi = make_float2(s * float(1 << BITS), s * float(1 << BITS));
-                const float2 s_off = make_float2(s * (-1.5f * float(1 << BITS)), s * (-1.5f * float(1 << BITS)));
-                float2 y[8];
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    const int k0 = 2 * k, k1 = 2 * k + 1;
-                    constexpr int POS = 23 - BITS;
-                    const int b0 = k0 * BITS, b1 = k1 * BITS;
-                    const uint32_t v0 = (b0 & 31) <= POS ? (wx.w[b0 >> 5] << (POS - (b0 & 31))) : (wx.w[b0 >> 5] >> ((b0 & 31) - POS));
-                    const uint32_t v1 = (b1 & 31) <= POS ? (wx.w[b1 >> 5] << (POS - (b1 & 31))) : (wx.w[b1 >> 5] >> ((b1 & 31) - POS));
-                    const float2 f = make_float2(__uint_as_float(lop3_and_or(v0, mhi, one)),
-                                                 __uint_as_float(lop3_and_or(v1, mhi, one)));
-                    y[k] = __ffma2_rn(f, s_hi, s_off);          // q*s, exact
-                }
-                // certificate: every non-final partial sum exact in f32
-                bool cert = true;
-                if constexpr (S >= 2) {
-                    float unit = fmaxf(__uint_as_float((__float_as_uint(s) & 0x7F800000u) - (3u << 23)), 0.001953125f);
-                    float bound = s * float(1 << (BITS - 1));
-#pragma unroll
-                    for (int t = 1; t < S; t++) {
-                        const float2 m = meta[(uint32_t(t * a.K + ai[u][t]) << pl.lchunk) + c];
-                        unit = fminf(unit, m.x);
-                        bound = __fadd_ru(bound, m.y);
-                    }
-                    cert = bound < unit * 16777216.f;
-                }
-#pragma unroll
-                for (int t = S - 1; t >= 0; t--) {                 // reversed(stages)
-                    const float *row = tab + uint32_t(t * a.K + ai[u][t]) * d;
-#pragma unroll
-                    for (int j = 0; j < 4; j++) {
-                        const float4 cv = *reinterpret_cast<const float4 *>(row + off[j]);
-                        y[2 * j] = __fadd2_rn(y[2 * j], make_float2(cv.x, cv.y));
-                        y[2 * j + 1] = __fadd2_rn(y[2 * j + 1], make_float2(cv.z, cv.w));
-                    }
-                }
-                if (!cert) {   // rare: recompute the row with the float64 chain
-#pragma unroll
-                    for (int k = 0; k < 16; k++) {
-                        const int b = k * BITS, wi = b >> 5, o = b & 31;
-                        constexpr int POS = 23 - BITS;
-                        const uint32_t v = o <= POS ? (wx.w[wi] << (POS - o)) : (wx.w[wi] >> (o - POS));
-                        const float qs = __fmaf_rn(__uint_as_float(lop3_and_or(v, mhi, one)), s_hi.x, s_off.x);
-                        const float r = v6_exact_addback<S>(qs, tab, off[k >> 2] + (k & 3), d, a.K, ai[u][0],
-                                                            ai[u][SS > 1 ? 1 : 0], ai[u][SS > 2 ? 2 : 0],
-                                                            ai[u][SS > 3 ? 3 : 0]);
-                        if (k & 1) y[k >> 1].y = r; else y[k >> 1].x = r;
-                    }
-                }
-                if (!valid) continue;
-                const uint64_t o = (pN + ii[u]) * d + col;
-                if constexpr (OBF16) {
-                    uint32_t v[8];
-#pragma unroll
-                    for (int q = 0; q < 8; q++) {
-                        __nv_bfloat162 h = __floats2bfloat162_rn(y[q].x, y[q].y);
-                        v[q] = *reinterpret_cast<uint32_t *>(&h);
-                    }
-                    uint4 *op = reinterpret_cast<uint4 *>(static_cast<uint16_t *>(a.out) + o);
-                    op[0] = make_uint4(v[0], v[1], v[2], v[3]);
-                    op[1] = make_uint4(v[4], v[5], v[6], v[7]);
-                } else {
-                    float4 *op = reinterpret_cast<float4 *>(static_cast<float *>(a.out) + o);
-#pragma unroll
-                    for (int q = 0; q < 4; q++) op[q] = make_float4(y[2 * q].x, y[2 * q].y, y[2 * q + 1].x, y[2 * q + 1].y);
-                }
-            }
-        }
-    }
-    const uint32_t stat = (bad_scale ? QVG_STATUS_NAN_SCALE : 0u) | (bad_asg ? QVG_STATUS_BAD_ASSIGN : 0u);
-    const uint32_t all = __reduce_or_sync(0xffffffffu, stat);
-    if (all && (threadIdx.x & 31) == 0) atomicOr(a.status, int(all));
-}
-
-// packing constant: sum over the fields of one word of 0x4B400000 << (b*k)
-template <int BITS>
-__host__ __device__ constexpr uint32_t v6_magic_sum() {
-    uint32_t acc = 0;
-    for (int k = 0; k < 32 / BITS; k++) acc += 0x4B400000u << (BITS * k);
-    return acc;
-}
-
-template <int BITS, int S, bool XBF16>
-__global__ void __launch_bounds__(256, 2) k_quantize_v6(QuantArgs a, V6Plane pl) {
-    constexpr int QMAX = (1 << (BITS - 1)) - 1;
-    constexpr int SS = S > 0 ? S : 1;
-    constexpr int U = 2;
-    constexpr int FPW = 32 / BITS;                       // fields per payload word
-    constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
-    constexpr float MAGIC = 12582912.f + float(1 << (BITS - 1));   // 1.5*2^23 + bias
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint64_t bar;
-    uint16_t *const stg = reinterpret_cast<uint16_t *>(smem);
-    float *const tab = reinterpret_cast<float *>(smem + pl.tbytes);
-    float2 *const meta = reinterpret_cast<float2 *>(smem + 3 * size_t(pl.tbytes));
-    const uint32_t d = uint32_t(a.d), N = a.N;
-    const uint32_t c = threadIdx.x & ((1u << a.lvpr) - 1u);
-    const int col = int(c) << 4;
-    const uint32_t rslot = threadIdx.x >> a.lvpr, rpp = 256u >> a.lvpr;
-    const int glanes = 1 << a.gshift;
-    const int lane = threadIdx.x & 31;
-    uint32_t off[4];
-#pragma unroll
-    for (int j = 0; j < 4; j++) off[j] = v6_swz(uint32_t(col + 4 * j));
-    bool nonfinite = false;
-    if (threadIdx.x == 0) {
-        mbar_init(&bar, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    uint32_t it0, it1;
-    v6_items(pl, it0, it1);
-    if (S > 0 && threadIdx.x == 0 && it0 < it1) stage_table(a.cent, it0 / pl.ipp, pl.tbytes, stg, &bar);
-    uint32_t jp = 0, cur = 0xFFFFFFFFu;
-    for (uint32_t it = it0; it < it1; it++) {
-        const uint32_t p = it / pl.ipp;
-        const uint32_t r0 = (it - p * pl.ipp) * pl.rpi, r1 = min(N, r0 + pl.rpi);
-        if (p != cur) {
-            const int64_t nxt = int64_t(p + 1) * pl.ipp < int64_t(it1) ? int64_t(p + 1) : -1;
-            if (S > 0) v6_plane_tables(a.cent, jp, nxt, pl, stg, tab, meta, &bar, d);
-            cur = p;
-            jp++;
-        }
-        const uint64_t pN = uint64_t(p) * N;
-        const uint8_t *xb = static_cast<const uint8_t *>(a.x) + pN * d * (XBF16 ? 2 : 4);
-        const uint8_t *ap = a.asg + pN * S;
-        for (uint32_t i0 = r0; i0 < r1; i0 += rpp * U) {
-            float2 r[U][8];
-            uint32_t ii[U];
-            int ai[U][SS];
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                const uint32_t i = i0 + u * rpp + rslot;
-                ii[u] = i < r1 ? i : r1 - 1;
-                load_x16<XBF16>(xb, ii[u] * d + col, reinterpret_cast<float *>(r[u]));
-#pragma unroll
-                for (int t = 0; t < S; t++) ai[u][t] = __ldg(ap + t * N + ii[u]);
-            }
-            float eb[U], am[U];
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                // sum_t max|r_t| <= S*max|r_S| + sum_t t*max|c_{t+1}| (|r_t| <= |r_S| + sum_{v>t}|c_v|)
-                float cb = 0.f;
-#pragma unroll
-                for (int t = 0; t < S; t++) {
-                    const float *row = tab + uint32_t(t * a.K + ai[u][t]) * d;
-#pragma unroll
-                    for (int j = 0; j < 4; j++) {
-                        const float4 cv = *reinterpret_cast<const float4 *>(row + off[j]);
-                        r[u][2 * j] = __fadd2_rn(r[u][2 * j], make_float2(-cv.x, -cv.y));
-                        r[u][2 * j + 1] = __fadd2_rn(r[u][2 * j + 1], make_float2(-cv.z, -cv.w));
-                    }
-                    if (t > 0) cb = __fmaf_ru(float(t), meta[(uint32_t(t * a.K + ai[u][t]) << pl.lchunk) + c].y, cb);
-                }
-                // max|r| with NaN propagation: NaN/Inf in x or a centroid -> non-finite am
-                float mx = 0.f;
-#pragma unroll
-                for (int k = 0; k < 8; k++) mx = max3_nan_abs(mx, r[u][k].x, r[u][k].y);
-                nonfinite |= !(mx <= 3.402823466e38f) || !(cb <= 3.402823466e38f);
-                am[u] = mx;
-                eb[u] = S > 0 ? __fmaf_ru(float(S), mx, cb) : 0.f;
-            }
-            for (int m = 1; m < glanes; m <<= 1) {
-#pragma unroll
-                for (int u = 0; u < U; u++) {
-                    am[u] = fmaxf(am[u], __shfl_xor_sync(0xffffffffu, am[u], m));
-                    eb[u] = fmaxf(eb[u], __shfl_xor_sync(0xffffffffu, eb[u], m));
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                const bool valid = i0 + u * rpp + rslot < r1;
-                const float E = __fmul_ru(eb[u], 2.38418579e-7f);      // 2^-22
-                uint32_t code;
-                bool camb = false;
-                if (am[u] == 0.f && E == 0.f) code = 0x38u;
-                else {
-                    const float lo = __fsub_rd(am[u], E), hi = __fadd_ru(am[u], E);
-                    if (lo > 0.f) code = scale_code<QMAX>(lo, hi, camb);
-                    else { code = 0x38u; camb = true; }
-                }
-                camb &= valid;
-                const float *rf = reinterpret_cast<const float *>(r[u]);
-                auto exact_r = [&](int k) {
-                    return v6_exact_residual<XBF16, S>(xb, tab, ii[u] * d + col + k, off[k >> 2] + (k & 3), d,
-                                                       a.K, ai[u][0], ai[u][SS > 1 ? 1 : 0],
-                                                       ai[u][SS > 2 ? 2 : 0], ai[u][SS > 3 ? 3 : 0]);
-                };
-                if (__any_sync(0xffffffffu, camb)) {          // exact scale (rare)
-                    const float thr = __fsub_rd(am[u], __fmul_ru(E, 2.f));
-                    uint32_t cand = 0;
-#pragma unroll
-                    for (int k = 0; k < 16; k++) cand |= (camb && fabsf(rf[k]) >= thr) ? 1u << k : 0u;
-                    double a64 = 0.0;
-                    while (cand) {
-                        const int k = __ffs(cand) - 1;
-                        cand &= cand - 1;
-                        a64 = fmax(a64, fabs(exact_r(k)));
-                    }
-                    for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
-                    if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
-                }
-                const float s = e4m3_decode_fast(code);
-                const float inv = __frcp_rn(s);
-                const float2 inv2 = make_float2(inv, inv);
-                // codes: bits of fma(r, 1/s, MAGIC) = 0x4B400000 + q + 2^(b-1)
-                uint32_t acc[BITS / 2];
-#pragma unroll
-                for (int q = 0; q < BITS / 2; q++) acc[q] = 0u;
-                float2 yv[8];
-#pragma unroll
-                for (int k = 0; k < 8; k++) {
-                    yv[k] = __ffma2_rn(r[u][k], inv2, make_float2(MAGIC, MAGIC));
-                    const int k0 = 2 * k, k1 = 2 * k + 1;
-                    acc[k0 / FPW] += __float_as_uint(yv[k].x) << (BITS * (k0 % FPW));
-                    acc[k1 / FPW] += __float_as_uint(yv[k].y) << (BITS * (k1 % FPW));
-                }
-                uint32_t b32[BITS / 2];
-#pragma unroll
-                for (int q = 0; q < BITS / 2; q++) b32[q] = (acc[q] - v6_magic_sum<BITS>()) ^ SIGNS;
-                // ambiguity: an element whose exact code could differ.  The
-                // per-element predicate in_window(k) is evaluated once as a row
-                // reduction and again, identically, to pick the elements to fix.
-                const bool all = !(E < 0.125f * s) || code == 0x7Eu;    // loose bound / saturation: check all
-                float2 pa, pb;    // predicate constants
-                float thr;
-                if constexpr (QMAX == 1) {
-                    // ||r| - s/2| <= W  =>  |r^2 - (s/2)^2| <= W (s + W) (up to rounding),
-                    // W = E + the 1/s rounding of the decision
-                    const float h = 0.5f * s;
-                    const float W = __fmaf_ru(h, 2.38418579e-7f, E);
-                    thr = __fmul_ru(__fmul_ru(W, __fadd_ru(s, W)), 1.00000095367f);
-                    pa = make_float2(-h * h, -h * h);
-                    pb = pa;
-                } else {
-                    // |t - rint(t)| >= 1/2 - delta, t = r/s; delta covers E/s, the
-                    // 1/s rounding and the reference's float64 division
-                    const float delta = __fmaf_ru(__fmul_ru(E, inv), 1.0000002f, float(QMAX + 1) * 2.38418579e-7f);
-                    thr = __fsub_rd(0.5f, delta);
-                    pa = make_float2(-MAGIC, -MAGIC);
-                    pb = pa;
-                }
-                (void)pb;
-                auto window = [&](int k) -> float2 {     // |g| (2-bit) or |t - q| (b > 2) of pair k
-                    if constexpr (QMAX == 1) {
-                        const float2 g = __ffma2_rn(r[u][k], r[u][k], pa);
-                        return make_float2(fabsf(g.x), fabsf(g.y));
-                    } else {
-                        const float2 qf = __fadd2_rn(yv[k], pa);
-                        const float2 dist = __ffma2_rn(r[u][k], inv2, make_float2(-qf.x, -qf.y));
-                        return make_float2(fabsf(dist.x), fabsf(dist.y));
-                    }
-                };
-                bool amb;
-                if constexpr (QMAX == 1) {
-                    float gmin = __int_as_float(0x7F800000);
-#pragma unroll
-                    for (int k = 0; k < 8; k++) { const float2 g = window(k); gmin = fminf(gmin, fminf(g.x, g.y)); }
-                    amb = all || gmin <= thr;
-                } else {
-                    float dmax = 0.f;
-#pragma unroll
-                    for (int k = 0; k < 8; k++) { const float2 g = window(k); dmax = fmaxf(dmax, fmaxf(g.x, g.y)); }
-                    amb = all || dmax >= thr;
-                }
-                amb &= valid;
-                if (__any_sync(0xffffffffu, amb) && amb) {   // exact codes (rare)
-                    uint32_t todo = 0;
-#pragma unroll
-                    for (int k = 0; k < 8; k++) {
-                        const float2 g = window(k);
-                        bool in0, in1;
-                        if constexpr (QMAX == 1) { in0 = g.x <= thr; in1 = g.y <= thr; }
-                        else { in0 = g.x >= thr; in1 = g.y >= thr; }
-                        in0 |= all || !(fabsf(r[u][k].x) <= 3.402823466e38f);
-                        in1 |= all || !(fabsf(r[u][k].y) <= 3.402823466e38f);
-                        todo |= (in0 ? 1u << (2 * k) : 0u) | (in1 ? 2u << (2 * k) : 0u);
-                    }
-                    while (todo) {
-                        const int k = __ffs(todo) - 1;
-                        todo &= todo - 1;
-                        const uint32_t q = exact_code<QMAX>(exact_r(k), s) & ((1u << BITS) - 1u);
-                        const int sh = (k * BITS) & 31, wi = (k * BITS) >> 5;
-#pragma unroll
-                        for (int q2 = 0; q2 < BITS / 2; q2++)
-                            if (q2 == wi) b32[q2] = (b32[q2] & ~(((1u << BITS) - 1u) << sh)) | (q << sh);
-                    }
-                }
-                if (!valid) continue;
-                const uint32_t e0 = ii[u] * d + col;
-                uint8_t *plp = a.payload + uint64_t(p) * a.pb + ((e0 * BITS) >> 3);
-                if constexpr (BITS == 2) *reinterpret_cast<uint32_t *>(plp) = b32[0];
-                else if constexpr (BITS == 4) *reinterpret_cast<uint2 *>(plp) = make_uint2(b32[0], b32[1]);
-                else *reinterpret_cast<uint4 *>(plp) = make_uint4(b32[0], b32[1], b32[2], b32[3]);
-                if ((lane & (glanes - 1)) == 0) a.scales[uint64_t(p) * a.ng + (e0 >> a.lgB)] = uint8_t(code);
-            }
-        }
-    }
-    const uint32_t all = __reduce_or_sync(0xffffffffu, nonfinite ? uint32_t(QVG_STATUS_NONFINITE) : 0u);
-    if (all && lane == 0) atomicOr(a.status, int(all));
-}
-
-// ------------------------------------------------------------------------
-// v5w: the v5 quantize with ONE CTA per SM (32 warps by default) sharing
-// double-buffered f32 centroid tables (padded, conflict-free 16-channel
-// blocks) widened once per plane from a TMA-staged bf16 copy: the per-element
-// bf16 -> f32 conversions of the centroids disappear.  For bf16 inputs a
-// per-row exactness certificate (block {unit, max} metadata from the widen)
-// proves the f32 residual equals the reference's float64 one, which zeroes the
-// error bound: scale straddles at exact E4M3 grid hits vanish and exact ties
-// are resolved from registers instead of reloading x.
-// ------------------------------------------------------------------------
-struct V5W {
-    uint32_t P, tbytes, off_tab, tab_floats, pitch, nchunk, lchunk;
-    uint32_t nbuf;       // f32 table buffers (2, or 1 when two do not fit: one more barrier per plane)
-};
-__host__ __device__ __forceinline__ uint32_t v5w_blk(uint32_t c) { return 16u * c + 4u * (c >> 1); }
-// the 4-float pad after each block pair holds the pair's {unit, max |c|} metadata
-__host__ __device__ __forceinline__ uint32_t v5w_meta(uint32_t c) { return 36u * (c >> 1) + 32u + 2u * (c & 1u); }
-__device__ __forceinline__ void v5w_widen(const uint16_t *stg, float *tab, uint32_t nchunk, uint32_t lchunk,
-                                          uint32_t pitch) {
-    const uint32_t cmask = (1u << lchunk) - 1u;
-    for (uint32_t q = threadIdx.x; q < nchunk; q += blockDim.x) {
-        const uint4 *src = reinterpret_cast<const uint4 *>(stg + size_t(q) * 16);
-        float c[16];
-        cvt16(src[0], src[1], c);
-        float4 *dst = reinterpret_cast<float4 *>(tab + size_t(q >> lchunk) * pitch + v5w_blk(q & cmask));
-#pragma unroll
-        for (int jj = 0; jj < 4; jj++) dst[jj] = make_float4(c[4 * jj], c[4 * jj + 1], c[4 * jj + 2], c[4 * jj + 3]);
-        // {unit, max |c|}: unit = 2^(e-7), the ulp of a bf16 with the smallest
-        // non-zero magnitude's exponent (0 when that is not a normal float, +inf
-        // for an all-zero block); NaN/Inf make max non-finite
-        float mx = 0.f, mn = __int_as_float(0x7F800000);
-#pragma unroll
-        for (int k = 0; k < 16; k++) {
-            const float av = fabsf(c[k]);
-            mx = fmaxf(mx, av);
-            mn = av > 0.f ? fminf(mn, av) : mn;
-        }
-        float unit = mn;
-        if (mn != __int_as_float(0x7F800000)) {
-            const uint32_t eb = __float_as_uint(mn) & 0x7F800000u;
-            unit = eb > (7u << 23) ? __uint_as_float(eb - (7u << 23)) : 0.f;
-        }
-        *reinterpret_cast<float2 *>(tab + size_t(q >> lchunk) * pitch + v5w_meta(q & cmask)) = make_float2(unit, mx);
-    }
-}
-__device__ __forceinline__ void v5w_arrive(uint64_t *bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ float v5_min3_abs(float m, float a, float b) {
-    float t, d;
-    asm("min.f32 %0, %1, %2;" : "=f"(t) : "f"(fabsf(a)), "f"(fabsf(b)));
-    asm("min.f32 %0, %1, %2;" : "=f"(d) : "f"(m), "f"(t));
-    return d;
-}
-
-template <int BITS, int S, bool XBF16, int NT, int U, int C, bool PIPE = false>
-__global__ void __launch_bounds__(NT, 1) k_quantize_v5w(QuantArgs a, V5W pl) {
-    // PIPE (bf16, one 16-channel row per pass): the next pass's x and
-    // assignments are loaded into registers before this pass is processed
-    static_assert(!PIPE || (XBF16 && U == 1 && C == 16), "register pipeline: bf16 rows, U = 1, C = 16");
-    constexpr int QMAX = (1 << (BITS - 1)) - 1;
-    constexpr int SS = S > 0 ? S : 1;
-    extern __shared__ __align__(128) uint8_t smem[];
-    __shared__ uint64_t bar;
-    __shared__ uint64_t full[2], empty[2];  // f32 table buffer b: widened / released by every warp
-    __shared__ float rcp_tab[128];          // RN32(1 / e4m3(code))
-    uint16_t *const stg = reinterpret_cast<uint16_t *>(smem);
-    float *const tabs = reinterpret_cast<float *>(smem + pl.off_tab);
-    const uint32_t d = uint32_t(a.d), N = a.N;
-    // Two table buffers and no CTA-wide barrier per plane: plane j+1's table is
-    // widened half-way through plane j (after every warp released buffer
-    // (j+1)&1 at the end of plane j-1), so warps flow across plane boundaries.
-    const bool flow = S > 0 && pl.nbuf == 2;
-    // C = 16 or 32 channels per thread (one or two padded 16-channel blocks,
-    // contiguous in the table: v5w_blk(2c + 1) = v5w_blk(2c) + 16)
-    static_assert(C == 16 || C == 32, "channels per thread");
-    constexpr int NQ = C / 2, NW = BITS * C / 32;
-    constexpr uint32_t LC = C == 32 ? 1u : 0u;
-    const uint32_t lv = a.lvpr - LC;
-    const uint32_t cc = threadIdx.x & ((1u << lv) - 1u);
-    const int col = int(cc) * C;
-    const uint32_t coff = v5w_blk(cc << LC);
-    const uint32_t mdelta = C == 32 || !(cc & 1u) ? 32u : 18u;       // metadata, relative to coff
-    const uint32_t rslot = threadIdx.x >> lv, rpp = uint32_t(NT) >> lv;
-    const int glanes = 1 << (a.gshift - int(LC));
-    const int lane = threadIdx.x & 31;
-    bool nonfinite = false;
-    if (threadIdx.x < 128) rcp_tab[threadIdx.x] = __frcp_rn(e4m3_decode_fast(threadIdx.x));
-    if (threadIdx.x == 0) {
-        mbar_init(&bar, 1);
-        for (int b = 0; b < 2; b++) {
-            mbar_init(&full[b], NT);
-            mbar_init(&empty[b], NT / 32);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-    if (S > 0 && threadIdx.x == 0 && blockIdx.x < pl.P) stage_table(a.cent, blockIdx.x, pl.tbytes, stg, &bar);
-    if (flow && blockIdx.x < pl.P) {
-        mbar_wait(&bar, 0);
-        v5w_widen(stg, tabs, pl.nchunk, pl.lchunk, pl.pitch);
-        v5w_arrive(&full[0]);
-    }
-    const uint32_t mid = ((N + rpp * U - 1) / (rpp * U)) / 2;    // the pass that widens the next table
-    uint32_t j = 0;
-    for (uint32_t p = blockIdx.x; p < pl.P; p += gridDim.x, j++) {
-        float *const ct = tabs + (pl.nbuf == 2 ? (j & 1u) : 0u) * pl.tab_floats;
-        if (flow) {
-            mbar_wait(&full[j & 1u], (j >> 1) & 1u);             // every thread widened its share,
-            if (threadIdx.x == 0 && p + gridDim.x < pl.P) {      // so the staging copy is free
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                stage_table(a.cent, p + gridDim.x, pl.tbytes, stg, &bar);
-            }
-        } else if (S > 0) {
-            // widen plane p's staged bf16 table into f32 buffer j&1 (the buffer was last
-            // read two planes ago, before the previous plane's barrier), then restage
-            if (pl.nbuf == 1 && j > 0) __syncthreads();       // previous plane done with the only buffer
-            mbar_wait(&bar, j & 1u);
-            v5w_widen(stg, ct, pl.nchunk, pl.lchunk, pl.pitch);
-            __syncthreads();
-            if (threadIdx.x == 0 && p + gridDim.x < pl.P) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                stage_table(a.cent, p + gridDim.x, pl.tbytes, stg, &bar);
-            }
-        }
-        const uint64_t pN = uint64_t(p) * N;
-        const uint8_t *xb = static_cast<const uint8_t *>(a.x) + pN * d * (XBF16 ? 2 : 4);
-        const uint8_t *ap = a.asg + pN * S;
-        uint8_t *const pay = a.payload + uint64_t(p) * a.pb;     // this plane's code and scale bytes
-        uint8_t *const scl = a.scales + uint64_t(p) * a.ng;
-        uint4 nx0, nx1;
-        int na[SS];
-        auto fetch = [&](uint32_t i) {
-            i = i < N ? i : N - 1;
-            const uint4 *xp = reinterpret_cast<const uint4 *>(xb + (uint64_t(i) * d + col) * 2);
-            nx0 = __ldg(xp);
-            nx1 = __ldg(xp + 1);
-#pragma unroll
-            for (int t = 0; t < S; t++) na[t] = __ldg(ap + t * N + i);
-        };
-        if constexpr (PIPE) fetch(rslot);
-        uint32_t pass = 0;
-        for (uint32_t i0 = 0; i0 < N; i0 += rpp * U, pass++) {
-            if (flow && pass == mid && p + gridDim.x < pl.P) {
-                const uint32_t jn = j + 1;
-                if (jn >= 2) mbar_wait(&empty[jn & 1u], ((jn - 2) >> 1) & 1u);   // plane j-1 released
-                mbar_wait(&bar, jn & 1u);                                     // staged
-                v5w_widen(stg, tabs + (jn & 1u) * pl.tab_floats, pl.nchunk, pl.lchunk, pl.pitch);
-                v5w_arrive(&full[jn & 1u]);
-            }
-            float r[U][C];
-            uint32_t ii[U];
-            int ai[U][SS];
-            if constexpr (PIPE) {
-                const uint32_t i = i0 + rslot;
-                ii[0] = i < N ? i : N - 1;
-                cvt16(nx0, nx1, r[0]);
-#pragma unroll
-                for (int t = 0; t < S; t++) ai[0][t] = na[t];
-                if (i0 + rpp < N) fetch(i + rpp);
-            } else {
-#pragma unroll
-                for (int u = 0; u < U; u++) {
-                    const uint32_t i = i0 + u * rpp + rslot;
-                    ii[u] = i < N ? i : N - 1;
-                    load_x16<XBF16>(xb, ii[u] * d + col, r[u]);
-                    if constexpr (C == 32) load_x16<XBF16>(xb, ii[u] * d + col + 16, r[u] + 16);
-#pragma unroll
-                    for (int t = 0; t < S; t++) ai[u][t] = __ldg(ap + t * N + ii[u]);
-                }
-            }
-            float eb[U], am[U];
-            bool cert[U];
-            constexpr bool kCert = XBF16 && S > 0;
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                float2 *r2 = reinterpret_cast<float2 *>(r[u]);
-                // bf16 x: certificate that every partial sum x - c_1 - ... is exact in
-                // f32 (all operands multiples of a power of two `unit`, every partial
-                // magnitude < 2^24 unit; the bound uses |x| <= |r_S| + sum |c_t| with a
-                // 2x margin) -- then r IS the reference's float64 residual: E = 0
-                float xmn = __int_as_float(0x7F800000);
-                if constexpr (kCert) {
-#pragma unroll
-                    for (int q = 0; q < NQ; q++) xmn = v5_min3_abs(xmn, r2[q].x, r2[q].y);
-                }
-                float e = 0.f, csum = 0.f, cun = __int_as_float(0x7F800000);
-#pragma unroll
-                for (int t = 0; t < S; t++) {
-                    const uint32_t row = uint32_t(t * a.K + ai[u][t]);
-                    const float *cr = ct + row * pl.pitch + coff;
-                    const float4 *c4 = reinterpret_cast<const float4 *>(cr);
-#pragma unroll
-                    for (int q = 0; q < C / 4; q++) {
-                        const float4 cv = c4[q];
-                        r2[2 * q] = __fadd2_rn(r2[2 * q], make_float2(-cv.x, -cv.y));
-                        r2[2 * q + 1] = __fadd2_rn(r2[2 * q + 1], make_float2(-cv.z, -cv.w));
-                    }
-                    if constexpr (kCert) {
-                        if constexpr (C == 32) {
-                            const float4 m = *reinterpret_cast<const float4 *>(cr + mdelta);
-                            cun = fminf(cun, fminf(m.x, m.z));
-                            csum = __fadd_ru(csum, fmaxf(m.y, m.w));
-                        } else {
-                            const float2 m = *reinterpret_cast<const float2 *>(cr + mdelta);
-                            cun = fminf(cun, m.x);
-                            csum = __fadd_ru(csum, m.y);
-                        }
-                    } else if (t < S - 1) {
-                        // e = sum_{t<S} max_k |r_t,k| (+ max |r_S| below) bounds every
-                        // element's sum_t |r_t,k|, the error-bound input
-                        float m = 0.f;
-#pragma unroll
-                        for (int q = 0; q < NQ; q++) m = v5_max3_nan_abs(m, r2[q].x, r2[q].y);
-                        e = __fadd_ru(e, m);
-                    }
-                }
-                // the maxima propagate NaN: a NaN/Inf in x or a centroid is caught here
-                float mx = 0.f;
-#pragma unroll
-                for (int q = 0; q < NQ; q++) mx = v5_max3_nan_abs(mx, r2[q].x, r2[q].y);
-                if constexpr (kCert) {
-                    const uint32_t xe = __float_as_uint(xmn) & 0x7F800000u;
-                    const float unit = fminf(xe > (7u << 23) ? __uint_as_float(xe - (7u << 23)) : 0.f, cun);
-                    const float bnd = __fadd_ru(mx, __fmul_ru(csum, 2.f));
-                    cert[u] = bnd < unit * 8388608.f;
-                    // otherwise max |r_t| <= max |r_S| + sum_t' max |c_t'| for every t
-                    e = cert[u] ? 0.f : __fmul_ru(float(S), __fadd_ru(mx, csum));
-                    eb[u] = e;
-                } else {
-                    cert[u] = false;
-                    eb[u] = S > 0 ? __fadd_ru(e, mx) : 0.f;
-                }
-                nonfinite |= !(mx <= 3.402823466e38f) || (!kCert && !(e <= 3.402823466e38f));
-                am[u] = mx;
-            }
-            for (int m = 1; m < glanes; m <<= 1) {
-#pragma unroll
-                for (int u = 0; u < U; u++) {
-                    am[u] = fmaxf(am[u], __shfl_xor_sync(0xffffffffu, am[u], m));
-                    eb[u] = fmaxf(eb[u], __shfl_xor_sync(0xffffffffu, eb[u], m));
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; u++) {
-                const bool valid = i0 + u * rpp + rslot < N;
-                const float E = __fmul_ru(eb[u], 2.38418579e-7f);
-                uint32_t code;
-                bool camb = false;
-                if (am[u] == 0.f && E == 0.f) code = 0x38u;
-                else {
-                    const float lo = __fsub_rd(am[u], E), hi = __fadd_ru(am[u], E);
-                    if (lo > 0.f) code = scale_code<QMAX>(lo, hi, camb);
-                    else { code = 0x38u; camb = true; }
-                }
-                camb &= valid;
-                auto exact_r = [&](int k) {
-                    return v6_exact_residual<XBF16, S>(xb, ct, ii[u] * d + col + k, coff + k, pl.pitch, a.K, ai[u][0],
-                                                    ai[u][SS > 1 ? 1 : 0], ai[u][SS > 2 ? 2 : 0],
-                                                    ai[u][SS > 3 ? 3 : 0]);
-                };
-                if (__any_sync(0xffffffffu, camb)) {          // exact scale (rare)
-                    const float thr = __fsub_rd(am[u], __fmul_ru(E, 2.f));
-                    double a64 = 0.0;
-                    if (camb) {
-                        if (cert[u]) {                          // the row's own exact maximum
-                            float m = 0.f;
-#pragma unroll
-                            for (int k = 0; k < C; k++) m = fmaxf(m, fabsf(r[u][k]));
-                            a64 = double(m);
-                        }
-                        else {
-                            uint32_t cand = 0;
-#pragma unroll
-                            for (int k = 0; k < C; k++) cand |= fabsf(r[u][k]) >= thr ? 1u << k : 0u;
-                            while (cand) {
-                                const int k = __ffs(cand) - 1;
-                                cand &= cand - 1;
-                                a64 = fmax(a64, fabs(exact_r(k)));
-                            }
-                        }
-                    }
-                    for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
-                    if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
-                }
-                const float s = e4m3_decode_fast(code);
-                const float inv = rcp_tab[code & 0x7Fu];
-                const float2 inv2 = make_float2(inv, inv);
-                const float2 *r2 = reinterpret_cast<const float2 *>(r[u]);
-                // codes: the bits of fma(r, 1/s, 1.5*2^23 + 2^(b-1)) are 0x4B400000 + q + 2^(b-1);
-                // a multiply-add tree packs the fields (no carries: q + 2^(b-1) < 2^b)
-                constexpr float MAGIC = 12582912.f + float(1 << (BITS - 1));
-                constexpr int FPW = 32 / BITS;
-                constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
-                float2 yv[NQ];
-#pragma unroll
-                for (int q = 0; q < NQ; q++) yv[q] = __ffma2_rn(r2[q], inv2, make_float2(MAGIC, MAGIC));
-                uint32_t b32[NW];
-#pragma unroll
-                for (int wd = 0; wd < NW; wd++) {
-                    uint32_t v[FPW];
-#pragma unroll
-                    for (int k2 = 0; k2 < FPW; k2++) {
-                        const int e = wd * FPW + k2;
-                        v[k2] = __float_as_uint((e & 1) ? yv[e >> 1].y : yv[e >> 1].x);
-                    }
-#pragma unroll
-                    for (int span = 1; span < FPW; span *= 2)
-#pragma unroll
-                        for (int k2 = 0; k2 < FPW; k2 += 2 * span) v[k2] += v[k2 + span] << (BITS * span);
-                    b32[wd] = (v[0] - v5_magic_sum<BITS>()) ^ SIGNS;
-                }
-                // ambiguity: per-element window predicate (E plus the 1/s rounding),
-                // reduced over the row, re-evaluated identically for the fix-up
-                const bool all = !(E < 0.125f * s) || code == 0x7Eu;
-                float thr;
-                float2 pa;
-                if constexpr (QMAX == 1) {
-                    const float h = 0.5f * s;
-                    const float W = __fmaf_ru(h, 2.38418579e-7f, E);
-                    thr = __fmul_ru(__fmul_ru(W, __fadd_ru(s, W)), 1.00000095367f);
-                    pa = make_float2(-h * h, -h * h);
-                } else {
-                    const float delta = __fmaf_ru(__fmul_ru(E, inv), 1.0000002f, float(QMAX + 1) * 2.38418579e-7f);
-                    thr = __fsub_rd(0.5f, delta);
-                    pa = make_float2(-MAGIC, -MAGIC);
-                }
-                auto window = [&](int q) -> float2 {
-                    if constexpr (QMAX == 1) {
-                        const float2 gg = __ffma2_rn(r2[q], r2[q], pa);
-                        return make_float2(fabsf(gg.x), fabsf(gg.y));
-                    } else {
-                        const float2 qf = __fadd2_rn(yv[q], pa);
-                        const float2 dist = __ffma2_rn(r2[q], inv2, make_float2(-qf.x, -qf.y));
-                        return make_float2(fabsf(dist.x), fabsf(dist.y));
-                    }
-                };
-                bool amb;
-                {
-                    // two 3-input chains (min for the 2-bit distance to s/2, max for
-                    // the distance from the nearest integer)
-                    float w0 = QMAX == 1 ? __int_as_float(0x7F800000) : 0.f, w1 = w0;
-#pragma unroll
-                    for (int q = 0; q < NQ; q++) {
-                        const float2 w = window(q);
-                        float &acc = (q & 1) ? w1 : w0;
-                        acc = QMAX == 1 ? fminf(acc, fminf(w.x, w.y)) : fmaxf(acc, fmaxf(w.x, w.y));
-                    }
-                    const float wv = QMAX == 1 ? fminf(w0, w1) : fmaxf(w0, w1);
-                    amb = all || (QMAX == 1 ? wv <= thr : wv >= thr);
-                }
-                amb &= valid;
-                if (__any_sync(0xffffffffu, amb) && amb) {   // exact codes (rare)
-                    uint32_t todo = 0;
-#pragma unroll
-                    for (int q = 0; q < NQ; q++) {
-                        const float2 w = window(q);
-                        bool in0, in1;
-                        if constexpr (QMAX == 1) { in0 = w.x <= thr; in1 = w.y <= thr; }
-                        else { in0 = w.x >= thr; in1 = w.y >= thr; }
-                        in0 |= all || !(fabsf(r2[q].x) <= 3.402823466e38f);
-                        in1 |= all || !(fabsf(r2[q].y) <= 3.402823466e38f);
-                        todo |= (in0 ? 1u << (2 * q) : 0u) | (in1 ? 2u << (2 * q) : 0u);
-                    }
-                    if (cert[u]) {                             // r is exact: no reloads
-#pragma unroll
-                        for (int k = 0; k < C; k++) {
-                            if (!((todo >> k) & 1u)) continue;
-                            const uint32_t q = exact_code<QMAX>(double(r[u][k]), s) & ((1u << BITS) - 1u);
-                            const int sh = (k * BITS) & 31, wi = (k * BITS) >> 5;
-                            b32[wi] = (b32[wi] & ~(((1u << BITS) - 1u) << sh)) | (q << sh);
-                        }
-                    } else {
-                        while (todo) {
-                            const int k = __ffs(todo) - 1;
-                            todo &= todo - 1;
-                            const uint32_t q = exact_code<QMAX>(exact_r(k), s) & ((1u << BITS) - 1u);
-                            const int sh = (k * BITS) & 31, wi = (k * BITS) >> 5;
-#pragma unroll
-                            for (int q2 = 0; q2 < NW; q2++)
-                                if (q2 == wi) b32[q2] = (b32[q2] & ~(((1u << BITS) - 1u) << sh)) | (q << sh);
-                        }
-                    }
-                }
-                if (!valid) continue;
-                const uint32_t e0 = ii[u] * d + col;
-                uint8_t *plp = pay + ((e0 * BITS) >> 3);
-                if constexpr (NW == 1) *reinterpret_cast<uint32_t *>(plp) = b32[0];
-                else if constexpr (NW == 2) *reinterpret_cast<uint2 *>(plp) = make_uint2(b32[0], b32[1]);
-                else {
-#pragma unroll
-                    for (int w4 = 0; w4 < NW / 4; w4++)
-                        reinterpret_cast<uint4 *>(plp)[w4] = make_uint4(b32[4 * w4], b32[4 * w4 + 1], b32[4 * w4 + 2], b32[4 * w4 + 3]);
-                }
-                if ((lane & (glanes - 1)) == 0) scl[e0 >> a.lgB] = uint8_t(code);
-            }
-        }
-        if (flow) {                                               // done reading buffer j&1
-            __syncwarp();
-            if (lane == 0) v5w_arrive(&empty[j & 1u]);
-        }
-    }
-    const uint32_t all = __reduce_or_sync(0xffffffffu, nonfinite ? uint32_t(QVG_STATUS_NONFINITE) : 0u);
-    if (all && lane == 0) atomicOr(a.status, int(all));
-}
-
-// ------------------------------------------------------------------------
 // launchers
 // ------------------------------------------------------------------------
 static int grid_for(int64_t work, int block) {
@@ -1976,147 +735,16 @@ static int tile_grid(const TileArgs &t) {
     return int(t.n_tiles < 148u * 4u ? t.n_tiles : 148u * 4u);
 }
 
-// v5 (TMA-staged centroid tables) when two tables fit beside each other in
-// shared memory and there are enough planes to fill the GPU with CTAs.
-static int v5_ctas_per_sm(int64_t P, uint32_t tbytes, int S) {
-    if (S == 0 || tbytes % 16 != 0 || 2 * size_t(tbytes) > 200 * 1024) return 0;
-    int per_sm = int((224 * 1024) / (2 * size_t(tbytes) + 1024));
-    if (per_sm > 8) per_sm = 8;
-    if (per_sm < 1 || P < 2 * 148) return 0;
-    return per_sm;
-}
-
-
-// warp-specialised TMA streaming kernels (qvg_stream.cu); return 0 when the
-// configuration does not fit them
+// warp-specialised TMA ring kernels (qvg_stream.cu); return 0 when the
+// configuration does not fit them (S = 0, N % 4 != 0, misaligned buffers, tables
+// too large for shared memory) -- the tile kernels below take those
 int launch_quantize_stream(const QuantArgs &a, int64_t P, int bits, int S, bool xbf16, cudaStream_t st);
 int launch_dequantize_stream(const DequantArgs &a, int64_t P, int bits, int S, bool obf16, cudaStream_t st);
-// per-warp TMA rings (qvg_wring.cu)
-int launch_quantize_wring(const QuantArgs &a, int64_t P, int bits, int S, bool xbf16, cudaStream_t st);
-
-// QVG_CODEC_KERNEL=wring|stream|v6|v5|v4 restricts the fast-path choice (A/B
-// measurements); unset = best available
-static int codec_kernel_pref() {
-    static int pref = -1;
-    if (pref < 0) {
-        const char *e = getenv("QVG_CODEC_KERNEL");
-        pref = !e ? 0 : !strcmp(e, "v5w") ? 7 : !strcmp(e, "wring") ? 2 : !strcmp(e, "stream") ? 1 : !strcmp(e, "v6") ? 6 : !strcmp(e, "v5") ? 5 : !strcmp(e, "v4") ? 4 : 0;
-    }
-    return pref;
-}
-
-// v6 geometry: smem = staged bf16 table + f32 table + chunk metadata; work
-// items = planes split into row ranges so that every CTA has >= ~8 items
-struct V6Launch {
-    V6Plane pl;
-    size_t smem;
-    int grid;
-};
-static bool v6_plan(int64_t P, int64_t N, int d, int S, int K, V6Launch &L) {
-    if (S < 1 || d % 16 != 0 || N < 1) return false;
-    const size_t tbytes = size_t(S) * K * d * 2;
-    const size_t nchunk = size_t(S) * K * d / 16;
-    const size_t smem = 3 * tbytes + nchunk * 8;
-    if (smem > 200 * 1024) return false;
-    int per_sm = int((227 * 1024) / (smem + 2048));
-    if (per_sm > 2) per_sm = 2;                 // __launch_bounds__(256, 2)
-    const int64_t ctas = int64_t(148) * per_sm;
-    const int64_t rows_min = 512;               // keep the table widening amortised
-    int64_t ipp = 1;
-    while (P * ipp < 8 * ctas && N / (ipp * 2) >= rows_min) ipp *= 2;
-    const int64_t rpi = (N + ipp - 1) / ipp;
-    const int64_t n_items = P * ipp;
-    if (n_items >= (int64_t(1) << 31)) return false;
-    L.pl = V6Plane{uint32_t(P), uint32_t(tbytes), uint32_t(nchunk), uint32_t(ilog2(d / 16)), uint32_t(ipp),
-                   uint32_t(rpi), uint32_t(n_items)};
-    L.smem = smem;
-    L.grid = int(n_items < ctas ? n_items : ctas);
-    return true;
-}
-
-template <int BITS, int S>
-static bool launch_quant_v5w(const QuantArgs &a, bool xbf16, cudaStream_t st) {
-    const int n = a.d / 16;
-    if (n < 2 || (n & (n - 1)) || int64_t(a.P) < 148) return false;
-    const uint32_t pitch = uint32_t(16 * n + 4 * (n / 2));
-    const size_t tbytes = size_t(S) * a.K * a.d * 2;
-    const size_t off_tab = (tbytes + 127) & ~size_t(127);
-    const size_t tab_floats = size_t(S) * a.K * pitch;
-    const size_t nchunk = size_t(S) * a.K * n;
-    uint32_t nbuf = 2;
-    size_t smem = off_tab + 2 * tab_floats * 4;
-    if (smem > 220 * 1024) {
-        nbuf = 1;
-        smem = off_tab + tab_floats * 4;
-    }
-    if (smem > 220 * 1024) return false;
-    const V5W pl{a.P, uint32_t(tbytes), uint32_t(off_tab), uint32_t(tab_floats), pitch,
-                 uint32_t(nchunk), uint32_t(ilog2(n)), nbuf};
-    const int grid = int(a.P < 148u ? a.P : 148u);
-    static const int cfg = [] {
-        const char *e = getenv("QVG_V5W_CFG");
-        return e ? atoi(e) : 0;
-    }();
-#define V5W_GO(XB, NT, UU, CC, PP)                                                                        \
-    do {                                                                                                  \
-        cudaFuncSetAttribute(k_quantize_v5w<BITS, S, XB, NT, UU, CC, PP>,                                 \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));                     \
-        k_quantize_v5w<BITS, S, XB, NT, UU, CC, PP><<<grid, NT, smem, st>>>(a, pl);                       \
-    } while (0)
-    const bool c32 = a.lvpr >= 1 && a.gshift >= 1;      // d >= 32 and groups of >= 32 channels
-    // the loop is a long dependent chain: many warps of one row each, with the
-    // next row's loads in flight, issue best (measured 4.76 ms vs 4.87 for 32
-    // warps without the register pipeline and 4.97 for 24 warps x 2 rows).
-    // QVG_V5W_CFG=1: 24 warps x 2 rows, 2: 24 warps x 32 channels,
-    // 3: 32 warps x 1 row (measurement knobs)
-    if (xbf16) {
-        if (cfg == 1) V5W_GO(true, 768, 2, 16, false);
-        else if (cfg == 2 && c32) V5W_GO(true, 768, 1, 32, false);
-        else if (cfg == 3) V5W_GO(true, 1024, 1, 16, false);
-        else V5W_GO(true, 768, 1, 16, true);
-    } else {
-        V5W_GO(false, 768, 2, 16, false);
-    }
-#undef V5W_GO
-    return true;
-}
 
 template <int BITS, int S>
 static void launch_quant_fast(const QuantArgs &a, bool xbf16, cudaStream_t st) {
+    if (S > 0 && a.v16 && launch_quantize_stream(a, a.P, BITS, S, xbf16, st)) return;
     const int g = tile_grid(a.ta);
-    // quantize: the v5 kernel (bf16 tables, L1-resident rows in flight over 24
-    // warps/SM) is still the fastest measured for many planes (2.22 vs 2.12
-    // TB/s on the Self-Forcing cache); the per-warp-ring kernel serves the rest
-    const int pref = codec_kernel_pref();
-    // the warp-specialised ring kernel (qvg_stream.cu) first
-    if (S > 0 && a.v16 && (pref == 0 || pref == 1) && launch_quantize_stream(a, a.P, BITS, S, xbf16, st)) return;
-    if (S > 0 && a.v16 && (pref == 0 || pref == 7) && launch_quant_v5w<BITS, S>(a, xbf16, st)) return;
-    const bool v5_ok = a.v16 && a.v5 && (pref == 0 || pref == 5);
-    if (S > 0 && a.v16 && !v5_ok && (pref == 0 || pref == 2) && launch_quantize_wring(a, a.P, BITS, S, xbf16, st)) return;
-    V6Launch L;
-    if (S > 0 && a.v16 && !v5_ok && pref == 6 && v6_plan(a.P, a.N, a.d, S, a.K, L)) {
-        if (xbf16) {
-            cudaFuncSetAttribute(k_quantize_v6<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
-            k_quantize_v6<BITS, S, true><<<L.grid, 256, L.smem, st>>>(a, L.pl);
-        } else {
-            cudaFuncSetAttribute(k_quantize_v6<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
-            k_quantize_v6<BITS, S, false><<<L.grid, 256, L.smem, st>>>(a, L.pl);
-        }
-        return;
-    }
-    if (a.v16 && a.v5 && pref != 4) {
-        const PlaneLoop pl{a.P, uint32_t(S) * a.K * a.d * 2};
-        const size_t sm = 2 * size_t(pl.tbytes);
-        const int grid = int(int64_t(a.P) < int64_t(148) * a.v5 ? int64_t(a.P) : int64_t(148) * a.v5);
-        if (xbf16) {
-            cudaFuncSetAttribute(k_quantize_v5<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            k_quantize_v5<BITS, S, true><<<grid, 256, sm, st>>>(a, pl);
-        } else {
-            cudaFuncSetAttribute(k_quantize_v5<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            k_quantize_v5<BITS, S, false><<<grid, 256, sm, st>>>(a, pl);
-        }
-        return;
-    }
     if (a.v16) {
         if (xbf16) k_quantize_v4<BITS, S, true><<<g, 256, 0, st>>>(a);
         else k_quantize_v4<BITS, S, false><<<g, 256, 0, st>>>(a);
@@ -2148,8 +776,7 @@ int launch_quantize(const void *x, int xdtype, int64_t P, int64_t N, int d, int 
         QuantArgs a{x, cent, asg, payload, scales, uint32_t(N), d, K, B, lvpr,
                     v16 ? ilog2(B / 16) : ilog2(B / 8), status,
                     uint32_t(N * d * bits / 8), uint32_t(N * d / B), uint32_t(ilog2(B)),
-                    make_tiles(P, N, lvpr), v16 ? 1 : 0,
-                    v16 ? v5_ctas_per_sm(P, uint32_t(S) * K * d * 2, S) : 0, uint32_t(P), 1u};
+                    make_tiles(P, N, lvpr), v16 ? 1 : 0, uint32_t(P)};
         if (bits == 2) dispatch_quant_s<2>(a, S, xbf16, st);
         else if (bits == 4) dispatch_quant_s<4>(a, S, xbf16, st);
         else dispatch_quant_s<8>(a, S, xbf16, st);
@@ -2181,33 +808,8 @@ int launch_unpack(const uint8_t *in, int64_t n, int bits, int8_t *out, cudaStrea
 
 template <int BITS, int S>
 static void launch_deq_fast(const DequantArgs &a, bool obf16, cudaStream_t st) {
+    if (S > 0 && a.v16 && launch_dequantize_stream(a, a.P, BITS, S, obf16, st)) return;
     const int g = tile_grid(a.ta);
-    const int pref = codec_kernel_pref();
-    if (S > 0 && a.v16 && (pref <= 3) && launch_dequantize_stream(a, a.P, BITS, S, obf16, st)) return;
-    V6Launch L;
-    if (S > 0 && a.v16 && (pref <= 2 || pref == 6) && v6_plan(a.P, a.N, a.d, S, a.K, L)) {
-        if (obf16) {
-            cudaFuncSetAttribute(k_dequant_v6<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
-            k_dequant_v6<BITS, S, true><<<L.grid, 256, L.smem, st>>>(a, L.pl);
-        } else {
-            cudaFuncSetAttribute(k_dequant_v6<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(L.smem));
-            k_dequant_v6<BITS, S, false><<<L.grid, 256, L.smem, st>>>(a, L.pl);
-        }
-        return;
-    }
-    if (a.v16 && a.v5 && pref != 4) {
-        const PlaneLoop pl{a.P, uint32_t(S) * a.K * a.d * 2};
-        const size_t sm = 2 * size_t(pl.tbytes);
-        const int grid = int(int64_t(a.P) < int64_t(148) * a.v5 ? int64_t(a.P) : int64_t(148) * a.v5);
-        if (obf16) {
-            cudaFuncSetAttribute(k_dequant_v5<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            k_dequant_v5<BITS, S, true><<<grid, 256, sm, st>>>(a, pl);
-        } else {
-            cudaFuncSetAttribute(k_dequant_v5<BITS, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-            k_dequant_v5<BITS, S, false><<<grid, 256, sm, st>>>(a, pl);
-        }
-        return;
-    }
     if (a.v16) {
         if (obf16) k_dequant_v4<BITS, S, true><<<g, 256, 0, st>>>(a);
         else k_dequant_v4<BITS, S, false><<<g, 256, 0, st>>>(a);
@@ -2239,8 +841,7 @@ int launch_dequantize(const uint8_t *payload, const uint8_t *scales, const uint1
         const int lvpr = v16 ? ilog2(d / 16) : ilog2(vpr);
         DequantArgs a{payload, scales, cent, asg, out, uint32_t(N), d, K, B, lvpr, status,
                       uint32_t(N * d * bits / 8), uint32_t(N * d / B), uint32_t(ilog2(B)),
-                      make_tiles(P, N, lvpr), v16 ? 1 : 0,
-                      v16 ? v5_ctas_per_sm(P, uint32_t(S) * K * d * 2, S) : 0, uint32_t(P)};
+                      make_tiles(P, N, lvpr), v16 ? 1 : 0, uint32_t(P)};
         if (bits == 2) dispatch_deq_s<2>(a, S, obf16, st);
         else if (bits == 4) dispatch_deq_s<4>(a, S, obf16, st);
         else dispatch_deq_s<8>(a, S, obf16, st);

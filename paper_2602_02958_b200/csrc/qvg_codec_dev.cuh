@@ -158,10 +158,8 @@ struct QuantArgs {
     int32_t *status;
     uint32_t pb, ng, lgB;   // payload bytes / scale bytes per plane, log2(B)
     TileArgs ta;
-    int v16;                // 16 channels per thread (k_quantize_v4/v5)
-    int v5;                 // CTAs per SM for k_quantize_v5 (0: not used)
+    int v16;                // 16 channels per thread (k_quantize_v4, the ring kernel)
     uint32_t P;
-    uint32_t one;           // always 1 (see k_quantize_v5)
 };
 
 struct DequantArgs {
@@ -175,8 +173,7 @@ struct DequantArgs {
     int32_t *status;
     uint32_t pb, ng, lgB;
     TileArgs ta;
-    int v16;                // 16 channels per thread (k_dequant_v4/v5)
-    int v5;                 // CTAs per SM for k_dequant_v5 (0: not used)
+    int v16;                // 16 channels per thread (k_dequant_v4, the ring kernel)
     uint32_t P;
 };
 
@@ -261,9 +258,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
-struct PlaneLoop {
-    uint32_t P, tbytes;          // planes, centroid-table bytes per plane (S*K*d*2)
-};
+
 
 // issue the bulk copy of plane p's centroid table into buffer b
 __device__ __forceinline__ void stage_table(const uint16_t *cent, uint32_t p, uint32_t tbytes,

@@ -8,7 +8,7 @@ SURVEY §8(d) K/V parameters:
   assignments, float64 centroids, iterations, payload, scales and the f32
   reconstruction bit-exact against the oracle (Q/prq.py:58-80,113-132).
 * Self-Forcing compress of 456 C1-shaped planes (4680 x 128, S2 K64) in one
-  call: the final quantize takes the persistent v5w kernel with ~3 planes
+  call: the final quantize takes the ring kernel with ~3 planes
   per CTA and 49 row passes per plane, i.e. the mbarrier flow across plane
   boundaries (buffer reuse j >= 2, mid-plane widening) the bench exercises.
 * C5 N 65 536, K 256: the full k-means trajectory (k-means++ picks, every
@@ -122,7 +122,7 @@ def test_c5_full_trajectory_n65536_k256(oracle_lib):
 @pytest.mark.parametrize("P,N", [(4, 4680), (160, 1560)])
 def test_generic_f32_compress_vs_oracle(oracle_lib, P, N):
     """float32 planes that are not bf16-exact (the reference's KVPlane dtype,
-    Q/types.py:57-64): the uncertified residual paths and the float32 v5w."""
+    Q/types.py:57-64): the uncertified residual paths and the float32 ring kernel."""
     cfg = QuantConfig(bits=2, group_size=64, stages=2, centroids=64)
     refs = G.cache_layout(P // 24 or 1, 12, [1])[:P]
     x = _planes(refs, 12, N, drift=0.0125, bf16=False)

@@ -318,7 +318,7 @@ def test_compress_tiny_and_huge_scale_planes_vs_oracle(oracle_lib, scale_exp):
 
 @pytest.mark.parametrize("bits,B,S", [(2, 64, 2), (2, 16, 1), (4, 32, 3), (8, 64, 2), (2, 128, 4)])
 def test_many_planes_bf16_certificate_stress(oracle_lib, bits, B, S):
-    """>= 148 bf16 planes select the certified persistent quantize (v5w):
+    """>= 148 bf16 planes through the certified ring quantize (qvg_stream.cu):
     coarse dyadic inputs and centroids put residuals exactly on code
     boundaries and group maxima exactly on the E4M3 grid (exact ties resolved
     from registers), while zeros, subnormals and 1e-30 .. 1e4 magnitude mixes

@@ -9,7 +9,7 @@ set -u
     > /dev/null 2>&1
 # the bench-shape launches (time_codec first compresses 14 chunks of 720 planes)
 timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
-    -k regex:'k_quantize_v5w' --launch-skip 15 -c 1 -o /tmp/codec_q python tools/time_codec.py > /dev/null 2>&1
+    -k regex:'k_quantize_stream' --launch-skip 15 -c 1 -o /tmp/codec_q python tools/time_codec.py > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
     -k regex:'k_dequant_stream<.int.2, .int.2' --launch-skip 2 -c 1 -o /tmp/codec_d python tools/time_codec.py \
     > /dev/null 2>&1

@@ -12,9 +12,7 @@ TOOLS=${TOOLS:-"memcheck synccheck racecheck"}
 for tool in $TOOLS; do
     if [ $tool = memcheck ]; then   # compress under memcheck only at the 4-plane size
         run $tool default SAN_ONLY=compress,codec_q,attention,container
-        run $tool v5w QVG_CODEC_KERNEL=v5w SAN_ONLY=codec_q
     else
         run $tool default
-        run $tool v5w QVG_CODEC_KERNEL=v5w SAN_ONLY=codec
     fi
 done

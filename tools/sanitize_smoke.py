@@ -2,7 +2,7 @@
 (racecheck / synccheck / memcheck) runs:
     compute-sanitizer --tool racecheck python tools/sanitize_smoke.py
 Shapes are small but take the same code paths as the bench: the persistent
-ring quantize (>= 148 planes), the stream dequantize, v5w (QVG_CODEC_KERNEL=v5w),
+ring quantize (>= 148 planes), the stream dequantize,
 k-means++ / tensor-core assignment / Lloyd inside compress, attention (TMA,
 tcgen05), container record pack/unpack."""
 import os
