@@ -329,6 +329,355 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_stream(QuantArgs 
 }
 
 // ============================================================================
+// K5 quantize, 32 channels per thread (d = 128 / 256, groups of >= 32)
+// ============================================================================
+// Same pipeline and numerics as k_quantize_stream; a thread owns a 32-channel
+// slice of a row, so the per-row work (certificate, group interval, scale code,
+// window thresholds, stores) is amortised over twice the elements and a
+// 64-channel group spans two lanes (one shuffle round).
+// Bank-conflict-free table reads: slices are stored as 36 floats (8 blocks of
+// 4 + {unit, max |c|} + 2 spare) and table rows padded to a multiple of 32
+// floats, so the 4 slices of one table row sit on bank quads 0..3 (+ block).
+// With d = 128 a quarter-warp holds two rows (rho = 0, 1) reading unrelated
+// table rows; the rho = 1 row reads its slice's upper half first (blocks 4-7,
+// then 0-3), which puts the two rows on disjoint quads.  Its registers hold
+// the slice half-rotated, so x is loaded with the same rotation and the two
+// halves of the packed codes are swapped back at the store.
+// A stage is released to the producer as soon as its bytes are in registers
+// (the rare exact paths re-read x from global memory), so the whole ring stays
+// in flight.
+__device__ __forceinline__ void widen32(const uint16_t *src, float *tab, const Geo &g, uint32_t nthr) {
+    const uint32_t ns = g.d / 32, nslice = g.tbytes / 64;          // 32-channel slices of all tables
+    for (uint32_t q = threadIdx.x; q < nslice; q += nthr) {
+        const uint4 *sp = reinterpret_cast<const uint4 *>(src + size_t(q) * 32);
+        float c[32];
+        cvt16(sp[0], sp[1], c);
+        cvt16(sp[2], sp[3], c + 16);
+        float mx = 0.f, mn = __int_as_float(0x7F800000);
+#pragma unroll
+        for (int k = 0; k < 32; k++) {
+            const float a = fabsf(c[k]);
+            mx = max_nan(mx, a);
+            mn = a > 0.f ? fminf(mn, a) : mn;
+        }
+        float *dst = tab + size_t(q / ns) * g.pitch + 36u * (q % ns);
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            reinterpret_cast<float4 *>(dst)[j] = make_float4(c[4 * j], c[4 * j + 1], c[4 * j + 2], c[4 * j + 3]);
+        float unit;
+        if (mn == __int_as_float(0x7F800000)) unit = mn;
+        else {
+            const uint32_t eb = __float_as_uint(mn) & 0x7F800000u;
+            unit = eb > (7u << 23) ? __uint_as_float(eb - (7u << 23)) : 0.f;
+        }
+        *reinterpret_cast<float2 *>(dst + 32) = make_float2(unit, mx);
+    }
+}
+
+template <int BITS, int S, bool XBF16, int CW>
+__global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs a, Geo g) {
+    constexpr int QMAX = (1 << (BITS - 1)) - 1;
+    constexpr int SS = S > 0 ? S : 1;
+    constexpr int FPW = 32 / BITS;
+    constexpr uint32_t SIGNS = BITS == 2 ? 0xAAAAAAAAu : (BITS == 4 ? 0x88888888u : 0x80808080u);
+    constexpr float MAGIC = 12582912.f + float(1 << (BITS - 1));
+    constexpr uint32_t XB = XBF16 ? 2 : 4;
+    constexpr int NWD = BITS;               // 32-bit code words per 32 fields
+    extern __shared__ __align__(1024) uint8_t smem[];
+    __shared__ Bars bars;
+    uint16_t *const stg = reinterpret_cast<uint16_t *>(smem);
+    float *const tab = reinterpret_cast<float *>(smem + g.off_tab);
+    uint8_t *const ring = smem + g.off_ring;
+    __shared__ float rcp_tab[128];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t d = g.d, N = g.N;
+
+    if (threadIdx.x < 128)
+        rcp_tab[threadIdx.x] = QMAX == 1 ? __frcp_rd(e4m3_decode_fast(threadIdx.x)) : __frcp_rn(e4m3_decode_fast(threadIdx.x));
+    if (threadIdx.x == 0) {
+        for (uint32_t k = 0; k < g.nst; k++) {
+            mbar_init(&bars.full[k], 1 + 32);
+            mbar_init(&bars.empty[k], CW);
+        }
+        mbar_init(&bars.tab, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    Sched sc;
+    sc.init(g);
+
+    if (warp == CW) {
+        // ---------------- producer ----------------
+        uint32_t s = 0, k = 0, ph = 0;
+        for (; sc.valid(); sc.next(g), s++, k = k + 1 == g.nst ? (ph ^= 1u, 0u) : k + 1) {
+            if (s >= g.nst) mbar_wait(&bars.empty[k], ph ^ 1u);
+            const uint32_t nr = min(g.R, sc.r1 - sc.i0);
+            uint8_t *st = ring + k * g.stage_bytes;
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&bars.full[k], nr * g.big_row);
+                bulk_g2s_cta(st, static_cast<const uint8_t *>(a.x) + (uint64_t(sc.p) * N + sc.i0) * g.big_row,
+                             nr * g.big_row, &bars.full[k]);
+            }
+            const uint32_t nw = nr >> 2;
+#pragma unroll
+            for (int t = 0; t < S; t++)
+                for (uint32_t q = lane; q < nw; q += 32)
+                    cp_async4(st + g.off_small + t * g.R + 4 * q,
+                              a.asg + (uint64_t(sc.p) * S + t) * N + sc.i0 + 4 * q);
+            cp_async_arrive_noinc(&bars.full[k]);
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    const uint32_t lt = g.lchunk;                       // log2(threads per row) = log2(d / 32)
+    const uint32_t c = threadIdx.x & ((1u << lt) - 1u);
+    const uint32_t rho = d == 128 ? (uint32_t(lane) >> 2) & 1u : 0u;
+    const uint32_t rslot = threadIdx.x >> lt;
+    const uint32_t soff = 36u * c;                      // this thread's slice in a table row
+    const uint32_t hlo = 16u * rho, hhi = 16u * (rho ^ 1u);   // slot halves -> channel halves
+    const int glanes = 1 << (a.gshift - 1);             // B / 32 lanes per group
+    const bool slead = (uint32_t(lane) & uint32_t(glanes - 1)) == 0;
+    const uint32_t pitch = g.pitch, KK = g.K, big_row = g.big_row;
+    bool nonfinite = false;
+    uint32_t cur = 0xFFFFFFFFu, jp = 0, k = 0, ph = 0;
+    uint8_t *pay = a.payload, *scl = a.scales;
+    if (!g.stg_global && threadIdx.x == 0 && sc.valid()) stage_table(a.cent, sc.p, g.tbytes, stg, &bars.tab);
+    for (; sc.valid(); sc.next(g), k = k + 1 == g.nst ? (ph ^= 1u, 0u) : k + 1) {
+        const uint32_t p = sc.p;
+        if (p != cur) {
+            named_sync_consumers<CW>();
+            if (!g.stg_global) mbar_wait(&bars.tab, jp & 1u);
+            widen32(g.stg_global ? a.cent + size_t(p) * (g.tbytes / 2) : stg, tab, g, CW * 32);
+            named_sync_consumers<CW>();
+            if (!g.stg_global && threadIdx.x == 0) {
+                const int64_t nx = sc.next_plane(g);
+                if (nx >= 0) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    stage_table(a.cent, uint32_t(nx), g.tbytes, stg, &bars.tab);
+                }
+            }
+            jp++;
+            pay = a.payload + uint64_t(p) * a.pb;
+            scl = a.scales + uint64_t(p) * a.ng;
+            cur = p;
+        }
+        mbar_wait(&bars.full[k], ph);
+        if (g.dbg == 1) {                      // measurement: consumers only drain the ring
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bars.empty[k]);
+            continue;
+        }
+        const uint8_t *st = ring + k * g.stage_bytes;
+        const uint32_t nr = min(g.R, sc.r1 - sc.i0);
+        const uint32_t l = rslot;
+        const bool valid = l < nr;
+        const uint32_t lr = valid ? l : nr - 1;
+        const uint8_t *xr = st + lr * big_row + 32u * c * XB;     // the slice's x (ring, then global)
+        float2 r[16];
+        float xmn = __int_as_float(0x7F800000);
+        {
+            const uint8_t *xa = xr + hlo * XB, *xb = xr + hhi * XB;   // slot halves (rotated for rho = 1)
+            if constexpr (XBF16) {
+                cvt16(*reinterpret_cast<const uint4 *>(xa), *reinterpret_cast<const uint4 *>(xa + 16),
+                      reinterpret_cast<float *>(r));
+                cvt16(*reinterpret_cast<const uint4 *>(xb), *reinterpret_cast<const uint4 *>(xb + 16),
+                      reinterpret_cast<float *>(r + 8));
+                float m0 = xmn, m1 = xmn;
+#pragma unroll
+                for (int q = 0; q < 16; q += 2) {
+                    m0 = min3_abs(m0, r[q].x, r[q].y);
+                    m1 = min3_abs(m1, r[q + 1].x, r[q + 1].y);
+                }
+                xmn = fminf(m0, m1);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const float4 v = *reinterpret_cast<const float4 *>(xa + 16 * j);
+                    const float4 w = *reinterpret_cast<const float4 *>(xb + 16 * j);
+                    r[2 * j] = make_float2(v.x, v.y);
+                    r[2 * j + 1] = make_float2(v.z, v.w);
+                    r[8 + 2 * j] = make_float2(w.x, w.y);
+                    r[8 + 2 * j + 1] = make_float2(w.z, w.w);
+                }
+            }
+        }
+        int ai[SS];
+#pragma unroll
+        for (int t = 0; t < S; t++) ai[t] = st[g.off_small + t * g.R + lr];
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.empty[k]);
+        xr = static_cast<const uint8_t *>(a.x) + (uint64_t(p) * N + sc.i0 + lr) * big_row + 32u * c * XB;
+        float csum = 0.f, cunit = __int_as_float(0x7F800000);
+#pragma unroll
+        for (int t = 0; t < S; t++) {
+            const float *cr = tab + uint32_t(t * int(KK) + ai[t]) * pitch + soff;
+            const float *ca = cr + hlo, *cb = cr + hhi;
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const float4 u = *reinterpret_cast<const float4 *>(ca + 4 * j);
+                r[2 * j] = __fadd2_rn(r[2 * j], make_float2(-u.x, -u.y));
+                r[2 * j + 1] = __fadd2_rn(r[2 * j + 1], make_float2(-u.z, -u.w));
+            }
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const float4 u = *reinterpret_cast<const float4 *>(cb + 4 * j);
+                r[8 + 2 * j] = __fadd2_rn(r[8 + 2 * j], make_float2(-u.x, -u.y));
+                r[8 + 2 * j + 1] = __fadd2_rn(r[8 + 2 * j + 1], make_float2(-u.z, -u.w));
+            }
+            const float2 m = *reinterpret_cast<const float2 *>(cr + 32);
+            csum = __fadd_ru(csum, m.y);
+            cunit = fminf(cunit, m.x);
+        }
+        float m0 = 0.f, m1 = 0.f;
+#pragma unroll
+        for (int q = 0; q < 16; q += 2) {
+            m0 = max3_nan_abs(m0, r[q].x, r[q].y);
+            m1 = max3_nan_abs(m1, r[q + 1].x, r[q + 1].y);
+        }
+        const float mx = max_nan(m0, m1);
+        nonfinite |= !(mx <= 3.402823466e38f) && valid;
+        const uint32_t xe = __float_as_uint(xmn) & 0x7F800000u;
+        const float un = fminf(xe > (7u << 23) ? __uint_as_float(xe - (7u << 23)) : 0.f, cunit);
+        const bool cert = XBF16 && __fmaf_ru(2.f, csum, mx) < un * 8388608.f;
+        const float El = cert ? 0.f : __fmul_ru(__fmul_ru(float(S), __fadd_ru(mx, csum)), 2.38418579e-7f);
+        float lo = __fsub_rd(mx, El), hi = __fadd_ru(mx, El);
+        for (int m = 1; m < glanes; m <<= 1) {
+            lo = fmaxf(lo, __shfl_xor_sync(0xffffffffu, lo, m));
+            hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, m));
+        }
+        bool cb = false;
+        uint32_t code;
+        if constexpr (QMAX == 1) {
+            const float hc = fminf(hi, 448.f);
+            const uint32_t t = (__float_as_uint(hc) + 0xFFFFFu) & 0xFFF00000u;
+            if (hc >= 0.015625f) {
+                code = (t >> 20) - (120u << 3);
+                cb = !(lo > __uint_as_float(t - 0x100000u));
+            } else {
+                code = e4m3_ceil_f32_bf(hi);
+                cb = !(lo > e4m3_decode_fast(code - 1u));
+            }
+        } else {
+            code = scale_code<QMAX>(lo > 0.f ? lo : hi, hi, cb);
+        }
+        const bool zero = hi == 0.f;
+        if (zero || !(lo > 0.f)) code = 0x38u;
+        const bool camb = valid && !zero && (cb || !(lo > 0.f));
+        if (__any_sync(0xffffffffu, camb)) {                    // exact scale (rare)
+            double a64 = 0.0;
+            if (camb) {
+                const float thr = __fsub_rd(lo, El);
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                    uint32_t cand = 0;
+#pragma unroll
+                    for (int q = 0; q < 8; q++)
+                        cand |= (fabsf(r[8 * h + q].x) >= thr ? 1u << (2 * q) : 0u) |
+                                (fabsf(r[8 * h + q].y) >= thr ? 2u << (2 * q) : 0u);
+                    const uint32_t hc = h == 0 ? hlo : hhi;
+                    if (cand)
+                        a64 = fmax(a64, exact_absmax<S, XBF16>(xr + hc * XB, tab, pitch, soff + hc, int(KK), ai[0],
+                                                               ai[SS > 1 ? 1 : 0], ai[SS > 2 ? 2 : 0],
+                                                               ai[SS > 3 ? 3 : 0], cand));
+                }
+            }
+            for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
+            if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
+        }
+        // ---- codes (slot order), fixed up per 16-field half, stored in channel order
+        const float sv = e4m3_decode_fast(code);
+        const float inv = rcp_tab[code & 0x7Fu];
+        const float2 inv2 = make_float2(inv, inv);
+        uint32_t w[NWD];
+#pragma unroll
+        for (int wd = 0; wd < NWD; wd++) {
+            uint32_t v[FPW];
+#pragma unroll
+            for (int k2 = 0; k2 < FPW; k2++) {
+                const int e = wd * FPW + k2;
+                const float2 y = __ffma2_rn(r[e >> 1], inv2, make_float2(MAGIC, MAGIC));
+                v[k2] = __float_as_uint((e & 1) ? y.y : y.x);
+            }
+#pragma unroll
+            for (int span = 1; span < FPW; span *= 2)
+#pragma unroll
+                for (int k2 = 0; k2 < FPW; k2 += 2 * span) v[k2] += v[k2 + span] << (BITS * span);
+            w[wd] = (v[0] - magic_sum<BITS>()) ^ SIGNS;
+        }
+        const bool allv = !(El < 0.125f * sv) || code == 0x7Eu;
+        const float thr = window_thr<QMAX>(sv, inv, El);
+        bool amb;
+        if constexpr (QMAX == 1) {
+            const float sexp = __uint_as_float(__float_as_uint(sv) & 0x7F800000u);
+            const bool fast = cert && code != 0x7Eu && sexp * 0.0625f >= un && sv < un * 4194304.f;
+            amb = false;
+            if (__any_sync(0xffffffffu, !fast)) {
+                const float h = 0.5f * sv;
+                const float2 pa = make_float2(-h * h, -h * h);
+                float w0 = __int_as_float(0x7F800000), w1 = w0;
+#pragma unroll
+                for (int q = 0; q < 16; q += 2) {
+                    const float2 g0 = __ffma2_rn(r[q], r[q], pa);
+                    const float2 g1 = __ffma2_rn(r[q + 1], r[q + 1], pa);
+                    w0 = min3_abs(w0, g0.x, g0.y);
+                    w1 = min3_abs(w1, g1.x, g1.y);
+                }
+                amb = !fast && (allv || fminf(w0, w1) <= thr);
+            }
+        } else {
+            const float2 pa = make_float2(-MAGIC, -MAGIC);
+            float w0 = 0.f, w1 = 0.f;
+#pragma unroll
+            for (int q = 0; q < 16; q += 2) {
+                const float2 y0 = __ffma2_rn(r[q], inv2, make_float2(MAGIC, MAGIC));
+                const float2 y1 = __ffma2_rn(r[q + 1], inv2, make_float2(MAGIC, MAGIC));
+                const float2 q0 = __fadd2_rn(y0, pa), q1 = __fadd2_rn(y1, pa);
+                const float2 d0 = __ffma2_rn(r[q], inv2, make_float2(-q0.x, -q0.y));
+                const float2 d1 = __ffma2_rn(r[q + 1], inv2, make_float2(-q1.x, -q1.y));
+                w0 = max3_abs(w0, d0.x, d0.y);
+                w1 = max3_abs(w1, d1.x, d1.y);
+            }
+            amb = allv || fmaxf(w0, w1) >= thr;
+        }
+        if (amb && valid) {                                     // exact codes (rare), per half
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const uint32_t hc = h == 0 ? hlo : hhi;
+                Words4 b;
+#pragma unroll
+                for (int wd = 0; wd < NWD / 2; wd++) b.w[wd] = w[h * (NWD / 2) + wd];
+                b = fix_codes<BITS, S, XBF16>(xr + hc * XB, tab, pitch, soff + hc, int(KK), ai[0],
+                                              ai[SS > 1 ? 1 : 0], ai[SS > 2 ? 2 : 0], ai[SS > 3 ? 3 : 0], sv,
+                                              inv, El, thr, allv, b);
+#pragma unroll
+                for (int wd = 0; wd < NWD / 2; wd++) w[h * (NWD / 2) + wd] = b.w[wd];
+            }
+        }
+        if (valid) {
+            // slot halves back to channel order (rho = 1 holds the upper half first)
+            uint32_t o[NWD];
+#pragma unroll
+            for (int wd = 0; wd < NWD; wd++) {
+                const int sw = (wd + NWD / 2) % NWD;
+                o[wd] = rho ? w[sw] : w[wd];
+            }
+            const uint32_t e0 = (sc.i0 + lr) * d + 32u * c;
+            uint8_t *plp = pay + ((e0 * BITS) >> 3);
+            if constexpr (NWD == 2) *reinterpret_cast<uint2 *>(plp) = make_uint2(o[0], o[1]);
+            else {
+#pragma unroll
+                for (int q4 = 0; q4 < NWD / 4; q4++)
+                    reinterpret_cast<uint4 *>(plp)[q4] = make_uint4(o[4 * q4], o[4 * q4 + 1], o[4 * q4 + 2], o[4 * q4 + 3]);
+            }
+            if (slead) scl[e0 >> a.lgB] = uint8_t(code);
+        }
+    }
+    const uint32_t all = __reduce_or_sync(0xffffffffu, nonfinite ? uint32_t(QVG_STATUS_NONFINITE) : 0u);
+    if (all && lane == 0) atomicOr(a.status, int(all));
+}
+
+// ============================================================================
 // K6 dequantize
 // ============================================================================
 template <int BITS, int S, bool OBF16>
@@ -596,17 +945,21 @@ static int ilog2i(int v) { int l = 0; while ((1 << l) < v) l++; return l; }
 // smem: [bf16 staging][f32 padded tables][metadata][ring]; false when the
 // configuration does not fit this kernel (callers fall back to v4/v5/v6)
 static bool plan(bool quant, int64_t P, int64_t N, int d, int S, int K, int bits, int B, int xbytes,
-                 uintptr_t align_probe, Geo &g, size_t &smem, int &grid, int cw = kCW, int ru = kU) {
+                 uintptr_t align_probe, Geo &g, size_t &smem, int &grid, int cw = kCW, int ru = kU,
+                 bool c32 = false) {
     if (S < 1 || S > 4 || d % 16 != 0 || d > 512 || N < 4 || N % 4 != 0) return false;
     const int n = d / 16;
     if (n & (n - 1)) return false;
     if ((align_probe & 3u) != 0) return false;
     if (P * N >= (int64_t(1) << 31) || N * d >= (int64_t(1) << 31)) return false;
-    const uint32_t R = uint32_t(cw * 32 / n * ru);
-    const uint32_t pitch = uint32_t(16 * n + 4 * ((n + 1) / 2));
+    if (c32 && (d != 128 && d != 256)) return false;
+    // c32: 32-channel slices of 36 floats (the 4-float pad holds the slice's
+    // {unit, max |c|}), rows padded to a multiple of 32 floats (see k_quantize_ring32)
+    const uint32_t R = uint32_t(cw * 32 / (c32 ? d / 32 : n) * ru);
+    const uint32_t pitch = c32 ? uint32_t((36 * (d / 32) + 31) / 32 * 32) : uint32_t(16 * n + 4 * ((n + 1) / 2));
     const size_t tbytes = size_t(S) * K * d * 2;
     const size_t tabb = size_t(S) * K * pitch * 4;
-    const size_t nchunk = size_t(S) * K * n;
+    const size_t nchunk = c32 ? 0 : size_t(S) * K * n;
     size_t off_tab = (tbytes + 127) & ~size_t(127);
     size_t off_meta = off_tab + ((tabb + 127) & ~size_t(127));
     size_t off_ring = off_meta + ((nchunk * 8 + 1023) & ~size_t(1023));
@@ -625,7 +978,9 @@ static bool plan(bool quant, int64_t P, int64_t N, int d, int S, int K, int bits
     const size_t small = size_t(R) * small_row + size_t(S) * R;
     const size_t stage = (big + ((small + 15) & ~size_t(15)) + 127) & ~size_t(127);
     const size_t budget = 227 * 1024 - 1024;
-    if (off_ring + 2 * stage > budget) {
+    // c32 widens straight from global memory (L2-resident tables): the staging
+    // copy's 32 KB buys one more ring stage (4 vs 3: 4.47 vs 4.58 ms)
+    if (off_ring + 2 * stage > budget || (quant && c32)) {
         // no room for the bf16 staging copy: widen straight from global memory
         stg_global = 1;
         off_tab = 0;
@@ -644,7 +999,7 @@ static bool plan(bool quant, int64_t P, int64_t N, int d, int S, int K, int bits
     rpi = (rpi + R - 1) / R * R;
     ipp = (N + rpi - 1) / rpi;
     g = Geo{uint32_t(P), uint32_t(N), uint32_t(d), uint32_t(K), R, nst, pitch, uint32_t(tbytes),
-            uint32_t(nchunk), uint32_t(ilog2i(n)), uint32_t(ipp), uint32_t(rpi), uint32_t(P * ipp),
+            uint32_t(nchunk), uint32_t(ilog2i(c32 ? d / 32 : n)), uint32_t(ipp), uint32_t(rpi), uint32_t(P * ipp),
             uint32_t(off_tab), uint32_t(off_meta), uint32_t(off_ring), uint32_t(stage), big_row, small_row,
             uint32_t(big), 0u, stg_global};
     if (const char *e = getenv("QVG_STREAM_DBG")) g.dbg = uint32_t(atoi(e));
@@ -671,6 +1026,18 @@ static int launch_q(const QuantArgs &a, bool xbf16, const Geo &g, size_t smem, i
 }
 
 template <int BITS, int S>
+static int launch_q32(const QuantArgs &a, bool xbf16, const Geo &g, size_t smem, int grid, cudaStream_t st) {
+    if (xbf16) {
+        cudaFuncSetAttribute(k_quantize_ring32<BITS, S, true, kCW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_quantize_ring32<BITS, S, true, kCW><<<grid, 32 * (kCW + 1), smem, st>>>(a, g);
+    } else {
+        cudaFuncSetAttribute(k_quantize_ring32<BITS, S, false, kCW>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        k_quantize_ring32<BITS, S, false, kCW><<<grid, 32 * (kCW + 1), smem, st>>>(a, g);
+    }
+    return 1;
+}
+
+template <int BITS, int S>
 static int launch_d(const DequantArgs &a, bool obf16, const Geo &g, size_t smem, int grid, cudaStream_t st) {
     if (obf16) {
         cudaFuncSetAttribute(k_dequant_stream<BITS, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
@@ -692,6 +1059,22 @@ int launch_quantize_stream(const QuantArgs &a, int64_t P, int bits, int S, bool 
     size_t smem;
     int grid;
     const uintptr_t probe = reinterpret_cast<uintptr_t>(a.asg) | reinterpret_cast<uintptr_t>(a.x);
+    // 32 channels per thread when rows are 128 / 256 channels and groups >= 32
+    static const bool no32 = [] { const char *e = getenv("QVG_QUANT_C16"); return e && atoi(e) == 1; }();
+    if (!no32 && a.B % 32 == 0 &&
+        plan(true, P, a.N, a.d, S, a.K, bits, a.B, xbf16 ? 2 : 4, probe, g, smem, grid, kCW, 1, true)) {
+#define QV_Q32(BB)                                                          \
+        switch (S) {                                                        \
+            case 1: return launch_q32<BB, 1>(a, xbf16, g, smem, grid, st); \
+            case 2: return launch_q32<BB, 2>(a, xbf16, g, smem, grid, st); \
+            case 3: return launch_q32<BB, 3>(a, xbf16, g, smem, grid, st); \
+            default: return launch_q32<BB, 4>(a, xbf16, g, smem, grid, st); \
+        }
+        if (bits == 2) { QV_Q32(2) }
+        if (bits == 4) { QV_Q32(4) }
+        QV_Q32(8)
+#undef QV_Q32
+    }
     if (!plan(true, P, a.N, a.d, S, a.K, bits, a.B, xbf16 ? 2 : 4, probe, g, smem, grid)) return 0;
     if ((reinterpret_cast<uintptr_t>(a.x) & 15u) != 0) return 0;
 #define QV_Q(BB)                                                      \
