@@ -389,6 +389,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
     float *const tab = reinterpret_cast<float *>(smem + g.off_tab);
     uint8_t *const ring = smem + g.off_ring;
     __shared__ float rcp_tab[128];
+    __shared__ uint32_t rcp_sink[CW];       // release-ordering stores (see below)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t d = g.d, N = g.N;
 
@@ -505,6 +506,18 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
         int ai[SS];
 #pragma unroll
         for (int t = 0; t < S; t++) ai[t] = st[g.off_small + t * g.R + lr];
+        // every shared-memory load of the stage must have landed before the
+        // release (the producer's TMA may overwrite the stage right after it):
+        // a store of a value depending on one register of each load cannot
+        // issue before those loads complete
+        {
+            uint32_t dep = 0;
+#pragma unroll
+            for (int t = 0; t < S; t++) dep ^= uint32_t(ai[t]);
+#pragma unroll
+            for (int q = 0; q < 16; q += 2) dep ^= __float_as_uint(r[q].x);
+            reinterpret_cast<volatile uint32_t *>(rcp_sink)[warp] = dep;
+        }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.empty[k]);
         xr = static_cast<const uint8_t *>(a.x) + (uint64_t(p) * N + sc.i0 + lr) * big_row + 32u * c * XB;
