@@ -7,9 +7,9 @@ set -u
 [ "${SKIP_LAUNCHES:-0}" = 1 ] || timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'k_(quantize|dequant)_|k_attention' \
     --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e \
     > /dev/null 2>&1
-# the bench-shape launches (time_codec first compresses 14 chunks of 720 planes)
+# the bench-shape launches (time_codec compresses TC=2 chunks of 720 planes first)
 timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
-    -k regex:'k_quantize_stream' --launch-skip 15 -c 1 -o /tmp/codec_q python tools/time_codec.py > /dev/null 2>&1
+    -k regex:'k_quantize_ring32' --launch-skip 4 -c 1 -o /tmp/codec_q python tools/time_codec.py > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
     -k regex:'k_dequant_stream<.int.2, .int.2' --launch-skip 2 -c 1 -o /tmp/codec_d python tools/time_codec.py \
     > /dev/null 2>&1
