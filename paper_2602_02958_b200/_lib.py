@@ -14,7 +14,7 @@ import os
 from .qvgcodec import errors as _errors
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqvg_b200.so")
+LIB_PATH = os.environ.get("QVG_LIB_PATH") or os.path.join(_HERE, "libqvg_b200.so")
 
 # status bits (QVG_STATUS_*)
 STATUS_NONFINITE = 1

@@ -740,6 +740,8 @@ static int tile_grid(const TileArgs &t) {
 // too large for shared memory) -- the tile kernels below take those
 int launch_quantize_stream(const QuantArgs &a, int64_t P, int bits, int S, bool xbf16, cudaStream_t st);
 int launch_dequantize_stream(const DequantArgs &a, int64_t P, int bits, int S, bool obf16, cudaStream_t st);
+// 32-channel ring kernel (qvg_dring.cu): the default K6 where it fits
+int launch_dequantize_ring32(const DequantArgs &a, int64_t P, int bits, int S, bool obf16, cudaStream_t st);
 
 template <int BITS, int S>
 static void launch_quant_fast(const QuantArgs &a, bool xbf16, cudaStream_t st) {
@@ -808,6 +810,7 @@ int launch_unpack(const uint8_t *in, int64_t n, int bits, int8_t *out, cudaStrea
 
 template <int BITS, int S>
 static void launch_deq_fast(const DequantArgs &a, bool obf16, cudaStream_t st) {
+    if (S > 0 && launch_dequantize_ring32(a, a.P, BITS, S, obf16, st)) return;
     if (S > 0 && a.v16 && launch_dequantize_stream(a, a.P, BITS, S, obf16, st)) return;
     const int g = tile_grid(a.ta);
     if (a.v16) {
