@@ -37,7 +37,9 @@ struct DGeo {
     uint32_t nslice;       // 32-channel table slices per plane (S*K*d/32)
     uint32_t lslc;         // log2(d / 32)
     uint32_t ipp, rpi, n_items;
-    uint32_t off_ring, stage_bytes, big_row, small_row, off_small;
+    uint32_t off_stg, off_ring, stage_bytes, big_row, small_row, off_small;
+    uint32_t tbytes;       // bf16 table bytes per plane (S*K*d*2)
+    uint32_t stg_global;   // 1: no room for the staging copy, widen from global memory (L2)
 };
 
 struct DSched {
@@ -79,15 +81,15 @@ __device__ __forceinline__ float2 meta16(const float *c) {
     return make_float2(unit, mx);
 }
 
-// widen one plane's bf16 tables [S*K][d] (global, L2-resident) into the padded
+// widen one plane's bf16 tables [S*K][d] (the staged shared copy) into the padded
 // f32 layout: slice q of row q / nslc at float 36 * (q % nslc), pad = metadata
 __device__ __forceinline__ void widen_h(const uint16_t *src, float *tab, const DGeo &g) {
     const uint32_t ns = g.d / 32;
     for (uint32_t q = threadIdx.x; q < g.nslice; q += kCW * 32) {
         const uint4 *sp = reinterpret_cast<const uint4 *>(src + size_t(q) * 32);
         float c[32];
-        cvt16(__ldg(sp), __ldg(sp + 1), c);
-        cvt16(__ldg(sp + 2), __ldg(sp + 3), c + 16);
+        cvt16(sp[0], sp[1], c);
+        cvt16(sp[2], sp[3], c + 16);
         float *dst = tab + size_t(q / ns) * g.pitch + 36u * (q % ns);
 #pragma unroll
         for (int j = 0; j < 8; j++)
@@ -123,6 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
     __shared__ stream::Bars bars;
     __shared__ uint32_t sink[kCW];
     float *const tab = reinterpret_cast<float *>(smem);
+    uint16_t *const stg = reinterpret_cast<uint16_t *>(smem + g.off_stg);   // next plane's bf16 tables (TMA)
     uint8_t *const ring = smem + g.off_ring;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t d = g.d, N = g.N;
@@ -132,6 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
             mbar_init(&bars.full[k], 1 + 32);
             mbar_init(&bars.empty[k], kCW);
         }
+        mbar_init(&bars.tab, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -176,12 +180,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
     const uint32_t kx = one | (1u << 22);
     const uint32_t KK = g.K, pitch = g.pitch;
     bool bad_scale = false, bad_asg = false;
-    uint32_t cur = 0xFFFFFFFFu, k = 0, ph = 0;
+    uint32_t cur = 0xFFFFFFFFu, k = 0, ph = 0, jp = 0;
+    // the first plane's tables; each later plane's are staged by TMA while the
+    // previous plane streams
+    if (!g.stg_global && threadIdx.x == 0 && sc.valid()) stage_table(a.cent, sc.p, g.tbytes, stg, &bars.tab);
     for (; sc.valid(); sc.next(g), k = k + 1 == g.nst ? (ph ^= 1u, 0u) : k + 1) {
         if (sc.p != cur) {
             stream::named_sync_consumers<kCW>();
-            widen_h(a.cent + size_t(sc.p) * (size_t(S) * KK * d), tab, g);
+            if (!g.stg_global) mbar_wait(&bars.tab, jp & 1u);
+            widen_h(g.stg_global ? a.cent + size_t(sc.p) * (g.tbytes / 2) : stg, tab, g);
             stream::named_sync_consumers<kCW>();
+            if (!g.stg_global && threadIdx.x == 0 && (sc.p + 1) * g.ipp < sc.it1) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                stage_table(a.cent, sc.p + 1, g.tbytes, stg, &bars.tab);
+            }
+            jp++;
             cur = sc.p;
         }
         mbar_wait(&bars.full[k], ph);
@@ -355,7 +368,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
 // ============================================================================
 static int ilog2i(int v) { int l = 0; while ((1 << l) < v) l++; return l; }
 
-// smem: [padded f32 tables][ring]; false when the configuration does not fit
+// smem: [padded f32 tables][bf16 staging copy of the next plane's tables][ring]; false when the configuration does not fit
 // (callers fall back to the 16-channel ring kernel)
 static bool plan(int64_t P, int64_t N, int d, int S, int K, int bits, int B, DGeo &g, size_t &smem, int &grid) {
     if (S < 1 || S > 4 || (d != 128 && d != 256) || B % 32 != 0 || N < 4 || N % 4 != 0) return false;
@@ -364,14 +377,21 @@ static bool plan(int64_t P, int64_t N, int d, int S, int K, int bits, int B, DGe
     const uint32_t R = uint32_t(kCW * 32 / nslc);
     const uint32_t pitch = uint32_t((36 * nslc + 31) / 32 * 32);
     const size_t tabb = size_t(S) * K * pitch * 4;
-    const size_t off_ring = (tabb + 1023) & ~size_t(1023);
+    const size_t tbytes = size_t(S) * K * d * 2;
+    const size_t off_stg = (tabb + 127) & ~size_t(127);
+    size_t off_ring = (off_stg + tbytes + 1023) & ~size_t(1023);
     const uint32_t big_row = uint32_t(d * bits / 8), small_row = uint32_t(d / B);
     if ((N * small_row) % 4 != 0) return false;
     const size_t big = size_t(R) * big_row;
     const size_t small = size_t(R) * small_row + size_t(S) * R;
     const size_t stage = (big + ((small + 15) & ~size_t(15)) + 127) & ~size_t(127);
     const size_t budget = 227 * 1024 - 1024;
-    if (off_ring + 2 * stage > budget) return false;
+    uint32_t stg_global = 0;
+    if (off_ring + 2 * stage > budget) {       // no room for the staging copy
+        stg_global = 1;
+        off_ring = (tabb + 1023) & ~size_t(1023);
+        if (off_ring + 2 * stage > budget) return false;
+    }
     uint32_t nst = uint32_t((budget - off_ring) / stage);
     if (nst > 16) nst = 16;
     const int64_t ctas = 148;
@@ -381,8 +401,8 @@ static bool plan(int64_t P, int64_t N, int d, int S, int K, int bits, int B, DGe
     rpi = (rpi + R - 1) / R * R;
     ipp = (N + rpi - 1) / rpi;
     g = DGeo{uint32_t(P), uint32_t(N), uint32_t(d), uint32_t(K), R, nst, pitch, uint32_t(size_t(S) * K * nslc),
-             uint32_t(ilog2i(nslc)), uint32_t(ipp), uint32_t(rpi), uint32_t(P * ipp), uint32_t(off_ring),
-             uint32_t(stage), big_row, small_row, uint32_t(big)};
+             uint32_t(ilog2i(nslc)), uint32_t(ipp), uint32_t(rpi), uint32_t(P * ipp), uint32_t(off_stg),
+             uint32_t(off_ring), uint32_t(stage), big_row, small_row, uint32_t(big), uint32_t(tbytes), stg_global};
     smem = off_ring + g.nst * stage;
     grid = int(P * ipp < ctas ? P * ipp : ctas);
     return true;
