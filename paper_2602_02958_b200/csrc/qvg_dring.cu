@@ -8,13 +8,17 @@
 // producer warp streaming the packed code rows and the scale / assignment
 // bytes through an mbarrier ring (as k_dequant_stream); the consumers widen
 // each plane's bf16 centroid tables once into the padded f32 layout of
-// k_quantize_ring32 (32-channel slices of 36 floats: the 4-float pad holds
-// the slice's certificate metadata {unit, max |c|} for each 16-channel half).
-// Bank conflicts: the 4 slices of a table row sit on bank quads c..c+3; the
-// second row of a quarter-warp (d = 128) reads its upper half first, so the
-// 8 threads of every LDS.128 hit 8 distinct quads.  Its code words are swapped
-// to match and each 16-channel half is written back with one 256-bit store
-// (STG.E.ENL2.256) to its own sector.
+// each plane's bf16 centroid tables are re-laid once into a padded bf16 layout
+// (32-channel slices at word 16c + 4(c/2), rows padded to a multiple of 128
+// bytes, the slices' certificate metadata {unit, max |c|} per 16-channel half
+// after the last slice) and added with FHADD.BF16 (`add.rn.f32.bf16`, f32 =
+// bf16 + f32, one rounding): half the shared-memory wavefronts of f32 tables,
+// which is what bounds this kernel (l1tex data pipe at ~90% with f32 tables).
+// Bank conflicts: chunk k of slice c sits on bank quad 4c + c/2 + k (mod 8);
+// the second row of a quarter-warp (d = 128) reads its upper half first, so
+// the 8 threads of every LDS.128 hit 8 distinct quads.  Its code words are
+// swapped to match and each 16-channel half is written back with one 256-bit
+// store (STG.E.ENL2.256) to its own sector.
 //
 // Numerics are those of k_dequant_stream (Q/prq.py:113-132, Q/quant.py:151):
 // q*s exact by one FFMA, the reference's float64 add-back order reproduced in
@@ -33,7 +37,7 @@ struct DGeo {
     uint32_t P, N, d, K;
     uint32_t R;            // rows per stage = kCW * 32 / (d / 32)
     uint32_t nst;          // ring stages
-    uint32_t pitch;        // f32 table row pitch (floats)
+    uint32_t pitch;        // padded bf16 table row pitch (32-bit words)
     uint32_t nslice;       // 32-channel table slices per plane (S*K*d/32)
     uint32_t lslc;         // log2(d / 32)
     uint32_t ipp, rpi, n_items;
@@ -81,22 +85,50 @@ __device__ __forceinline__ float2 meta16(const float *c) {
     return make_float2(unit, mx);
 }
 
-// widen one plane's bf16 tables [S*K][d] (the staged shared copy) into the padded
-// f32 layout: slice q of row q / nslc at float 36 * (q % nslc), pad = metadata
-__device__ __forceinline__ void widen_h(const uint16_t *src, float *tab, const DGeo &g) {
-    const uint32_t ns = g.d / 32;
+// word offset of 32-channel slice c in a padded table row: 16 c + 4 (c / 2)
+__host__ __device__ __forceinline__ uint32_t slice_w(uint32_t c) { return 16u * c + 4u * (c >> 1); }
+
+// re-lay one plane's bf16 tables [S*K][d] (the staged copy, or global memory)
+// into the padded layout: row pitch g.pitch words, slice c at slice_w(c), the
+// slices' metadata {unit, max |c|} x 2 halves (float4) after the last slice
+__device__ __forceinline__ void widen_h(const uint16_t *src, uint32_t *tab, const DGeo &g) {
+    const uint32_t ns = g.d / 32, mo = slice_w(ns - 1) + 16u;
     for (uint32_t q = threadIdx.x; q < g.nslice; q += kCW * 32) {
         const uint4 *sp = reinterpret_cast<const uint4 *>(src + size_t(q) * 32);
+        const uint4 v0 = sp[0], v1 = sp[1], v2 = sp[2], v3 = sp[3];
         float c[32];
-        cvt16(sp[0], sp[1], c);
-        cvt16(sp[2], sp[3], c + 16);
-        float *dst = tab + size_t(q / ns) * g.pitch + 36u * (q % ns);
-#pragma unroll
-        for (int j = 0; j < 8; j++)
-            reinterpret_cast<float4 *>(dst)[j] = make_float4(c[4 * j], c[4 * j + 1], c[4 * j + 2], c[4 * j + 3]);
+        cvt16(v0, v1, c);
+        cvt16(v2, v3, c + 16);
+        const uint32_t cs = q % ns;
+        uint32_t *row = tab + size_t(q / ns) * g.pitch;
+        uint4 *dst = reinterpret_cast<uint4 *>(row + slice_w(cs));
+        dst[0] = v0; dst[1] = v1; dst[2] = v2; dst[3] = v3;
         const float2 m0 = meta16(c), m1 = meta16(c + 16);
-        *reinterpret_cast<float4 *>(dst + 32) = make_float4(m0.x, m0.y, m1.x, m1.y);
+        *reinterpret_cast<float4 *>(row + mo + 4u * cs) = make_float4(m0.x, m0.y, m1.x, m1.y);
     }
+}
+
+// f32 = bf16 (low / high half of w) + y, one rounding (FHADD.BF16)
+__device__ __forceinline__ float2 fhadd2(uint32_t w, float2 y) {
+    float r0, r1;
+    asm("{.reg .b16 l, h;\nmov.b32 {l, h}, %2;\nadd.rn.f32.bf16 %0, l, %3;\nadd.rn.f32.bf16 %1, h, %4;\n}"
+        : "=f"(r0), "=f"(r1)
+        : "r"(w), "f"(y.x), "f"(y.y));
+    return make_float2(r0, r1);
+}
+
+// the reference's float64 add-back of one element (Q/prq.py:113-132), padded bf16 tables
+template <int S>
+__device__ __noinline__ float exact_addback_p(float qs, const uint32_t *tab, uint32_t pitch, uint32_t wo, uint32_t hsel,
+                                              int K, int a0, int a1, int a2, int a3) {
+    const int ai[4] = {a0, a1, a2, a3};
+    double acc = double(qs);
+#pragma unroll
+    for (int t = S - 1; t >= 0; t--) {
+        const uint32_t w = tab[uint32_t(t * K + ai[t]) * pitch + wo];
+        acc = __dadd_rn(acc, double(__uint_as_float(hsel ? (w & 0xFFFF0000u) : (w << 16))));
+    }
+    return __double2float_rn(acc);
 }
 
 // one 256-bit global store (STG.E.ENL2.256) of 8 words to a 32-byte aligned address
@@ -124,7 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ stream::Bars bars;
     __shared__ uint32_t sink[kCW];
-    float *const tab = reinterpret_cast<float *>(smem);
+    uint32_t *const tab = reinterpret_cast<uint32_t *>(smem);           // padded bf16 tables (word view)
     uint16_t *const stg = reinterpret_cast<uint16_t *>(smem + g.off_stg);   // next plane's bf16 tables (TMA)
     uint8_t *const ring = smem + g.off_ring;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -173,7 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
     const uint32_t c = threadIdx.x & ((1u << ls) - 1u);
     const uint32_t rslot = threadIdx.x >> ls;
     const uint32_t rho = d == 128 ? (uint32_t(lane) >> 2) & 1u : 0u;     // slot half 0 = channel half rho
-    const uint32_t col = 32u * c, soff = 36u * c;
+    const uint32_t col = 32u * c, soff = slice_w(c), moff = slice_w((d >> 5) - 1) + 16u + 4u * c;
     const uint32_t mhi = ((1u << BITS) - 1u) << POS, one = 0x3F800000u;
     // field u at mantissa bits [POS, 23) of 1.0, its sign bit (bit 22) flipped
     // by the same LOP3: f = 1 + (u ^ 2^(b-1)) / 2^b
@@ -253,9 +285,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
             const float2 f = make_float2(__uint_as_float(lop3_and_xor(v0, mhi, kx)), __uint_as_float(lop3_and_xor(v1, mhi, kx)));
             y[q] = __ffma2_rn(f, s_hi, s_off);          // q*s, exact
         }
-        const float *row[SS];
+        const uint32_t *row[SS];
 #pragma unroll
-        for (int t = 0; t < S; t++) row[t] = tab + (uint32_t(t) * KK + uint32_t(ai[t])) * pitch + soff;
+        for (int t = 0; t < S; t++) row[t] = tab + (uint32_t(t) * KK + uint32_t(ai[t])) * pitch;
         // per slot half: certificate (every non-final partial sum exact in f32,
         // see k_dequant_stream), S = 2 swapped order, add-back
         bool certh[2];
@@ -273,13 +305,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
                 float unit = unit_s, bound = bound_s;
 #pragma unroll
                 for (int t = 1; t < S; t++) {
-                    const float4 m = *reinterpret_cast<const float4 *>(row[t] + 32);
+                    const float4 m = *reinterpret_cast<const float4 *>(row[t] + moff);
                     unit = fminf(unit, chh ? m.z : m.x);
                     bound = __fadd_ru(bound, chh ? m.w : m.y);
                 }
                 cert = S == 2 && !anyq ? true : bound < unit * 16777216.f;
                 if constexpr (S == 2) {
-                    const float4 m = *reinterpret_cast<const float4 *>(row[0] + 32);
+                    const float4 m = *reinterpret_cast<const float4 *>(row[0] + moff);
                     const float u0 = chh ? m.z : m.x, m0 = chh ? m.w : m.y;
                     swap01 = !cert && __fadd_ru(bound_s, m0) < fminf(unit_s, u0) * 16777216.f &&
                              __fadd_ru(bound, m0) < fminf(unit, u0) * 9007199254740992.f;
@@ -287,18 +319,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
                 }
             }
             certh[sh] = cert;
-            const float *r1 = row[SS > 1 ? 1 : 0], *r0 = row[0];
+            const uint32_t *r1 = row[SS > 1 ? 1 : 0], *r0 = row[0];
             if constexpr (S == 2) {
-                if (swap01) { const float *tmp = r1; r1 = r0; r0 = tmp; }
+                if (swap01) { const uint32_t *tmp = r1; r1 = r0; r0 = tmp; }
             }
 #pragma unroll
             for (int t = S - 1; t >= 0; t--) {
-                const float *rr = (S == 2 ? (t == 1 ? r1 : r0) : row[t]) + 16u * chh;
+                const uint32_t *rr = (S == 2 ? (t == 1 ? r1 : r0) : row[t]) + soff + 8u * chh;
 #pragma unroll
-                for (int j = 0; j < 4; j++) {
-                    const float4 cv = *reinterpret_cast<const float4 *>(rr + 4 * j);
-                    y[8 * sh + 2 * j] = __fadd2_rn(y[8 * sh + 2 * j], make_float2(cv.x, cv.y));
-                    y[8 * sh + 2 * j + 1] = __fadd2_rn(y[8 * sh + 2 * j + 1], make_float2(cv.z, cv.w));
+                for (int j = 0; j < 2; j++) {
+                    const uint4 cv = *reinterpret_cast<const uint4 *>(rr + 4 * j);
+                    y[8 * sh + 4 * j] = fhadd2(cv.x, y[8 * sh + 4 * j]);
+                    y[8 * sh + 4 * j + 1] = fhadd2(cv.y, y[8 * sh + 4 * j + 1]);
+                    y[8 * sh + 4 * j + 2] = fhadd2(cv.z, y[8 * sh + 4 * j + 2]);
+                    y[8 * sh + 4 * j + 3] = fhadd2(cv.w, y[8 * sh + 4 * j + 3]);
                 }
             }
         }
@@ -318,13 +352,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
                     bool bad = false;
 #pragma unroll
                     for (int t = S - 1; t >= 1; t--) {
-                        const float cc = row[t][cof];
+                        const uint32_t cw = row[t][soff + (cof >> 1)];
+                        const float cc = __uint_as_float((cof & 1u) ? (cw & 0xFFFF0000u) : (cw << 16));
                         const float P2 = __fadd_rn(P, cc);
                         bad |= __fadd_rn(__fadd_rn(P2, -P), -cc) != 0.f || __fadd_rn(__fadd_rn(P2, -cc), -P) != 0.f;
                         P = P2;
                     }
                     if (bad) {
-                        const float rr = stream::exact_addback<S>(qs, tab, pitch, soff + cof, int(KK), ai[0],
+                        const float rr = exact_addback_p<S>(qs, tab, pitch, soff + (cof >> 1), cof & 1u, int(KK), ai[0],
                                                                   ai[SS > 1 ? 1 : 0], ai[SS > 2 ? 2 : 0], ai[SS > 3 ? 3 : 0]);
                         if (e & 1) y[e >> 1].y = rr; else y[e >> 1].x = rr;
                     }
@@ -368,14 +403,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
 // ============================================================================
 static int ilog2i(int v) { int l = 0; while ((1 << l) < v) l++; return l; }
 
-// smem: [padded f32 tables][bf16 staging copy of the next plane's tables][ring]; false when the configuration does not fit
+// smem: [padded bf16 tables][bf16 staging copy of the next plane's tables][ring]; false when the configuration does not fit
 // (callers fall back to the 16-channel ring kernel)
 static bool plan(int64_t P, int64_t N, int d, int S, int K, int bits, int B, DGeo &g, size_t &smem, int &grid) {
     if (S < 1 || S > 4 || (d != 128 && d != 256) || B % 32 != 0 || N < 4 || N % 4 != 0) return false;
     if (P * N >= (int64_t(1) << 31) || N * d >= (int64_t(1) << 31)) return false;
     const int nslc = d / 32;
     const uint32_t R = uint32_t(kCW * 32 / nslc);
-    const uint32_t pitch = uint32_t((36 * nslc + 31) / 32 * 32);
+    const uint32_t pitch = (slice_w(uint32_t(nslc) - 1) + 16u + 4u * uint32_t(nslc) + 31u) / 32u * 32u;
     const size_t tabb = size_t(S) * K * pitch * 4;
     const size_t tbytes = size_t(S) * K * d * 2;
     const size_t off_stg = (tabb + 127) & ~size_t(127);
