@@ -209,6 +209,26 @@ def bench_attention(dev, rank, world, H=32, nc=38400, nq=7800, d=128):
     chunks = D.compress(planes, cfg, chunk_index=0)
     torch.cuda.synchronize()
     enc_s = time.perf_counter() - t0
+    # LongCat codec throughput (this rank's planes, same kernels as the C2 leg)
+    qb, db = plane_bytes(nc, d, cfg)
+    Pl = planes.shape[0]
+    pay, scl = torch.empty_like(chunks.payload), torch.empty_like(chunks.scales)
+    rec = torch.empty_like(planes)
+    stw = torch.zeros(1, dtype=torch.int32, device=dev)
+    ms_qz = time_ms(lambda: D.quantize(planes, cfg, chunks.centroids, chunks.assignments, payload=pay, scales=scl,
+                                       check=False, status=stw), reps=10, warmup=3)
+    ms_dq = time_ms(lambda: D.dequantize(chunks, out=rec, check=False, status=stw), reps=10, warmup=3)
+    codec_ok = torch.equal(pay, chunks.payload) and torch.equal(scl, chunks.scales)
+    del pay, scl, rec
+    ms_qz, ms_dq = allmax([ms_qz, ms_dq], dev, world)
+    hbm = peaks()[0]
+    codec = {"planes": Pl * world, "tokens_per_plane": nc, "quantize_ms": round(ms_qz, 3),
+             "quantize_GBps": round(Pl * world * qb / ms_qz / 1e6, 1),
+             "dequantize_ms": round(ms_dq, 3), "dequantize_GBps": round(Pl * world * db / ms_dq / 1e6, 1),
+             "quant_dequant_GBps": round(Pl * world * (qb + db) / (ms_qz + ms_dq) / 1e6, 1),
+             "quant_dequant_frac": round(Pl * world * (qb + db) / (ms_qz + ms_dq) / 1e6 / hbm, 4),
+             "requantize_matches_compress": bool(codec_ok),
+             "note": "quantize given the compress output's centroids / assignments; input 5x larger than L2"}
     g = torch.Generator(device=dev)
     g.manual_seed(12345)
     q = torch.randn((nq, H, d), generator=g, device=dev).to(torch.bfloat16)
@@ -251,6 +271,7 @@ def bench_attention(dev, rank, world, H=32, nc=38400, nq=7800, d=128):
                      "peak_kind": kind},
         "encode_s": round(enc_s, 3),
         "kv_compression": round(memory_breakdown(cfg, ChunkSpec(nc, d)).ratio_vs_bf16, 3),
+        "codec": codec,
     }
     if world > 1:
         backend = torch.distributed.get_backend()
