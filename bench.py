@@ -242,6 +242,23 @@ def bench_attention(dev, rank, world, H=32, nc=38400, nq=7800, d=128):
         tb.append(time_ms(lambda: D.attention(ql, None, kl, vl, kv_bf16=planes, out=out, check=False), reps=3, warmup=1))
         tq.append(time_ms(lambda: D.attention(ql, chunks, kl, vl, out=out, check=False), reps=3, warmup=1))
     ms_b, ms_q = float(np.median(tb)), float(np.median(tq))
+    # the in-tile decode kernel (fused=True: codes / scales / centroids read
+    # inside the attention kernel, no bf16 workspace) at the layer shape and at
+    # a small-query "step" shape (256 queries per head against the full cache)
+    ms_f = time_ms(lambda: D.attention(ql, chunks, kl, vl, out=out, fused=True, check=False), reps=3, warmup=1)
+    nq_s = 256
+    qs_, ks_, vs_ = ql[:nq_s].contiguous(), kl[:nq_s].contiguous(), vl[:nq_s].contiguous()
+    out_s = torch.empty((nq_s, Hr, d), dtype=torch.bfloat16, device=dev)
+    step = {"query_tokens": nq_s, "cur_tokens": nq_s,
+            "latency_ms_quantized": time_ms(lambda: D.attention(qs_, chunks, ks_, vs_, out=out_s, check=False), reps=10),
+            "latency_ms_quantized_fused": time_ms(lambda: D.attention(qs_, chunks, ks_, vs_, out=out_s, fused=True,
+                                                                      check=False), reps=10),
+            "latency_ms_bf16_same_kernel": time_ms(lambda: D.attention(qs_, None, ks_, vs_, kv_bf16=planes, out=out_s,
+                                                                       check=False), reps=10)}
+    ms_f, step["latency_ms_quantized"], step["latency_ms_quantized_fused"], step["latency_ms_bf16_same_kernel"] = allmax(
+        [ms_f, step["latency_ms_quantized"], step["latency_ms_quantized_fused"], step["latency_ms_bf16_same_kernel"]],
+        dev, world)
+    step = {k: (round(v, 4) if isinstance(v, float) else v) for k, v in step.items()}
     ms_g = None
     if world > 1:
         D.attention(ql, chunks, kl, vl, out=out)
@@ -262,6 +279,7 @@ def bench_attention(dev, rank, world, H=32, nc=38400, nq=7800, d=128):
         "workload": "longcat_layer", "heads": H, "heads_per_rank": Hr, "n_gpus": world,
         "cache_tokens": nc, "query_tokens": nq, "cur_tokens": nq, "config": "b2 S1 K256 B64",
         "latency_ms_quantized": round(ms_q, 3), "latency_ms_bf16_same_kernel": round(ms_b, 3),
+        "latency_ms_quantized_fused": round(ms_f, 3),
         "latency_ms_torch_sdpa_bf16": None if not ms_sdpa else round(ms_sdpa, 3),
         "ratio_quantized_vs_bf16": round(ms_q / ms_b, 4),
         "ratio_quantized_vs_sdpa": None if not ms_sdpa else round(ms_q / ms_sdpa, 4),
@@ -272,6 +290,7 @@ def bench_attention(dev, rank, world, H=32, nc=38400, nq=7800, d=128):
         "encode_s": round(enc_s, 3),
         "kv_compression": round(memory_breakdown(cfg, ChunkSpec(nc, d)).ratio_vs_bf16, 3),
         "codec": codec,
+        "step_shape": step,
     }
     if world > 1:
         backend = torch.distributed.get_backend()

@@ -11,7 +11,7 @@ set -u
 timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
     -k regex:'k_quantize_ring32' --launch-skip 4 -c 1 -o /tmp/codec_q python tools/time_codec.py > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none --kernel-name-base demangled \
-    -k regex:'k_dequant_stream<.int.2, .int.2' --launch-skip 2 -c 1 -o /tmp/codec_d python tools/time_codec.py \
+    -k regex:'k_dequant_ring32<.int.2, .int.2' --launch-skip 2 -c 1 -o /tmp/codec_d python tools/time_codec.py \
     > /dev/null 2>&1
 python tools/ncu_summary.py /tmp/codec_q.ncu-rep /tmp/codec_d.ncu-rep > gpurun_out/ncu_full_codec.txt 2>&1
 python tools/launch_list.py gpurun_out/launches.csv > gpurun_out/launches.txt 2>&1
