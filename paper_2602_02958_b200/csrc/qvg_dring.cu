@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
     constexpr int HW = BITS / 2;                 // code words per 16-field half
     extern __shared__ __align__(1024) uint8_t smem[];
     __shared__ stream::Bars bars;
-    __shared__ uint32_t sink[kCW];
+    __shared__ uint32_t sink[kCW * 32];          // release-ordering stores, one word per thread
     uint32_t *const tab = reinterpret_cast<uint32_t *>(smem);           // padded bf16 tables (word view)
     uint16_t *const stg = reinterpret_cast<uint16_t *>(smem + g.off_stg);   // next plane's bf16 tables (TMA)
     uint8_t *const ring = smem + g.off_ring;
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_dequant_ring32(DequantArgs a, D
             for (int t = 0; t < S; t++) dep ^= uint32_t(ai[t]);
 #pragma unroll
             for (int q = 0; q < BITS; q++) dep ^= w[q];
-            reinterpret_cast<volatile uint32_t *>(sink)[warp] = dep;
+            reinterpret_cast<volatile uint32_t *>(sink)[threadIdx.x] = dep;
         }
         __syncwarp();
         if (lane == 0) stream::mbar_arrive(&bars.empty[k]);

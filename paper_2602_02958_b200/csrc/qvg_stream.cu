@@ -389,7 +389,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
     float *const tab = reinterpret_cast<float *>(smem + g.off_tab);
     uint8_t *const ring = smem + g.off_ring;
     __shared__ float rcp_tab[128];
-    __shared__ uint32_t rcp_sink[CW];       // release-ordering stores (see below)
+    __shared__ uint32_t rcp_sink[CW * 32];  // release-ordering stores (see below), one word per thread
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t d = g.d, N = g.N;
 
@@ -516,7 +516,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
             for (int t = 0; t < S; t++) dep ^= uint32_t(ai[t]);
 #pragma unroll
             for (int q = 0; q < 16; q += 2) dep ^= __float_as_uint(r[q].x);
-            reinterpret_cast<volatile uint32_t *>(rcp_sink)[warp] = dep;
+            reinterpret_cast<volatile uint32_t *>(rcp_sink)[threadIdx.x] = dep;
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.empty[k]);

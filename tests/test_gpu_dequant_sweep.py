@@ -1,0 +1,51 @@
+"""K6 (prq_decompress_onepass, Q/prq.py:113-132) over synthetic compressed
+caches, bit-exact against the CPU oracle across the kernel-selection space:
+head_dim 128 / 256 (the 32-channel ring kernel), 64 (the tile kernels),
+bits 2 / 4 / 8, S = 1..4 stages, K = 16 / 256 centroids, groups of 32 / 64 /
+128, bf16 and f32 outputs, token counts that are not a multiple of a ring
+stage.  Inputs are arbitrary valid caches (random code bytes, every non-NaN
+E4M3 scale code, centroid rows whose magnitudes span 2^-24..2^12 with zero and
+tiny entries), which drives the per-half exactness certificates, the S = 2
+swapped-order certificate and the per-element float64 fallback."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2602_02958_b200 import device as D  # noqa: E402
+from paper_2602_02958_b200.qvgcodec.lowprec import round_to_bf16  # noqa: E402
+from paper_2602_02958_b200.qvgcodec.types import QuantConfig  # noqa: E402
+
+
+def _cache(P, N, d, bits, B, S, K, seed):
+    rng = np.random.default_rng(seed)
+    payload = rng.integers(0, 256, size=(P, N * d * bits // 8), dtype=np.uint8)
+    scales = rng.integers(0, 0x7F, size=(P, N * d // B), dtype=np.uint8)          # 0x00..0x7E
+    mag = 2.0 ** rng.integers(-24, 13, size=(P, S, K, 1))
+    cent = rng.normal(0.0, 1.0, size=(P, S, K, d)) * mag
+    cent[rng.random(cent.shape) < 0.02] = 0.0
+    cent[rng.random(cent.shape) < 0.01] *= 2.0 ** -30                              # tiny entries
+    cent = round_to_bf16(cent.astype(np.float32)).astype(np.float32)
+    asg = rng.integers(0, K, size=(P, S, N), dtype=np.uint8)
+    return payload, scales, cent, asg
+
+
+@pytest.mark.parametrize("d", [128, 256, 64])
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("S", [1, 2, 3, 4])
+def test_dequant_sweep_vs_oracle(oracle_lib, d, bits, S):
+    for K, B in ((16, 32), (256, 64), (64, 128)):
+        if B > d:
+            continue
+        P, N = 3, 1004
+        payload, scales, cent, asg = _cache(P, N, d, bits, B, S, K, seed=d * 1000 + bits * 100 + S * 10 + K % 7)
+        cfg = QuantConfig(bits=bits, group_size=B, stages=S, centroids=K)
+        cb = torch.from_numpy(cent).to(torch.bfloat16)
+        dc = D.DeviceChunks(cfg, N, d, torch.from_numpy(payload).cuda(), torch.from_numpy(scales).cuda(),
+                            cb.cuda(), torch.from_numpy(asg).cuda())
+        ref = oracle_lib.prq_decompress_batch(payload, scales, cent, asg, N, d, bits, B, 16)
+        out32 = D.dequantize(dc, torch.float32).cpu().numpy()
+        assert np.array_equal(out32.view(np.uint32), ref.view(np.uint32)), (K, B)
+        out16 = D.dequantize(dc, torch.bfloat16).cpu()
+        assert torch.equal(out16, torch.from_numpy(ref).to(torch.bfloat16)), (K, B)
