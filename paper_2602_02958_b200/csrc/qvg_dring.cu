@@ -420,7 +420,7 @@ static bool plan(int64_t P, int64_t N, int d, int S, int K, int bits, int B, DGe
     const size_t big = size_t(R) * big_row;
     const size_t small = size_t(R) * small_row + size_t(S) * R;
     const size_t stage = (big + ((small + 15) & ~size_t(15)) + 127) & ~size_t(127);
-    const size_t budget = 227 * 1024 - 1024;
+    const size_t budget = 227 * 1024 - 4096;      // dynamic smem; static arrays (barriers, sinks, tables) need the rest
     uint32_t stg_global = 0;
     if (off_ring + 2 * stage > budget) {       // no room for the staging copy
         stg_global = 1;

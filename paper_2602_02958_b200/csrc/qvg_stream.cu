@@ -990,7 +990,7 @@ static bool plan(bool quant, int64_t P, int64_t N, int d, int S, int K, int bits
     const size_t big = size_t(R) * big_row;
     const size_t small = size_t(R) * small_row + size_t(S) * R;
     const size_t stage = (big + ((small + 15) & ~size_t(15)) + 127) & ~size_t(127);
-    const size_t budget = 227 * 1024 - 1024;
+    const size_t budget = 227 * 1024 - 4096;      // dynamic smem; static arrays (barriers, sinks, tables) need the rest
     // c32 widens straight from global memory (L2-resident tables): the staging
     // copy's 32 KB buys one more ring stage (4 vs 3: 4.47 vs 4.58 ms)
     if (off_ring + 2 * stage > budget || (quant && c32)) {

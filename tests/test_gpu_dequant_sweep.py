@@ -49,3 +49,23 @@ def test_dequant_sweep_vs_oracle(oracle_lib, d, bits, S):
         assert np.array_equal(out32.view(np.uint32), ref.view(np.uint32)), (K, B)
         out16 = D.dequantize(dc, torch.bfloat16).cpu()
         assert torch.equal(out16, torch.from_numpy(ref).to(torch.bfloat16)), (K, B)
+
+
+@pytest.mark.parametrize("S,K", [(1, 256), (2, 256), (2, 64)])
+def test_longcat_tables_codec_vs_oracle(oracle_lib, S, K):
+    """LongCat-sized planes (38 400 tokens) with large centroid tables: the
+    ring kernels' shared-memory plans at the budget edge (K = 256 tables leave
+    few ring stages) -- quantize given the metadata and dequantize, bit-exact."""
+    P, N, d, bits, B = 2, 38400, 128, 2, 64
+    payload, scales, cent, asg = _cache(P, N, d, bits, B, S, K, seed=77 + S + K)
+    cfg = QuantConfig(bits=bits, group_size=B, stages=S, centroids=K)
+    cb = torch.from_numpy(cent).to(torch.bfloat16).cuda()
+    ag = torch.from_numpy(asg).cuda()
+    dc = D.DeviceChunks(cfg, N, d, torch.from_numpy(payload).cuda(), torch.from_numpy(scales).cuda(), cb, ag)
+    ref = oracle_lib.prq_decompress_batch(payload, scales, cent, asg, N, d, bits, B, 16)
+    out = D.dequantize(dc, torch.float32)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref.view(np.uint32))
+    x = out.to(torch.bfloat16)                                   # any bf16 planes: quantize given the metadata
+    pay, sc = D.quantize(x, cfg, cb, ag)
+    rp, rs = oracle_lib.quantize_given_metas_batch(x.float().cpu().numpy(), cent, asg, bits, B, 16)
+    assert np.array_equal(pay.cpu().numpy(), rp) and np.array_equal(sc.cpu().numpy(), rs)
