@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_stream(QuantArgs 
             int ai[SS];
 #pragma unroll
             for (int t = 0; t < S; t++) ai[t] = st[g.off_small + t * g.R + lr];
-            float csum = 0.f, cunit = __int_as_float(0x7F800000);
+            float csum = 0.f, cunit = __int_as_float(0x7F800000), cwt = 0.f;
 #pragma unroll
             for (int t = 0; t < S; t++) {
                 const uint32_t row = uint32_t(t * int(KK) + ai[t]);
@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_stream(QuantArgs 
                 }
                 const float2 m = meta[(row << lvpr) + c];
                 csum = __fadd_ru(csum, m.y);
+                if (t > 0) cwt = __fmaf_ru(float(t), m.y, cwt);
                 cunit = fminf(cunit, m.x);
             }
             float m0 = 0.f, m1 = 0.f;
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_stream(QuantArgs 
             const uint32_t xe = __float_as_uint(xmn) & 0x7F800000u;
             const float un = fminf(xe > (7u << 23) ? __uint_as_float(xe - (7u << 23)) : 0.f, cunit);
             const bool cert = S == 0 || (XBF16 && __fmaf_ru(2.f, csum, mx) < un * 8388608.f);
-            const float El = cert ? 0.f : __fmul_ru(__fmul_ru(float(S), __fadd_ru(mx, csum)), 2.38418579e-7f);
+            const float El = cert ? 0.f : err_bound(float(S), mx, cwt);
             // ---- the group's amax interval and its E4M3 "up" code
             float lo = __fsub_rd(mx, El), hi = __fadd_ru(mx, El);
             if (glanes == 4) {           // the three partners at once: one shuffle latency
@@ -521,7 +522,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.empty[k]);
         xr = static_cast<const uint8_t *>(a.x) + (uint64_t(p) * N + sc.i0 + lr) * big_row + 32u * c * XB;
-        float csum = 0.f, cunit = __int_as_float(0x7F800000);
+        float csum = 0.f, cunit = __int_as_float(0x7F800000), cwt = 0.f;   // cwt = sum_t t max|C_t| (0-based t)
 #pragma unroll
         for (int t = 0; t < S; t++) {
             const float *cr = tab + uint32_t(t * int(KK) + ai[t]) * pitch + soff;
@@ -540,6 +541,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
             }
             const float2 m = *reinterpret_cast<const float2 *>(cr + 32);
             csum = __fadd_ru(csum, m.y);
+            if (t > 0) cwt = __fmaf_ru(float(t), m.y, cwt);
             cunit = fminf(cunit, m.x);
         }
         float m0 = 0.f, m1 = 0.f;
@@ -553,7 +555,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
         const uint32_t xe = __float_as_uint(xmn) & 0x7F800000u;
         const float un = fminf(xe > (7u << 23) ? __uint_as_float(xe - (7u << 23)) : 0.f, cunit);
         const bool cert = XBF16 && __fmaf_ru(2.f, csum, mx) < un * 8388608.f;
-        const float El = cert ? 0.f : __fmul_ru(__fmul_ru(float(S), __fadd_ru(mx, csum)), 2.38418579e-7f);
+        const float El = cert ? 0.f : err_bound(float(S), mx, cwt);
         float lo = __fsub_rd(mx, El), hi = __fadd_ru(mx, El);
         for (int m = 1; m < glanes; m <<= 1) {
             lo = fmaxf(lo, __shfl_xor_sync(0xffffffffu, lo, m));

@@ -203,6 +203,21 @@ __device__ __forceinline__ float xat(const uint8_t *xrow, int k) {
     else return reinterpret_cast<const float *>(xrow)[k];
 }
 
+// Bound on |r_f32 - r_ref| for a lane whose residual is not certified exact.
+// The kernel forms r_t = RN32(r_{t-1} - C_t) (r_0 = x); each step's rounding
+// error is at most u|r_t| (u = 2^-24, relative to the step's result), so
+// r_S = x - sum C + sum_t e_t with |e_t| <= u' |r_t|, and |r_t| <= max|r_S| +
+// sum_{tau > t} max|C_tau| (+ second order).  The reference's float64 chain
+// has the same form with 2^-53.  Hence
+//   |r_f32 - r_ref| <= 2^-23 (S max|r_S| + sum_{t >= 2} (t - 1) max|C_t|)
+// (factor 2 over u' + u64' for the second-order terms), plus S * 2^-149 for
+// steps whose result is subnormal.  The first stage's centroid never enters:
+// its subtraction's error is relative to r_1 = x - C_1.  cwt = sum_t t max|C_t|
+// over 0-based t (rounded up); all arithmetic rounds up.
+__device__ __forceinline__ float err_bound(float S, float mx, float cwt) {
+    return __fmaf_ru(__fmaf_ru(S, mx, cwt), 1.1920928955078125e-7f, S * 1.40129846e-45f);
+}
+
 // per-row threshold of the ambiguity window (see K5)
 template <int QMAX>
 __device__ __forceinline__ float window_thr(float sv, float inv, float E) {
