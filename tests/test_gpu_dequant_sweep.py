@@ -1,6 +1,7 @@
 """K6 (prq_decompress_onepass, Q/prq.py:113-132) over synthetic compressed
 caches, bit-exact against the CPU oracle across the kernel-selection space:
-head_dim 128 / 256 (the 32-channel ring kernel), 64 (the tile kernels),
+head_dim 128 / 256 (the 32-channel ring kernel), 64 (the 16-channel ring
+kernel), odd token counts (the tile kernels),
 bits 2 / 4 / 8, S = 1..4 stages, K = 16 / 256 centroids, groups of 32 / 64 /
 128, bf16 and f32 outputs, token counts that are not a multiple of a ring
 stage.  Inputs are arbitrary valid caches (random code bytes, every non-NaN
@@ -35,10 +36,10 @@ def _cache(P, N, d, bits, B, S, K, seed):
 @pytest.mark.parametrize("bits", [2, 4, 8])
 @pytest.mark.parametrize("S", [1, 2, 3, 4])
 def test_dequant_sweep_vs_oracle(oracle_lib, d, bits, S):
-    for K, B in ((16, 32), (256, 64), (64, 128)):
+    for K, B, N in ((16, 32, 1004), (256, 64, 1004), (64, 128, 1004), (16, 64, 1003)):
         if B > d:
             continue
-        P, N = 3, 1004
+        P = 3
         payload, scales, cent, asg = _cache(P, N, d, bits, B, S, K, seed=d * 1000 + bits * 100 + S * 10 + K % 7)
         cfg = QuantConfig(bits=bits, group_size=B, stages=S, centroids=K)
         cb = torch.from_numpy(cent).to(torch.bfloat16)
@@ -69,3 +70,36 @@ def test_longcat_tables_codec_vs_oracle(oracle_lib, S, K):
     pay, sc = D.quantize(x, cfg, cb, ag)
     rp, rs = oracle_lib.quantize_given_metas_batch(x.float().cpu().numpy(), cent, asg, bits, B, 16)
     assert np.array_equal(pay.cpu().numpy(), rp) and np.array_equal(sc.cpu().numpy(), rs)
+
+
+@pytest.mark.parametrize("d", [128, 256, 64])
+@pytest.mark.parametrize("bits", [2, 4, 8])
+@pytest.mark.parametrize("S", [0, 1, 2, 3])
+def test_quantize_sweep_vs_oracle(oracle_lib, d, bits, S):
+    """K5 (quantize given the stage metadata, Q/quant.py:124-148 after
+    Q/smoothing.py:40) over every kernel the dispatcher can pick: the
+    32-channel ring (S >= 2), the 16-channel ring (S = 1, d = 64), the tile
+    kernels (S = 0, odd N), on bf16 planes with outlier channels and tiny
+    entries (uncertified lanes, window and exact-scale fallbacks)."""
+    rng = np.random.default_rng(d * 100 + bits * 10 + S)
+    for K, B, N in ((16, 64, 1004), (64, 32, 1003)):
+        if B > d:
+            continue
+        P = 3
+        x = rng.normal(0.0, 2.5, size=(P, N, d))
+        x[:, :, ::16] *= 40.0                                          # outlier channels
+        x[rng.random(x.shape) < 0.003] *= 2.0 ** -20                   # tiny entries
+        x = round_to_bf16(x.astype(np.float32)).astype(np.float32)
+        Sc = max(S, 1)
+        cent = round_to_bf16((rng.normal(0.0, 2.0, size=(P, Sc, K, d)) *
+                              np.where(np.arange(d) % 16 == 0, 30.0, 1.0)).astype(np.float32)).astype(np.float32)
+        asg = rng.integers(0, K, size=(P, Sc, N), dtype=np.uint8)
+        cent, asg = cent[:, :S], asg[:, :S]
+        cfg = QuantConfig(bits=bits, group_size=B, stages=S, centroids=K)
+        xd = torch.from_numpy(x).to(torch.bfloat16).cuda()
+        pay, sc = D.quantize(xd, cfg, torch.from_numpy(np.ascontiguousarray(cent)).to(torch.bfloat16).cuda(),
+                             torch.from_numpy(np.ascontiguousarray(asg)).cuda())
+        rp, rs = oracle_lib.quantize_given_metas_batch(x, np.ascontiguousarray(cent), np.ascontiguousarray(asg),
+                                                       bits, B, 16)
+        assert np.array_equal(sc.cpu().numpy(), rs), (K, B, N)
+        assert np.array_equal(pay.cpu().numpy(), rp), (K, B, N)
