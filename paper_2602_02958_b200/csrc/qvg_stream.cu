@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
         const uint32_t l = rslot;
         const bool valid = l < nr;
         const uint32_t lr = valid ? l : nr - 1;
-        const uint8_t *xr = st + lr * big_row + 32u * c * XB;     // the slice's x (ring, then global)
+        const uint8_t *xr = st + lr * big_row + 32u * c * XB;     // the slice's x in the ring slot
         float2 r[16];
         float xmn = __int_as_float(0x7F800000);
         {
@@ -521,7 +521,9 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars.empty[k]);
-        xr = static_cast<const uint8_t *>(a.x) + (uint64_t(p) * N + sc.i0 + lr) * big_row + 32u * c * XB;
+        // the rare exact paths re-read x from global memory (the slot may be refilled)
+        const uint32_t xrow = sc.i0 + lr;
+        auto xg = [&]() { return static_cast<const uint8_t *>(a.x) + (uint64_t(p) * N + xrow) * big_row + 32u * c * XB; };
         float csum = 0.f, cunit = __int_as_float(0x7F800000), cwt = 0.f;   // cwt = sum_t t max|C_t| (0-based t)
 #pragma unroll
         for (int t = 0; t < S; t++) {
@@ -592,7 +594,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
                                 (fabsf(r[8 * h + q].y) >= thr ? 2u << (2 * q) : 0u);
                     const uint32_t hc = h == 0 ? hlo : hhi;
                     if (cand)
-                        a64 = fmax(a64, exact_absmax<S, XBF16>(xr + hc * XB, tab, pitch, soff + hc, int(KK), ai[0],
+                        a64 = fmax(a64, exact_absmax<S, XBF16>(xg() + hc * XB, tab, pitch, soff + hc, int(KK), ai[0],
                                                                ai[SS > 1 ? 1 : 0], ai[SS > 2 ? 2 : 0],
                                                                ai[SS > 3 ? 3 : 0], cand));
                 }
@@ -662,7 +664,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
                 Words4 b;
 #pragma unroll
                 for (int wd = 0; wd < NWD / 2; wd++) b.w[wd] = w[h * (NWD / 2) + wd];
-                b = fix_codes<BITS, S, XBF16>(xr + hc * XB, tab, pitch, soff + hc, int(KK), ai[0],
+                b = fix_codes<BITS, S, XBF16>(xg() + hc * XB, tab, pitch, soff + hc, int(KK), ai[0],
                                               ai[SS > 1 ? 1 : 0], ai[SS > 2 ? 2 : 0], ai[SS > 3 ? 3 : 0], sv,
                                               inv, El, thr, allv, b);
 #pragma unroll
