@@ -556,3 +556,28 @@ def token_axis_dequantize(payload: torch.Tensor, scales: torch.Tensor, n_tokens:
     pad = (-n_tokens) % group_size
     t = rtn_dequantize(payload, scales, head_dim, n_tokens + pad, bits, group_size)
     return token_untranspose(t, n_tokens)
+
+
+# ---------------------------------------------------------------------------
+# tracing: QVG_NVTX=1 wraps the device entry points in NVTX ranges (named as
+# the reference functions they replace), visible in nsys / ncu --nvtx timelines
+# ---------------------------------------------------------------------------
+def _nvtx_wrap(name, fn):
+    import functools
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        torch.cuda.nvtx.range_push(name)
+        try:
+            return fn(*args, **kwargs)
+        finally:
+            torch.cuda.nvtx.range_pop()
+    return wrapped
+
+
+if __import__("os").environ.get("QVG_NVTX") == "1":
+    for _n, _ref in (("compress", "prq_compress"), ("quantize", "quantize_matrix"),
+                     ("dequantize", "prq_decompress_onepass"), ("attention", "qvg_attention"),
+                     ("kmeans", "kmeans"), ("sa_smoothing", "sa_smoothing")):
+        globals()[_n] = _nvtx_wrap(f"qvg.{_ref}", globals()[_n])
+
