@@ -1076,12 +1076,15 @@ int launch_quantize_stream(const QuantArgs &a, int64_t P, int bits, int S, bool 
     size_t smem;
     int grid;
     const uintptr_t probe = reinterpret_cast<uintptr_t>(a.asg) | reinterpret_cast<uintptr_t>(a.x);
-    // 32 channels per thread when rows are 128 / 256 channels, groups >= 32 and
-    // S >= 2; with one stage the 16-channel kernel is faster (its per-lane
-    // certificates cover 16 channels, so fewer lanes need the window test):
-    // C5 grid, S = 1: 2-bit +15..70%, 4-bit +1..8%; Self-Forcing S = 2: 4.55 vs 4.68 ms
+    // 32 channels per thread for 2-bit, two-stage caches with 128 / 256-channel
+    // rows and groups >= 32 (Self-Forcing: 4.54 vs 4.68 ms).  Everywhere else
+    // the 16-channel kernel measured faster: its per-lane certificates cover
+    // 16 channels (fewer lanes need the window test), and its f32 tables are
+    // smaller per stage (the 32-channel tables of S = 4, K = 64 leave 2 ring
+    // stages).  microbench N 4K/64K, K 64: S = 1 2-bit +15..70%, S = 2 4-bit
+    // +9%, S = 3 +7% / +24%, S = 4 +32% / x2 (2-bit / 4-bit)
     static const bool no32 = [] { const char *e = getenv("QVG_QUANT_C16"); return e && atoi(e) == 1; }();
-    if (!no32 && S >= 2 && a.B % 32 == 0 &&
+    if (!no32 && S == 2 && bits == 2 && a.B % 32 == 0 &&
         plan(true, P, a.N, a.d, S, a.K, bits, a.B, xbf16 ? 2 : 4, probe, g, smem, grid, kCW, 1, true)) {
 #define QV_Q32(BB)                                                          \
         switch (S) {                                                        \

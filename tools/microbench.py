@@ -33,7 +33,7 @@ def main():
         del xh
         for K in Ks:
             for bits in (2, 4):
-                cfg = QuantConfig(bits=bits, group_size=64, stages=1, centroids=K)
+                cfg = QuantConfig(bits=bits, group_size=64, stages=int(os.environ.get("MB_S", "1")), centroids=K)
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
                 dc = D.compress(x, cfg, chunk_index=0)
