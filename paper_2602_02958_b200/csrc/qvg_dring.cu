@@ -462,7 +462,10 @@ static int launch_d(const DequantArgs &a, bool obf16, const DGeo &g, size_t smem
 int launch_dequantize_ring32(const DequantArgs &a, int64_t P, int bits, int S, bool obf16, cudaStream_t st) {
     using namespace dring;
     static const bool off = [] { const char *e = getenv("QVG_DEQ_C16"); return e && atoi(e) == 1; }();
-    if (off) return 0;
+    // S >= 3: the 16-channel kernel's finer certificates leave fewer rows to the
+    // per-element Fast2Sum fallback (microbench N 64K, K 64, S = 3: 1.90 vs
+    // 1.32 TB/s; S = 4 equal); S <= 2: this kernel (S = 2, K 256: 4.49 vs 2.84)
+    if (off || S > 2) return 0;
     DGeo g;
     size_t smem;
     int grid;
