@@ -108,3 +108,19 @@ def test_memory_breakdown_matches_paper_accounting():
     fr = metrics.breakdown_fractions(metrics.memory_breakdown(QuantConfig(), ChunkSpec(100, 128)))
     assert math.isclose(sum(fr.values()), 1.0)
     assert metrics.psnr(np.zeros(3), np.zeros(3)) == metrics.PSNR_INF
+
+
+def test_nvtx_wrappers_opt_in():
+    """QVG_NVTX=1 wraps the device entry points in NVTX ranges (tracing hook);
+    without it the functions are the plain ones."""
+    import subprocess
+    import sys
+    code = ("import paper_2602_02958_b200.device as D; "
+            "print(int(all(hasattr(getattr(D, n), '__wrapped__') for n in "
+            "('compress', 'quantize', 'dequantize', 'attention'))))")
+    env = dict(__import__("os").environ, QVG_NVTX="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert out.stdout.strip() == "1", out.stderr
+    env.pop("QVG_NVTX")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert out.stdout.strip() == "0", out.stderr
