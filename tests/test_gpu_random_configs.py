@@ -1,0 +1,60 @@
+"""Randomised configurations through the codec dispatcher (quantize given the
+stage metadata, then dequantize), bit-exact against the CPU oracle.
+
+Each case draws P, N, head_dim, bits, group size, stages and centroid count
+from the ranges the kernels plan for (and their fallbacks: N not a multiple
+of 4, head_dims other than 128 / 256, K up to 256 with tables at the shared-
+memory budget edge), and bf16 planes with outlier channels, tiny entries,
+exact zeros and exactly representable ties (values on a coarse grid), so the
+certificates, the window tests, the exact-scale and exact-code fallbacks and
+the Fast2Sum add-back checks all run.  Seeds are fixed: failures reproduce."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_2602_02958_b200 import device as D  # noqa: E402
+from paper_2602_02958_b200.qvgcodec.lowprec import round_to_bf16  # noqa: E402
+from paper_2602_02958_b200.qvgcodec.types import QuantConfig  # noqa: E402
+
+N_CASES = 150
+
+
+def _case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    d = int(rng.choice([64, 128, 128, 256]))
+    bits = int(rng.choice([2, 2, 4, 8]))
+    B = int(rng.choice([b for b in (16, 32, 64, 128) if b <= d]))
+    S = int(rng.integers(0, 5))
+    K = int(rng.choice([8, 16, 64, 256]))
+    P = int(rng.integers(1, 6))
+    N = int(rng.integers(1, 40)) * 64 + int(rng.choice([0, 0, 0, 1, 3]))
+    x = rng.normal(0.0, float(rng.choice([0.01, 1.0, 2.5])), size=(P, N, d))
+    x[:, :, :: int(rng.choice([8, 16, 32]))] *= float(rng.choice([1.0, 40.0, 300.0]))
+    x[rng.random(x.shape) < 0.002] *= 2.0 ** -30
+    x[rng.random(x.shape) < 0.002] = 0.0
+    grid = rng.random(x.shape) < 0.05
+    x[grid] = np.round(x[grid] * 4.0) / 4.0                     # coarse values: exact ties
+    x = round_to_bf16(x.astype(np.float32)).astype(np.float32)
+    Sc = max(S, 1)
+    cent = rng.normal(0.0, 1.5, size=(P, Sc, K, d)) * (2.0 ** rng.integers(-6, 4, size=(P, Sc, K, 1)))
+    cent = round_to_bf16(cent.astype(np.float32)).astype(np.float32)[:, :S]
+    asg = rng.integers(0, K, size=(P, Sc, N), dtype=np.uint8)[:, :S]
+    return dict(P=P, N=N, d=d, bits=bits, B=B, S=S, K=K), x, np.ascontiguousarray(cent), np.ascontiguousarray(asg)
+
+
+@pytest.mark.parametrize("seed", range(N_CASES))
+def test_random_config_codec_vs_oracle(oracle_lib, seed):
+    c, x, cent, asg = _case(seed)
+    cfg = QuantConfig(bits=c["bits"], group_size=c["B"], stages=c["S"], centroids=c["K"])
+    cb = torch.from_numpy(cent).to(torch.bfloat16).cuda()
+    ag = torch.from_numpy(asg).cuda()
+    pay, sc = D.quantize(torch.from_numpy(x).to(torch.bfloat16).cuda(), cfg, cb, ag)
+    rp, rs = oracle_lib.quantize_given_metas_batch(x, cent, asg, c["bits"], c["B"], 16)
+    assert np.array_equal(sc.cpu().numpy(), rs), c
+    assert np.array_equal(pay.cpu().numpy(), rp), c
+    dc = D.DeviceChunks(cfg, c["N"], c["d"], pay, sc, cb, ag)
+    out = D.dequantize(dc, torch.float32).cpu().numpy()
+    ref = oracle_lib.prq_decompress_batch(rp, rs, cent, asg, c["N"], c["d"], c["bits"], c["B"], 16)
+    assert np.array_equal(out.view(np.uint32), ref.view(np.uint32)), c
