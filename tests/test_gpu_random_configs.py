@@ -58,3 +58,38 @@ def test_random_config_codec_vs_oracle(oracle_lib, seed):
     out = D.dequantize(dc, torch.float32).cpu().numpy()
     ref = oracle_lib.prq_decompress_batch(rp, rs, cent, asg, c["N"], c["d"], c["bits"], c["B"], 16)
     assert np.array_equal(out.view(np.uint32), ref.view(np.uint32)), c
+
+
+def _compress_case(seed):
+    rng = np.random.default_rng(5000 + seed)
+    d = int(rng.choice([24, 64, 128, 128]))
+    bits = int(rng.choice([2, 2, 4, 8]))
+    B = int(rng.choice([b for b in (8, 16, 32, 64) if d % b == 0]))
+    S = int(rng.integers(1, 4))
+    K = int(rng.choice([4, 8, 16, 64]))
+    P = int(rng.integers(1, 4))
+    N = int(rng.integers(max(K, 40), 1200))
+    centers = rng.normal(0.0, 3.0, size=(P, 12, d))
+    x = centers[:, rng.integers(0, 12, size=N)] + rng.normal(0.0, 0.7, size=(P, N, d))
+    x[:, :, :: int(rng.choice([8, 16]))] *= float(rng.choice([1.0, 20.0]))
+    x = round_to_bf16(x.astype(np.float32)).astype(np.float32)
+    chunks = [int(v) for v in rng.integers(0, 50, size=P)]
+    return dict(P=P, N=N, d=d, bits=bits, B=B, S=S, K=K, chunks=chunks), x
+
+
+@pytest.mark.parametrize("seed", range(80))
+def test_random_config_compress_vs_oracle(oracle_lib, seed):
+    """prq_compress (k-means++ / Lloyd / smoothing / quantize) over random
+    shapes, bits, groups, stages, K and per-plane chunk indices: assignments,
+    bf16 centroids, iteration counts, payload and scales bit-exact."""
+    c, x = _compress_case(seed)
+    cfg = QuantConfig(bits=c["bits"], group_size=c["B"], stages=c["S"], centroids=c["K"])
+    dc = D.compress(torch.from_numpy(x).to(torch.bfloat16).cuda(), cfg, chunk_index=c["chunks"])
+    draws = np.stack([oracle_lib.pp_draws(0, ch, c["S"], c["K"]) for ch in c["chunks"]])
+    pay, sc, cent, asg, iters = oracle_lib.prq_compress_batch(x, c["bits"], c["B"], c["S"], c["K"], 10, 1e-4,
+                                                              draws, 16)
+    assert np.array_equal(dc.assignments.cpu().numpy(), asg), c
+    assert np.array_equal(dc.centroids.float().cpu().numpy().view(np.uint32), cent.view(np.uint32)), c
+    assert np.array_equal(dc.iters.cpu().numpy(), iters), c
+    assert np.array_equal(dc.scales.cpu().numpy(), sc), c
+    assert np.array_equal(dc.payload.cpu().numpy(), pay), c
