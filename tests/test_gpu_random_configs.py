@@ -93,3 +93,44 @@ def test_random_config_compress_vs_oracle(oracle_lib, seed):
     assert np.array_equal(dc.iters.cpu().numpy(), iters), c
     assert np.array_equal(dc.scales.cpu().numpy(), sc), c
     assert np.array_equal(dc.payload.cpu().numpy(), pay), c
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_random_attention_vs_oracle(oracle_lib, seed):
+    """Attention over a quantized cache at random head counts, query / cache /
+    current-chunk lengths (partial tiles, empty cache or empty current chunk),
+    codec configs and softmax scales, both the two-pass (decode + tcgen05
+    pipeline) and the in-tile decoder, within the fp64 oracle tolerance of
+    tests/test_gpu_attention.py (max-abs <= 2e-2 max|O|, rel-L2 <= 1e-2)."""
+    from paper_2602_02958_b200.synth import clustered_planes
+    rng = np.random.default_rng(9000 + seed)
+    H, d = int(rng.integers(1, 4)), 128
+    nq = int(rng.integers(1, 300))
+    nc = int(rng.choice([0, int(rng.integers(1, 700))]))
+    ncur = int(rng.integers(0 if nc else 1, 260))
+    cfg = QuantConfig(bits=int(rng.choice([2, 4])), group_size=int(rng.choice([32, 64])),
+                      stages=int(rng.integers(1, 3)), centroids=int(rng.choice([8, 16])))
+    fused = bool(rng.integers(0, 2))
+    scale = float(rng.choice([d ** -0.5, 0.3]))
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    q = (torch.randn((nq, H, d), generator=g, device="cuda") * 0.5).to(torch.bfloat16)
+    kc = torch.randn((ncur, H, d), generator=g, device="cuda").to(torch.bfloat16)
+    vc = torch.randn((ncur, H, d), generator=g, device="cuda").to(torch.bfloat16)
+    if nc:
+        planes = clustered_planes(2 * H, nc, d, n_clusters=8, outlier_scale=4.0, seed=seed)
+        chunks = D.compress(planes, cfg)
+        out = D.attention(q, chunks, kc, vc, scale, fused=fused)
+        deq = oracle_lib.prq_decompress_batch(chunks.payload.cpu().numpy(), chunks.scales.cpu().numpy(),
+                                              chunks.centroids.float().cpu().numpy(),
+                                              chunks.assignments.cpu().numpy(), nc, d, cfg.bits,
+                                              cfg.group_size, 8)
+        kcache, vcache = deq[0::2], deq[1::2]
+    else:
+        out = D.attention(q, None, kc, vc, scale)
+        kcache = vcache = np.zeros((H, 0, d), np.float32)
+    ref = oracle_lib.attention(q.float().cpu().numpy(), kcache, vcache, kc.float().cpu().numpy(),
+                               vc.float().cpu().numpy(), scale, 8)
+    o = out.float().cpu().numpy().astype(np.float64)
+    err = np.abs(o - ref).max() / np.abs(ref).max()
+    rl2 = np.linalg.norm(o - ref) / np.linalg.norm(ref)
+    assert err <= 2e-2 and rl2 <= 1e-2, (dict(H=H, nq=nq, nc=nc, ncur=ncur, fused=fused), err, rl2)
