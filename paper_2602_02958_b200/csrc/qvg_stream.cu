@@ -257,6 +257,16 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_stream(QuantArgs 
             const float sv = e4m3_decode_fast(code);
             const float inv = rcp_tab[code & 0x7Fu];
             const float2 inv2 = make_float2(inv, inv);
+            if (__any_sync(0xffffffffu, code == 0x7Eu)) {
+                // saturated scale (amax / QMAX > 448, e.g. outlier channels of a
+                // coarse K): the reference clips, clip(rint(r / s), +-QMAX) ==
+                // rint(clamp(r, +-QMAX s) / s), so the magic-number codes stay in
+                // range and the lane needs no exact fallback for it
+                const float lim = code == 0x7Eu ? float(QMAX) * sv : __int_as_float(0x7F800000);
+#pragma unroll
+                for (int q = 0; q < 8; q++)
+                    r[q] = make_float2(fminf(fmaxf(r[q].x, -lim), lim), fminf(fmaxf(r[q].y, -lim), lim));
+            }
             float2 yv[8];
 #pragma unroll
             for (int q = 0; q < 8; q++) yv[q] = __ffma2_rn(r[q], inv2, make_float2(MAGIC, MAGIC));
@@ -275,14 +285,14 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_stream(QuantArgs 
                     for (int k2 = 0; k2 < FPW; k2 += 2 * span) v[k2] += v[k2 + span] << (BITS * span);
                 b32.w[w] = (v[0] - magic_sum<BITS>()) ^ SIGNS;
             }
-            const bool allv = !(El < 0.125f * sv) || code == 0x7Eu;
+            const bool allv = !(El < 0.125f * sv);
             const float thr = window_thr<QMAX>(sv, inv, El);
             bool amb;
             if constexpr (QMAX == 1) {
                 // exact without a window: certified lane, s/2 a multiple of unit
                 // (its lowest set bit >= 2^(exponent(s) - 4)), s/2 < 2^22 unit
                 const float sexp = __uint_as_float(__float_as_uint(sv) & 0x7F800000u);
-                const bool fast = cert && code != 0x7Eu && sexp * 0.0625f >= un && sv < un * 4194304.f;
+                const bool fast = cert && sexp * 0.0625f >= un && sv < un * 4194304.f;
                 amb = false;
                 if (__any_sync(0xffffffffu, !fast)) {
                     const float h = 0.5f * sv;
