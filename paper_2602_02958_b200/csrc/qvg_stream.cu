@@ -517,20 +517,8 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
         int ai[SS];
 #pragma unroll
         for (int t = 0; t < S; t++) ai[t] = st[g.off_small + t * g.R + lr];
-        // every shared-memory load of the stage must have landed before the
-        // release (the producer's TMA may overwrite the stage right after it):
-        // a store of a value depending on one register of each load cannot
-        // issue before those loads complete
-        {
-            uint32_t dep = 0;
-#pragma unroll
-            for (int t = 0; t < S; t++) dep ^= uint32_t(ai[t]);
-#pragma unroll
-            for (int q = 0; q < 16; q += 2) dep ^= __float_as_uint(r[q].x);
-            reinterpret_cast<volatile uint32_t *>(rcp_sink)[threadIdx.x] = dep;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars.empty[k]);
+        // the stage is released after the scale codes: the exact-scale path
+        // below re-reads x from the ring slot (shared memory, not L2)
         // the rare exact paths re-read x from global memory (the slot may be refilled)
         const uint32_t xrow = sc.i0 + lr;
         auto xg = [&]() { return static_cast<const uint8_t *>(a.x) + (uint64_t(p) * N + xrow) * big_row + 32u * c * XB; };
@@ -604,7 +592,7 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
                                 (fabsf(r[8 * h + q].y) >= thr ? 2u << (2 * q) : 0u);
                     const uint32_t hc = h == 0 ? hlo : hhi;
                     if (cand)
-                        a64 = fmax(a64, exact_absmax<S, XBF16>(xg() + hc * XB, tab, pitch, soff + hc, int(KK), ai[0],
+                        a64 = fmax(a64, exact_absmax<S, XBF16>(xr + hc * XB, tab, pitch, soff + hc, int(KK), ai[0],
                                                                ai[SS > 1 ? 1 : 0], ai[SS > 2 ? 2 : 0],
                                                                ai[SS > 3 ? 3 : 0], cand));
                 }
@@ -612,6 +600,21 @@ __global__ void __launch_bounds__(32 * (CW + 1), 1) k_quantize_ring32(QuantArgs 
             for (int m = 1; m < glanes; m <<= 1) a64 = fmax(a64, shfl_xor_d(a64, m));
             if (camb) code = a64 == 0.0 ? 0x38u : e4m3_encode_up(__ddiv_rn(a64, double(QMAX)));
         }
+        // every shared-memory load of the stage must have landed before the
+        // release (the producer's TMA may overwrite the stage right after it):
+        // a store of a value depending on one register of each load (x, the
+        // assignments, and through `code` the exact-scale re-reads) cannot
+        // issue before those loads complete
+        {
+            uint32_t dep = code;
+#pragma unroll
+            for (int t = 0; t < S; t++) dep ^= uint32_t(ai[t]);
+#pragma unroll
+            for (int q = 0; q < 16; q += 2) dep ^= __float_as_uint(r[q].x);
+            reinterpret_cast<volatile uint32_t *>(rcp_sink)[threadIdx.x] = dep;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars.empty[k]);
         // ---- codes (slot order), fixed up per 16-field half, stored in channel order
         const float sv = e4m3_decode_fast(code);
         const float inv = rcp_tab[code & 0x7Fu];
