@@ -7,7 +7,10 @@ of 4, head_dims other than 128 / 256, K up to 256 with tables at the shared-
 memory budget edge), and bf16 planes with outlier channels, tiny entries,
 exact zeros and exactly representable ties (values on a coarse grid), so the
 certificates, the window tests, the exact-scale and exact-code fallbacks and
-the Fast2Sum add-back checks all run.  Seeds are fixed: failures reproduce."""
+the Fast2Sum add-back checks all run.  Seeds are fixed: failures reproduce.
+QVG_RANDOM_SCALE=k multiplies the case counts (soak runs)."""
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -18,7 +21,8 @@ from paper_2602_02958_b200 import device as D  # noqa: E402
 from paper_2602_02958_b200.qvgcodec.lowprec import round_to_bf16  # noqa: E402
 from paper_2602_02958_b200.qvgcodec.types import QuantConfig  # noqa: E402
 
-N_CASES = 150
+SCALE = int(os.environ.get("QVG_RANDOM_SCALE", "1"))
+N_CASES = 150 * SCALE
 
 
 def _case(seed):
@@ -77,7 +81,7 @@ def _compress_case(seed):
     return dict(P=P, N=N, d=d, bits=bits, B=B, S=S, K=K, chunks=chunks), x
 
 
-@pytest.mark.parametrize("seed", range(80))
+@pytest.mark.parametrize("seed", range(80 * SCALE))
 def test_random_config_compress_vs_oracle(oracle_lib, seed):
     """prq_compress (k-means++ / Lloyd / smoothing / quantize) over random
     shapes, bits, groups, stages, K and per-plane chunk indices: assignments,
@@ -95,13 +99,21 @@ def test_random_config_compress_vs_oracle(oracle_lib, seed):
     assert np.array_equal(dc.payload.cpu().numpy(), pay), c
 
 
-@pytest.mark.parametrize("seed", range(60))
+@pytest.mark.parametrize("seed", range(60 * SCALE))
 def test_random_attention_vs_oracle(oracle_lib, seed):
     """Attention over a quantized cache at random head counts, query / cache /
     current-chunk lengths (partial tiles, empty cache or empty current chunk),
     codec configs and softmax scales, both the two-pass (decode + tcgen05
-    pipeline) and the in-tile decoder, within the fp64 oracle tolerance of
-    tests/test_gpu_attention.py (max-abs <= 2e-2 max|O|, rel-L2 <= 1e-2)."""
+    pipeline) and the in-tile decoder.  Both attend over the bf16 rounding of
+    the reconstruction (the operand precision of the tensor-core path), so the
+    fp64 oracle over that rounding is the tight reference (max-abs <= 1e-2
+    max|O|, rel-L2 <= 5e-3: bf16 P and output); at the model's softmax scale
+    d^-1/2 the result is also held to SURVEY 8(c)'s tolerance against the
+    oracle over the f32 reconstruction (max-abs <= 2e-2 max|O|, rel-L2 <=
+    1e-2).  At the sharper scale 0.3 the bf16 rounding of the cached keys moves
+    the logits by up to 3.4x more and that second bound is not the kernel's
+    to meet (soak: 3 of 3 600 cases at 1.7-2.5e-2 max-abs, all <= 3.2e-3
+    against the bf16 reconstruction; tools/diag_attn_seed.py)."""
     from paper_2602_02958_b200.synth import clustered_planes
     rng = np.random.default_rng(9000 + seed)
     H, d = int(rng.integers(1, 4)), 128
@@ -124,13 +136,17 @@ def test_random_attention_vs_oracle(oracle_lib, seed):
                                               chunks.centroids.float().cpu().numpy(),
                                               chunks.assignments.cpu().numpy(), nc, d, cfg.bits,
                                               cfg.group_size, 8)
-        kcache, vcache = deq[0::2], deq[1::2]
     else:
         out = D.attention(q, None, kc, vc, scale)
-        kcache = vcache = np.zeros((H, 0, d), np.float32)
-    ref = oracle_lib.attention(q.float().cpu().numpy(), kcache, vcache, kc.float().cpu().numpy(),
-                               vc.float().cpu().numpy(), scale, 8)
+        deq = np.zeros((2 * H, 0, d), np.float32)
     o = out.float().cpu().numpy().astype(np.float64)
-    err = np.abs(o - ref).max() / np.abs(ref).max()
-    rl2 = np.linalg.norm(o - ref) / np.linalg.norm(ref)
-    assert err <= 2e-2 and rl2 <= 1e-2, (dict(H=H, nq=nq, nc=nc, ncur=ncur, fused=fused), err, rl2)
+    args = (q.float().cpu().numpy(), kc.float().cpu().numpy(), vc.float().cpu().numpy())
+    case = dict(H=H, nq=nq, nc=nc, ncur=ncur, fused=fused, scale=scale)
+    for dq, tol, rtol in ((round_to_bf16(deq).astype(np.float32), 1e-2, 5e-3),
+                          (deq, 2e-2, 1e-2) if scale == d ** -0.5 else (None, 0, 0)):
+        if dq is None:
+            continue
+        ref = oracle_lib.attention(args[0], dq[0::2], dq[1::2], args[1], args[2], scale, 8)
+        err = np.abs(o - ref).max() / np.abs(ref).max()
+        rl2 = np.linalg.norm(o - ref) / np.linalg.norm(ref)
+        assert err <= tol and rl2 <= rtol, (case, tol, err, rl2)
