@@ -820,6 +820,129 @@ __global__ void __launch_bounds__(256) k_obj_leaves(ObjArgs a) {
     }
 }
 
+// K4 leaves over bf16 planes (d >= 128, a power of two), one CTA per plane,
+// one thread per leaf: the plane's float64 centroid table and bf16 stage-1
+// table are staged in shared memory (rows padded by 16 bytes, so the lanes'
+// 16-byte reads of unrelated rows spread over the banks), numpy's eight
+// accumulators r[0..7] live in registers, and each step of 8 consecutive
+// elements (leaf offsets are multiples of 8, so a step never crosses a row)
+// is one 16-byte load of x plus shared-memory reads -- the same float64
+// operations in the same order as k_obj_leaves' 8-lane groups (r[j]
+// sequential over the steps, then ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then
+// the tail).  k_obj_leaves' global-memory version was bound by L1 wavefronts
+// of the per-lane centroid-row reads.
+constexpr int kObjThreads = 512;
+
+__device__ __forceinline__ void bf16x8(uint4 w, float f[8]) {
+    const uint32_t v[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        f[2 * i] = __uint_as_float(v[i] << 16);
+        f[2 * i + 1] = __uint_as_float(v[i] & 0xFFFF0000u);
+    }
+}
+
+static size_t obj_plane_smem(int K, int d, bool c1) {
+    return size_t(K) * (size_t(d) * 8 + 16) + (c1 ? size_t(K) * (size_t(d) * 2 + 16) : 0);
+}
+
+__global__ void __launch_bounds__(kObjThreads, 2) k_obj_plane(ObjArgs a) {
+    extern __shared__ __align__(16) uint8_t osm[];
+    const int64_t p = blockIdx.x;
+    if (a.mode == 1 && a.st[p].done) return;
+    const int d = a.d, K = a.K;
+    const int cp = d * 8 + 16, bp = d * 2 + 16;       // padded row pitches (bytes)
+    uint8_t *sc = osm, *sb = osm + size_t(K) * cp;
+    const uint16_t *c1p = a.bf.c1 ? a.bf.c1 + p * a.bf.c1_stride : nullptr;
+    const uint8_t *a1p = a.bf.c1 ? a.bf.a1 + p * a.bf.a1_stride : nullptr;
+    {
+        const uint4 *cg = reinterpret_cast<const uint4 *>(a.cent + p * int64_t(K) * d);
+        const int per = d / 2;                        // 16-byte words per f64 row
+        for (int i = threadIdx.x; i < K * per; i += blockDim.x)
+            *reinterpret_cast<uint4 *>(sc + (i / per) * cp + (i % per) * 16) = cg[i];
+        if (c1p) {
+            const uint4 *bg = reinterpret_cast<const uint4 *>(c1p);
+            const int pb = d / 8;
+            for (int i = threadIdx.x; i < K * pb; i += blockDim.x)
+                *reinterpret_cast<uint4 *>(sb + (i / pb) * bp + (i % pb) * 16) = bg[i];
+        }
+    }
+    __syncthreads();
+    const int32_t *asg = a.assign + p * a.N;
+    const uint16_t *xp = a.bf.x16 + p * a.N * d;
+    const int n_nodes = 2 * a.n_leaves - 1;
+    auto elem1 = [&](int64_t e) {
+        const int64_t row = e >> a.lgd;
+        const int col = int(e & (d - 1));
+        double v = double(__uint_as_float(uint32_t(xp[e]) << 16));
+        if (c1p) v = __dsub_rn(v, double(__uint_as_float(uint32_t(
+                                    *reinterpret_cast<const uint16_t *>(sb + a1p[row] * bp + col * 2)) << 16)));
+        const double t = __dsub_rn(v, *reinterpret_cast<const double *>(sc + asg[row] * cp + col * 8));
+        return __dmul_rn(t, t);
+    };
+    for (int L = threadIdx.x; L < a.n_leaves; L += blockDim.x) {
+        const int64_t off = a.lf_off[L];
+        const int len = a.lf_len[L];
+        double s;
+        if (len < 8 || (off & 7) != 0) {
+            s = 0.0;
+            if (len < 8) {
+                for (int k = 0; k < len; k++) s = __dadd_rn(s, elem1(off + k));
+            } else {
+                const int m = len >> 3;
+                double r[8];
+                for (int k = 0; k < 8; k++) r[k] = elem1(off + k);
+                for (int i = 1; i < m; i++)
+                    for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], elem1(off + 8 * i + k));
+                s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                              __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+                for (int k = m * 8; k < len; k++) s = __dadd_rn(s, elem1(off + k));
+            }
+        } else {
+            const int64_t r0 = off >> a.lgd, r1 = (off + len - 1) >> a.lgd;   // a leaf spans <= 2 rows
+            const uint8_t *ce0 = sc + asg[r0] * cp, *ce1 = sc + asg[r1] * cp;
+            const uint8_t *cb0 = c1p ? sb + a1p[r0] * bp : nullptr, *cb1 = c1p ? sb + a1p[r1] * bp : nullptr;
+            auto elem8 = [&](int64_t e, double v[8]) {
+                const bool first = (e >> a.lgd) == r0;
+                const int col = int(e & (d - 1));
+                float xf[8];
+                bf16x8(*reinterpret_cast<const uint4 *>(xp + e), xf);
+                double xv[8];
+#pragma unroll
+                for (int k = 0; k < 8; k++) xv[k] = double(xf[k]);
+                if (c1p) {
+                    float cf[8];
+                    bf16x8(*reinterpret_cast<const uint4 *>((first ? cb0 : cb1) + col * 2), cf);
+#pragma unroll
+                    for (int k = 0; k < 8; k++) xv[k] = __dsub_rn(xv[k], double(cf[k]));
+                }
+                const double2 *ce = reinterpret_cast<const double2 *>((first ? ce0 : ce1) + col * 8);
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const double2 c = ce[k];
+                    const double t0 = __dsub_rn(xv[2 * k], c.x), t1 = __dsub_rn(xv[2 * k + 1], c.y);
+                    v[2 * k] = __dmul_rn(t0, t0);
+                    v[2 * k + 1] = __dmul_rn(t1, t1);
+                }
+            };
+            const int m = len >> 3;
+            double r[8];
+            elem8(off, r);
+#pragma unroll 2
+            for (int i = 1; i < m; i++) {
+                double v[8];
+                elem8(off + 8 * i, v);
+#pragma unroll
+                for (int k = 0; k < 8; k++) r[k] = __dadd_rn(r[k], v[k]);
+            }
+            s = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                          __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+            for (int k = m * 8; k < len; k++) s = __dadd_rn(s, elem1(off + k));
+        }
+        a.nodes[p * n_nodes + L] = s;
+    }
+}
+
 __global__ void __launch_bounds__(1024) k_obj_combine(ObjArgs a) {
     const int64_t p = blockIdx.x;
     if (a.mode == 1 && a.st[p].done) return;
@@ -917,9 +1040,18 @@ static void objective(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K
     ObjArgs o{bf_src(b), b.rows, b.rows32_valid ? b.rows32 : nullptr, b.rows32_ok, b.cent, b.assign, b.nodes, b.st,
               b.ob_off, b.ob_len, b.nd_l, b.nd_r, b.h_start, b.ob_leaves, b.ob_heights, N, d, K, mode, tol,
               lgd};
-    dim3 g((unsigned)((int64_t(b.ob_leaves) * 8 + 255) / 256 < 4096 ? (int64_t(b.ob_leaves) * 8 + 255) / 256 : 4096),
-           (unsigned)P);
-    k_obj_leaves<<<g, 256, 0, st>>>(o);
+    static const bool staged = [] { const char *e = getenv("QVG_OBJ_THREAD"); return !e || atoi(e) != 0; }();
+    const size_t osm = obj_plane_smem(K, d, o.bf.c1 != nullptr);
+    if (staged && o.bf.x16 && lgd >= 7 && osm <= 110 * 1024 && (!o.bf.c1 || o.bf.c1_stride % 8 == 0) &&
+        (reinterpret_cast<uintptr_t>(o.bf.x16) & 15) == 0 && (reinterpret_cast<uintptr_t>(o.bf.c1) & 15) == 0 &&
+        (reinterpret_cast<uintptr_t>(o.cent) & 15) == 0) {
+        cudaFuncSetAttribute(k_obj_plane, cudaFuncAttributeMaxDynamicSharedMemorySize, int(osm));
+        k_obj_plane<<<(unsigned)P, kObjThreads, osm, st>>>(o);
+    } else {
+        dim3 g((unsigned)((int64_t(b.ob_leaves) * 8 + 255) / 256 < 4096 ? (int64_t(b.ob_leaves) * 8 + 255) / 256 : 4096),
+               (unsigned)P);
+        k_obj_leaves<<<g, 256, 0, st>>>(o);
+    }
     k_obj_combine<<<(unsigned)P, 1024, 0, st>>>(o);
 }
 
