@@ -114,6 +114,24 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float v[32]) {
     for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
 }
 
+// the kAcc accumulator chunks of 32 columns with one wait (the loads overlap)
+__device__ __forceinline__ void tmem_ld32x4(uint32_t taddr, uint32_t stride, float v[4][32]) {
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        uint32_t *r = reinterpret_cast<uint32_t *>(v[c]);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+              "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+              "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+              "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr + c * stride));
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
 // x = hi + mid + lo (+ <= 2^-24 |x|), each RN to bf16 (bits)
 __device__ __forceinline__ void split3(double x, uint16_t &hi, uint16_t &mid, uint16_t &lo) {
     const __nv_bfloat16 h = __double2bfloat16(x);
@@ -191,6 +209,7 @@ struct TcArgs {
     const PlaneState *st;      // skip converged planes (nullable)
     int64_t P, N;
     int K, T, skip_done;
+    int a_one;                 // rows exactly bf16 (stage 1 of a bf16 chunk): splits 1, 2 are zero
 };
 
 // smem: A tiles (3 x 32 KB) | B tiles (3 x kNB x 128 bf16 = 96 KB) | c2, cnorm
@@ -249,8 +268,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_assign_tc(TcArgs a) {
     // transfer overlaps the epilogue
     auto load_tile = [&](int64_t item) {
         if (tid == 0 && item < it1) {
-            expect_tx(&bar_a, uint32_t(kSmemA));
-            bulk_g2s(sA, reinterpret_cast<const uint8_t *>(a.split) + size_t(item) * kSmemA, uint32_t(kSmemA), &bar_a);
+            // bf16-exact rows: only the hi split is nonzero (a third of the bytes)
+            const uint32_t nbytes = a.a_one ? uint32_t(kTileB) : uint32_t(kSmemA);
+            expect_tx(&bar_a, nbytes);
+            bulk_g2s(sA, reinterpret_cast<const uint8_t *>(a.split) + size_t(item) * kSmemA, nbytes, &bar_a);
         }
     };
     int64_t it = next_item(it0);
@@ -313,7 +334,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_assign_tc(TcArgs a) {
             if (tid == 0) {
                 fence_after();
                 const uint32_t id = idesc(uint32_t(nbp));
-                const int prod[6][2] = {{0, 0}, {0, 1}, {1, 0}, {0, 2}, {2, 0}, {1, 1}};
+                // bf16-exact rows (a_one): the products of the zero A splits (1, 0),
+                // (2, 0), (1, 1) vanish exactly and are skipped; order kept otherwise
+                const int prod6[6][2] = {{0, 0}, {0, 1}, {1, 0}, {0, 2}, {2, 0}, {1, 1}};
+                const int prod3[6][2] = {{0, 0}, {0, 1}, {0, 2}, {0, 0}, {0, 0}, {0, 0}};
+                const int (*prod)[2] = a.a_one ? prod3 : prod6;
+                const int npr = a.a_one ? 3 : 6;
 #pragma unroll
                 for (int q = 0; q < kAcc; q++) {
                     int first = 1;
@@ -322,6 +348,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_assign_tc(TcArgs a) {
                         const int k = (q * 2 + ks) * 16;
 #pragma unroll
                         for (int pr = 0; pr < 6; pr++) {
+                            if (pr >= npr) break;
                             const uint64_t ad = sdesc(su32(sA + prod[pr][0] * kTileB + kmaj_off(0, k)));
                             const uint64_t bd = sdesc(su32(sB + prod[pr][1] * (kNB * kD * 2) + kmaj_off(0, k)));
                             mma(tmem + q * kNB, ad, bd, id, first ? 0u : 1u);
@@ -337,14 +364,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_assign_tc(TcArgs a) {
             if (blk == nblk - 1) load_tile(it_next);     // sA no longer read by this item's MMAs
             // ---- epilogue: 32 centroids at a time
             for (int c0 = 32 * hh; c0 < nb; c0 += 64) {
-                float cr[32], tmp[32];
-                tmem_ld32(tmem + t_lane + c0, cr);
+                static_assert(kAcc == 4, "tmem_ld32x4 loads four accumulators");
+                float acc[4][32];
+                tmem_ld32x4(tmem + t_lane + c0, kNB, acc);
+                float cr[32];
 #pragma unroll
-                for (int q = 1; q < kAcc; q++) {
-                    tmem_ld32(tmem + t_lane + q * kNB + c0, tmp);
-#pragma unroll
-                    for (int i = 0; i < 32; i++) cr[i] += tmp[i];
-                }
+                for (int i = 0; i < 32; i++) cr[i] = ((acc[0][i] + acc[1][i]) + acc[2][i]) + acc[3][i];
                 const int nn = min(32, nb - c0);
                 // certified argmin in f32 with directed rounding: D = c2f - 2 cross (one
                 // rounding), E = 2^-15 |x||c| + 2^-22 (|c2f| + 2 |cross|) covers the split /
@@ -468,11 +493,14 @@ int launch_split_rows(const double *rows, uint16_t *split, float *xnorm, float *
 
 int launch_assign_tc(const uint16_t *split, const float *xnorm, const double *rows, const double *cent,
                      const double *c2, int32_t *assign, int32_t *recheck, int32_t *n_recheck,
-                     const PlaneState *st_planes, int skip_done, int64_t P, int64_t N, int K, cudaStream_t st) {
+                     const PlaneState *st_planes, int skip_done, int64_t P, int64_t N, int K, int a_one,
+                     cudaStream_t st) {
     using namespace atc;
     const int T = int((N + kM - 1) / kM);
     cudaMemsetAsync(n_recheck, 0, sizeof(int32_t), st);
-    TcArgs ta{split, xnorm, cent, c2, assign, recheck, n_recheck, st_planes, P, N, K, T, skip_done};
+    static const bool one_ok = [] { const char *e = getenv("QVG_ASSIGN_ONE"); return !e || atoi(e) != 0; }();
+    TcArgs ta{split, xnorm, cent, c2, assign, recheck, n_recheck, st_planes, P, N, K, T, skip_done,
+              (a_one && one_ok) ? 1 : 0};
     cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem));
     const int64_t items = P * T;
     const int grid = int(items < 148 ? items : 148);

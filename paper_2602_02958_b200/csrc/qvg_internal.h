@@ -79,7 +79,8 @@ int launch_split_rows(const double *rows, uint16_t *split, float *xnorm, float *
                       int64_t P, int64_t N, cudaStream_t st);
 int launch_assign_tc(const uint16_t *split, const float *xnorm, const double *rows, const double *cent,
                      const double *c2, int32_t *assign, int32_t *recheck, int32_t *n_recheck,
-                     const PlaneState *st_planes, int skip_done, int64_t P, int64_t N, int K, cudaStream_t st);
+                     const PlaneState *st_planes, int skip_done, int64_t P, int64_t N, int K, int a_one,
+                     cudaStream_t st);
 
 // qvg_attn.cu
 size_t attention_workspace_size(int64_t nq, int64_t n_cache, int64_t n_cur, int H, int d,

@@ -1073,7 +1073,7 @@ static void assign_step(const KMeansBuffers &b, int64_t P, int64_t N, int d, int
         const int64_t n8 = P * K * 8;
         k_c2<<<unsigned((n8 + 255) / 256), 256, 0, st>>>(b.cent, b.c2, b.st, skip, P, d, K);
         launch_assign_tc(b.rsplit, b.xnorm, b.rows, b.cent, b.c2, b.assign, b.recheck, b.n_recheck, b.st, skip,
-                         P, N, K, st);
+                         P, N, K, b.src16 != nullptr, st);
         return;
     }
     AssignArgs aa{b.rows, b.cent, b.assign, b.st, N, d, K, skip};
