@@ -147,8 +147,12 @@ __device__ __forceinline__ void split3(double x, uint16_t &hi, uint16_t &mid, ui
 // ---------------------------------------------------------------------------
 // rows [P][N][128] f64 -> [P][T][3][128x128 UMMA tile] bf16 + row norms
 // ---------------------------------------------------------------------------
-__global__ void k_split_rows(const double *rows, uint16_t *split, float *xnorm, float *rows32, int32_t *rows32_ok,
-                             int64_t P, int64_t N, int T) {
+// x16 (optional): the bf16 input when the rows are exactly it (stage 1 of a bf16
+// chunk) -- read instead of the float64 rows (a quarter of the bytes); the mid /
+// lo splits are then zero and are written only when write_lo (the assignment
+// kernel reads them unless it runs in its hi-split-only mode)
+__global__ void k_split_rows(const double *rows, const uint16_t *x16, int write_lo, uint16_t *split, float *xnorm,
+                             float *rows32, int32_t *rows32_ok, int64_t P, int64_t N, int T) {
     // one thread = 8 channels (one 16-byte chunk of the tile) of one row
     const int64_t total = P * int64_t(T) * kM * (kD / 8);
     for (int64_t e = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; e < total; e += int64_t(gridDim.x) * blockDim.x) {
@@ -161,7 +165,27 @@ __global__ void k_split_rows(const double *rows, uint16_t *split, float *xnorm, 
         const int64_t row = int64_t(t) * kM + r;
         uint16_t v[kSplit][8];
         double ss = 0.0;
-        if (row < N) {
+        if (row < N && x16) {
+            const uint4 w = *reinterpret_cast<const uint4 *>(x16 + (p * N + row) * kD + ch * 8);
+            const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+            float f[8];
+#pragma unroll
+            for (int h = 0; h < 4; h++) {
+                v[0][2 * h] = uint16_t(u[h] & 0xFFFFu);
+                v[0][2 * h + 1] = uint16_t(u[h] >> 16);
+                f[2 * h] = __uint_as_float(u[h] << 16);
+                f[2 * h + 1] = __uint_as_float(u[h] & 0xFFFF0000u);
+            }
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                const double x = double(f[k]);
+                ss = fma(x, x, ss);
+                v[1][k] = v[2][k] = 0;
+            }
+            float4 *dst32 = reinterpret_cast<float4 *>(rows32 + (p * N + row) * kD + ch * 8);
+            dst32[0] = make_float4(f[0], f[1], f[2], f[3]);
+            dst32[1] = make_float4(f[4], f[5], f[6], f[7]);
+        } else if (row < N) {
             const double *src = rows + (p * N + row) * kD + ch * 8;
             float f[8];
             bool exact = true;
@@ -182,8 +206,10 @@ __global__ void k_split_rows(const double *rows, uint16_t *split, float *xnorm, 
             for (int k = 0; k < 8; k++) v[0][k] = v[1][k] = v[2][k] = 0;
         }
         uint8_t *tile = reinterpret_cast<uint8_t *>(split) + pt * (kSplit * size_t(kTileB));
+        const int ns = (x16 && !write_lo) ? 1 : kSplit;
 #pragma unroll
         for (int s = 0; s < kSplit; s++) {
+            if (s >= ns) break;
             uint4 w;
             w.x = uint32_t(v[s][0]) | (uint32_t(v[s][1]) << 16);
             w.y = uint32_t(v[s][2]) | (uint32_t(v[s][3]) << 16);
@@ -480,14 +506,21 @@ size_t assign_tc_split_elems(int64_t P, int64_t N) {
 
 bool assign_tc_ok(int d, int K) { return d == atc::kD && K >= 1 && K <= 256; }
 
-int launch_split_rows(const double *rows, uint16_t *split, float *xnorm, float *rows32, int32_t *rows32_ok,
-                      int64_t P, int64_t N, cudaStream_t st) {
+static bool assign_one_enabled() {
+    static const bool v = [] { const char *e = getenv("QVG_ASSIGN_ONE"); return !e || atoi(e) != 0; }();
+    return v;
+}
+
+int launch_split_rows(const double *rows, const uint16_t *x16, uint16_t *split, float *xnorm, float *rows32,
+                      int32_t *rows32_ok, int64_t P, int64_t N, cudaStream_t st) {
     const int T = int((N + atc::kM - 1) / atc::kM);
     cudaMemsetAsync(rows32_ok, 1, size_t(P) * sizeof(int32_t), st);      // nonzero = exact until shown otherwise
     const int64_t total = P * T * atc::kM * (atc::kD / 8);
     int64_t g = (total + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
-    atc::k_split_rows<<<unsigned(g), 256, 0, st>>>(rows, split, xnorm, rows32, rows32_ok, P, N, T);
+    const bool xs = x16 && (reinterpret_cast<uintptr_t>(x16) & 15) == 0;
+    atc::k_split_rows<<<unsigned(g), 256, 0, st>>>(rows, xs ? x16 : nullptr, assign_one_enabled() ? 0 : 1, split, xnorm,
+                                                  rows32, rows32_ok, P, N, T);
     return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
 }
 
@@ -498,9 +531,8 @@ int launch_assign_tc(const uint16_t *split, const float *xnorm, const double *ro
     using namespace atc;
     const int T = int((N + kM - 1) / kM);
     cudaMemsetAsync(n_recheck, 0, sizeof(int32_t), st);
-    static const bool one_ok = [] { const char *e = getenv("QVG_ASSIGN_ONE"); return !e || atoi(e) != 0; }();
     TcArgs ta{split, xnorm, cent, c2, assign, recheck, n_recheck, st_planes, P, N, K, T, skip_done,
-              (a_one && one_ok) ? 1 : 0};
+              (a_one && assign_one_enabled()) ? 1 : 0};
     cudaFuncSetAttribute(k_assign_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kSmem));
     const int64_t items = P * T;
     const int grid = int(items < 148 ? items : 148);

@@ -75,8 +75,8 @@ int run_add_back(const double *residual, const uint16_t *cent, const uint8_t *as
 // qvg_assign_tc.cu
 size_t assign_tc_split_elems(int64_t P, int64_t N);
 bool assign_tc_ok(int d, int K);
-int launch_split_rows(const double *rows, uint16_t *split, float *xnorm, float *rows32, int32_t *rows32_ok,
-                      int64_t P, int64_t N, cudaStream_t st);
+int launch_split_rows(const double *rows, const uint16_t *x16, uint16_t *split, float *xnorm, float *rows32,
+                      int32_t *rows32_ok, int64_t P, int64_t N, cudaStream_t st);
 int launch_assign_tc(const uint16_t *split, const float *xnorm, const double *rows, const double *cent,
                      const double *c2, int32_t *assign, int32_t *recheck, int32_t *n_recheck,
                      const PlaneState *st_planes, int skip_done, int64_t P, int64_t N, int K, int a_one,

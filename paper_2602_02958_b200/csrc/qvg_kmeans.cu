@@ -1141,7 +1141,7 @@ static void lloyd_body(const KMeansBuffers &b, int64_t P, int64_t N, int d, int 
 static int split_rows(KMeansBuffers &b, int64_t P, int64_t N, cudaStream_t st) {
     b.rows32_valid = 0;
     if (b.rsplit && assign_tc_enabled()) {
-        if (launch_split_rows(b.rows, b.rsplit, b.xnorm, b.rows32, b.rows32_ok, P, N, st)) return QVG_ERR_CUDA;
+        if (launch_split_rows(b.rows, b.src16, b.rsplit, b.xnorm, b.rows32, b.rows32_ok, P, N, st)) return QVG_ERR_CUDA;
         b.rows32_valid = 1;
     }
     return QVG_OK;
