@@ -248,7 +248,7 @@ int qvg_compress(const void *x, int32_t x_dtype, int64_t P, int64_t N, int32_t d
             rc = run_kmeans_stage(b, P, N, d, K, cfg->kmeans_max_iters, cfg->kmeans_tol,
                                   warm ? nullptr : pp_draws + int64_t(t) * K, int64_t(S) * K, warm, st);
             if (rc) return set_err(rc, "k-means stage %d: %s", t, cudaGetErrorString(cudaGetLastError()));
-            rc = finalize_stage(b, P, N, d, K, S, t, centroids, centroids_f64, assign, iters, st);
+            rc = finalize_stage(b, P, N, d, K, S, t, centroids, centroids_f64, assign, iters, st, t + 1 < S);
             if (rc) return set_err(rc, "stage finalize failed");
         }
     }

@@ -68,7 +68,7 @@ int run_assign(const double *rows, const double *cent, int32_t *assign, int64_t 
                int K, cudaStream_t st);
 int finalize_stage(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int S, int t,
                    uint16_t *cent_out, double *cent64_out, uint8_t *assign_out, int32_t *iters_out,
-                   cudaStream_t st);
+                   cudaStream_t st, bool update_rows = true);
 int run_add_back(const double *residual, const uint16_t *cent, const uint8_t *assign, int64_t P,
                  int64_t N, int d, int K, double *out, cudaStream_t st);
 

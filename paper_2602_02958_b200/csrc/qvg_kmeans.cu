@@ -987,9 +987,12 @@ __global__ void k_finalize_cent(const double *cent, uint16_t *cent_out, double *
     }
 }
 
+// update_rows = 0: only the u8 assignments / iteration counts (the last stage of
+// prq_compress: its residual is never read -- the quantizer works from x and the
+// tables)
 __global__ void k_residual(double *rows, const double *cent, const int32_t *assign,
                            uint8_t *assign_out, int32_t *iters_out, const PlaneState *st,
-                           int64_t P, int64_t N, int S, int t, int K, int d) {
+                           int64_t P, int64_t N, int S, int t, int K, int d, int update_rows) {
     // grid.y = plane, one row per 32-thread group (no 64-bit divisions per element)
     const int64_t p = blockIdx.y;
     double *pr = rows + p * N * d;
@@ -1001,7 +1004,7 @@ __global__ void k_residual(double *rows, const double *cent, const int32_t *assi
         const int c = pa[row];
         const double *cr = pc + int64_t(c) * d;
         double *rr = pr + row * d;
-        for (int col = lane; col < d; col += 32) {
+        for (int col = lane; update_rows && col < d; col += 32) {
             const float cb = bf16_to_f32(f32_to_bf16_bits_rne(__double2float_rn(cr[col])));
             rr[col] = __dsub_rn(rr[col], double(cb));
         }
@@ -1218,11 +1221,11 @@ int run_add_back(const double *residual, const uint16_t *cent, const uint8_t *as
 
 int finalize_stage(const KMeansBuffers &b, int64_t P, int64_t N, int d, int K, int S, int t,
                    uint16_t *cent_out, double *cent64_out, uint8_t *assign_out, int32_t *iters_out,
-                   cudaStream_t st) {
+                   cudaStream_t st, bool update_rows) {
     k_finalize_cent<<<g1d(P * K * d, 256), 256, 0, st>>>(b.cent, cent_out, cent64_out, P, S, t, K, d);
     const int64_t rb = (N + 7) / 8;                       // 8 rows per 256-thread CTA
     k_residual<<<dim3(unsigned(rb < 4096 ? rb : 4096), unsigned(P)), 256, 0, st>>>(
-        b.rows, b.cent, b.assign, assign_out, iters_out, b.st, P, N, S, t, K, d);
+        b.rows, b.cent, b.assign, assign_out, iters_out, b.st, P, N, S, t, K, d, update_rows ? 1 : 0);
     return cudaGetLastError() == cudaSuccess ? QVG_OK : QVG_ERR_CUDA;
 }
 
