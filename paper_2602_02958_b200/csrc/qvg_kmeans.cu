@@ -669,6 +669,8 @@ __global__ void __launch_bounds__(128) k_sums(SumArgs a) {
 struct RepairArgs {
     const double *rows;
     double *cent;
+    const float *rows32;        // exact float32 copy when rows32_ok[p] (half the bytes; nullable)
+    const int32_t *rows32_ok;
     int32_t *assign;
     const int32_t *counts;
     double *dist;          // [P][N] scratch
@@ -686,22 +688,28 @@ __global__ void __launch_bounds__(1024) k_repair(RepairArgs a) {
     int any = 0;
     for (int j = threadIdx.x; j < K; j += blockDim.x) any |= cnt[j] == 0;
     if (!__syncthreads_or(any)) return;
-    const double *rows = a.rows + p * N * d;
     double *cent = a.cent + p * int64_t(K) * d;
     int32_t *asg = a.assign + p * N;
     double *dist = a.dist + p * N;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, j8 = lane & 7;
-    for (int64_t i0 = int64_t(warp) * 4; i0 < N; i0 += blockDim.x >> 3) {    // warp-uniform
-        const int64_t i = i0 + (lane >> 3);
-        const int64_t ii = i < N ? i : N - 1;
-        const double *ri = rows + ii * d;
-        const double *ci = cent + int64_t(asg[ii]) * d;
-        double s = row_pairwise8(d, j8, [&](int k) {
-            double t = __dsub_rn(ri[k], ci[k]);
-            return __dmul_rn(t, t);
-        });
-        if (j8 == 0 && i < N) dist[i] = __dadd_rn(0.0, s);
-    }
+    // a CTA streams its whole plane here (one SM's share of HBM), so the exact
+    // float32 copy of the rows is read when there is one: identical values
+    const bool r32 = a.rows32 && a.rows32_ok[p];
+    auto pass = [&](auto rowp) {
+        for (int64_t i0 = int64_t(warp) * 4; i0 < N; i0 += blockDim.x >> 3) {    // warp-uniform
+            const int64_t i = i0 + (lane >> 3);
+            const int64_t ii = i < N ? i : N - 1;
+            const auto ri = rowp + ii * d;
+            const double *ci = cent + int64_t(asg[ii]) * d;
+            double s = row_pairwise8(d, j8, [&](int k) {
+                double t = __dsub_rn(double(ri[k]), ci[k]);
+                return __dmul_rn(t, t);
+            });
+            if (j8 == 0 && i < N) dist[i] = __dadd_rn(0.0, s);
+        }
+    };
+    if (r32) pass(a.rows32 + p * N * d);
+    else pass(a.rows + p * N * d);
     __syncthreads();
     __shared__ double wv[32];
     __shared__ int64_t wi[32];
@@ -732,7 +740,8 @@ __global__ void __launch_bounds__(1024) k_repair(RepairArgs a) {
         }
         __syncthreads();
         const int64_t r = s_r;
-        for (int k = tid; k < d; k += blockDim.x) cent[int64_t(j) * d + k] = rows[r * d + k];
+        for (int k = tid; k < d; k += blockDim.x)
+            cent[int64_t(j) * d + k] = r32 ? double(a.rows32[(p * N + r) * d + k]) : a.rows[(p * N + r) * d + k];
         __syncthreads();
     }
 }
@@ -1134,7 +1143,7 @@ static void lloyd_body(const KMeansBuffers &b, int64_t P, int64_t N, int d, int 
     k_members<<<(unsigned)P, 1024, msmem, st>>>(ma);
     SumArgs sa{b.rows, b.rows32_valid ? b.rows32 : nullptr, b.rows32_ok, b.cent, b.counts, b.offsets, b.members, b.st, N, d, K};
     k_sums<<<dim3((unsigned)K, (unsigned)P), 128, 0, st>>>(sa);
-    RepairArgs ra{b.rows, b.cent, b.assign, b.counts, b.d2, b.st, N, d, K};
+    RepairArgs ra{b.rows, b.cent, b.rows32_valid ? b.rows32 : nullptr, b.rows32_ok, b.assign, b.counts, b.d2, b.st, N, d, K};
     k_repair<<<(unsigned)P, 1024, 0, st>>>(ra);
     objective(b, P, N, d, K, mode, tol, st);
 }
