@@ -113,7 +113,7 @@ def test_random_attention_vs_oracle(oracle_lib, seed):
     1e-2).  At the sharper scale 0.3 the bf16 rounding of the cached keys moves
     the logits by up to 3.4x more and that second bound is not the kernel's
     to meet (soak: 3 of 3 600 cases at 1.7-2.5e-2 max-abs, all <= 3.2e-3
-    against the bf16 reconstruction; tools/diag_attn_seed.py)."""
+    against the bf16 reconstruction; tests/diag_attn_seed.py)."""
     from paper_2602_02958_b200.synth import clustered_planes
     rng = np.random.default_rng(9000 + seed)
     H, d = int(rng.integers(1, 4)), 128
